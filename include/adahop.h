@@ -1,0 +1,225 @@
+/*
+ * adahop.h — C ABI of the B200-native AdaHOP MXFP4 linear (arXiv 2604.02525).
+ *
+ * Citations: P:<n> = line n of the paper's LaTeX source; the section,
+ * equation or table is named beside each one.
+ *
+ * The library computes, for one matmul C = A·B of a linear layer (P:72-79,
+ * eq:forward / eq:backward_gw / eq:backward_gx):
+ *   IHT:        C = Q(A H) · Q(H^T B)                        (eq:inner_hadamard)
+ *   OE-Left:    C = Q(A_res H) · Q(H^T B) + A_out · B        (eq:oe_left)
+ *   OE-Right:   C = Q(A H) · Q(H^T B_res) + A · B_out        (eq:oe_right)
+ *   BF16:       C = A · B in BF16                            (AdaHOP-Lv2 CC)
+ * H = blockwise normalised Walsh–Hadamard (block 32 along K); Q = MXFP4 (E2M1
+ * elements, one E8M0 scale per 32 elements along K); A_out / B_out = the top-k rows of
+ * A / columns of B chosen by FOID (variance of the first 64 elements).
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless a parameter says "host". Matrices are
+ *    row-major with an explicit leading dimension (elements).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default).
+ *    The library never allocates, frees, or synchronises on the hot path; it is
+ *    stateless apart from a per-device property cache, thread-safe, and every hot-path
+ *    call is CUDA-graph capturable (k and shapes are host values; indices stay on device).
+ *  - Ownership: the caller owns every buffer. Scratch comes from the caller's
+ *    workspace `ws` of `ws_bytes` bytes (query with adahop_workspace_bytes); it must be
+ *    256-byte aligned and must not be used by other work concurrently.
+ *  - Errors: all argument/shape checks run on the host before any launch, so an error
+ *    never leaves partial writes. A failed launch returns ADAHOP_E_CUDA. No exceptions
+ *    cross the ABI, nothing is printed, nothing aborts.
+ *  - Inputs must be finite (non-finite input is undefined behaviour).
+ *  - Shape rules: K % 32 == 0 (else ADAHOP_E_SHAPE; no padding);
+ *    had_block must be 32 (else ADAHOP_E_UNSUPPORTED); oe_k > rows/cols of the
+ *    extracted operand clamps; oe_k == 0 means "no OE"; oe_k <= 256.
+ *    Leading dimensions must keep every row 16-byte aligned.
+ */
+#ifndef ADAHOP_H_
+#define ADAHOP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADAHOP_ABI_VERSION 1
+
+typedef struct CUstream_st* adahop_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  ADAHOP_OK = 0,
+  ADAHOP_E_INVALID_ARG = 1,  /* null pointer, bad enum, bad leading dimension        */
+  ADAHOP_E_SHAPE = 2,        /* K % 32 != 0, non-positive sizes, T % 32 in wgrad     */
+  ADAHOP_E_UNSUPPORTED = 3,  /* had_block != 32, oe_k > 256, unsupported dtype       */
+  ADAHOP_E_WORKSPACE = 4,    /* ws too small or misaligned                           */
+  ADAHOP_E_CUDA = 5,         /* a CUDA launch / driver call failed                   */
+  ADAHOP_E_NO_DEVICE = 6     /* no sm_100 device (the library has no CPU fallback)   */
+} adahop_status_t;
+
+/* Outlier pattern of a tensor as fed to the matmul. */
+typedef enum { ADAHOP_PAT_NONE = 0, ADAHOP_PAT_ROW = 1, ADAHOP_PAT_COL = 2 } adahop_pattern_t;
+
+/* Strategy (tab:strategy_summary). */
+typedef enum {
+  ADAHOP_IHT = 0,
+  ADAHOP_OE_LEFT_IHT = 1,
+  ADAHOP_OE_RIGHT_IHT = 2,
+  ADAHOP_BF16 = 3
+} adahop_strategy_t;
+
+typedef enum { ADAHOP_DT_BF16 = 0, ADAHOP_DT_F32 = 1 } adahop_dtype_t;
+
+/* The three matmuls of a linear layer. */
+typedef enum { ADAHOP_PATH_FWD = 0, ADAHOP_PATH_DGRAD = 1, ADAHOP_PATH_WGRAD = 2 } adahop_path_t;
+
+typedef struct {
+  int32_t had_block;  /* Hadamard block along K; 32                         */
+  int32_t oe_k;       /* extracted rows/cols; 64; 0 = no OE          */
+  int32_t foid_probe; /* FOID probe length; 64                              */
+  int32_t level;      /* 1 = AdaHOP-Lv1, 2 = AdaHOP-Lv2                 */
+  float tau;          /* CV threshold; 2.0                                  */
+  float eps;          /* CV stabiliser; 1e-8 ("small constant")               */
+} adahop_params_t;
+
+/* ---------------------------------------------------------------- host utilities */
+
+/* Fill `p` (host) with the paper's defaults: 32, 64, 64, 1, 2.0, 1e-8. */
+void adahop_default_params(adahop_params_t* p);
+int32_t adahop_abi_version(void);
+const char* adahop_status_string(adahop_status_t s);
+
+/* tab:strategy_summary: CN,NN,CR,NR -> IHT; RN,RR -> OE-Left; RC,NC -> OE-Right;
+ * CC -> OE-Right (level 1) or BF16 (level 2). Pure host function. */
+adahop_strategy_t adahop_strategy_for_pair(adahop_pattern_t left, adahop_pattern_t right,
+                                           int32_t level);
+
+/* Majority vote over per-step patterns; ties resolve R > C > N (R9).
+ * `per_step` is a host array of n >= 1 values. Returns ADAHOP_PAT_NONE for n <= 0. */
+adahop_pattern_t adahop_majority_vote(const int32_t* per_step, int32_t n);
+
+/* Classification rule of App. A on already-reduced CVs (host, pure):
+ * ROW if cv_col > tau, COL if cv_row > tau, larger wins when both, tie -> ROW.
+ * DESIGN.md R7: the raw CV is compared with tau (the printed /sqrt(dim) bounds it < 1). */
+adahop_pattern_t adahop_classify_cv(double cv_row, double cv_col, const adahop_params_t* p);
+
+/* ------------------------------------------------------------- calibration (§5.1) */
+
+/* Pattern statistics of a rows x cols tensor T (dt = BF16 or F32, leading dim ld):
+ * row_stats[i*4 + {0,1,2,3}] = {sum x, sum x^2, sum |x|, max |x|} over row i (fp64),
+ * col_stats[j*4 + ...]       = the same over column j (fp64).
+ * Multi-rank callers sum-all-reduce col_stats[.,0..2] and max-all-reduce col_stats[.,3]
+ * before adahop_classify. Workspace: adahop_stats_workspace_bytes(rows, cols). */
+size_t adahop_stats_workspace_bytes(int64_t rows, int64_t cols);
+adahop_status_t adahop_stats(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
+                             int64_t ld, double* row_stats, double* col_stats, void* ws,
+                             size_t ws_bytes, adahop_stream_t stream);
+
+/* CV sums from statistics (App. A; population std):
+ * d_cv[0] = sum_i std(T_i,:)/(mean|T_i,:| + eps) over the `rows` given rows (each has
+ * `cols` elements); d_cv[1] = sum_j std(T_:,j)/(mean|T_:,j| + eps) over `cols` columns,
+ * each with `col_count` elements (the global row count under token sharding).
+ * Also writes d_pattern[0] = classification with CV_row = d_cv[0]/rows and
+ * CV_col = d_cv[1]/cols (correct for a single rank). */
+adahop_status_t adahop_classify(const double* row_stats, int64_t rows, const double* col_stats,
+                                int64_t cols, int64_t col_count, const adahop_params_t* p,
+                                double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
+
+/* One-call calibration of one tensor for one step on a single rank: stats + classify.
+ * d_cv (2 doubles) and d_pattern (1 byte) are device outputs.
+ * Workspace: adahop_calibrate_workspace_bytes(rows, cols). */
+size_t adahop_calibrate_workspace_bytes(int64_t rows, int64_t cols);
+adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
+                                 int64_t ld, const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                 double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
+
+/* ------------------------------------------------------------------- hot path */
+
+/* Generic AdaHOP GEMM in stored form: C[M x N] = A_store[M x K] · B_store[N x K]^T under
+ * `strategy`. A_store / B_store are views of bf16 memory:
+ *   a_kstrided == 0: A_store[m][k] = A[m*lda + k]   (K contiguous)
+ *   a_kstrided == 1: A_store[m][k] = A[k*lda + m]   (K strided: the transposing quant)
+ * and likewise for B. C is written with leading dimension ldc in out_dt.
+ * OE-Left extracts rows of A_store, OE-Right rows of B_store (= columns of B). */
+size_t adahop_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
+                                   const adahop_params_t* p);
+adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, const void* B,
+                            int32_t b_kstrided, int64_t ldb, void* C, adahop_dtype_t out_dt,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
+                            const adahop_params_t* p, void* ws, size_t ws_bytes,
+                            adahop_stream_t stream);
+
+/* Linear-layer paths. X: T x d_in, W: d_out x d_in, G_Y: T x d_out, all bf16
+ * row-major and contiguous. Outputs contiguous in out_dt.
+ *   fwd:   Y   = X W^T      (A_store = X,     B_store = W)      M=T,     N=d_out, K=d_in
+ *   dgrad: G_X = G_Y W      (A_store = G_Y,   B_store = W^T)    M=T,     N=d_in,  K=d_out
+ *   wgrad: G_W = G_Y^T X    (A_store = G_Y^T, B_store = X^T)    M=d_out, N=d_in,  K=T
+ * wgrad additionally requires T % 32 == 0. Under token-row data parallelism each rank
+ * calls wgrad on its shard and the caller all-reduces G_W (fp32) across ranks. */
+size_t adahop_workspace_bytes(adahop_path_t path, int64_t T, int64_t d_in, int64_t d_out,
+                              adahop_strategy_t s, const adahop_params_t* p);
+adahop_status_t adahop_linear_fwd(const void* X, const void* W, void* Y, adahop_dtype_t out_dt,
+                                  int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                  const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                  adahop_stream_t stream);
+adahop_status_t adahop_linear_dgrad(const void* GY, const void* W, void* GX, adahop_dtype_t out_dt,
+                                    int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                    const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                    adahop_stream_t stream);
+adahop_status_t adahop_linear_wgrad(const void* GY, const void* X, void* GW, adahop_dtype_t out_dt,
+                                    int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                    const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                    adahop_stream_t stream);
+
+/* ------------------------------------------------------- debug / parity entry points */
+
+/* Fused IHT + MXFP4 quantisation of a stored operand (the production kernels), with the
+ * results converted to canonical layouts: codes_canon R x K/2 bytes (element 2j in the
+ * low nibble), scales_canon R x K/32 bytes of biased E8M0 (e + 127). in is bf16 or f32:
+ * k_strided == 0: row r = in[r*ld + 0..K); k_strided == 1: in[k*ld + r].
+ * zero_rows (nzero sorted int32, device; may be NULL when nzero == 0) are masked to +0
+ * before the transform (the OE residual). had_out (nullable, R x K f32) receives the
+ * fp32 Hadamard output that enters the quantiser. */
+adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,
+                                       int64_t ld, int32_t k_strided, const int32_t* zero_rows,
+                                       int32_t nzero, float* had_out, uint8_t* codes_canon,
+                                       uint8_t* scales_canon, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream);
+size_t adahop_debug_workspace_bytes(int64_t R, int64_t K);
+
+/* FOID: idx_sorted[0..min(k,R)) = ascending indices of the top-k stored rows by
+ * the fp64 probe variance (ties -> lower index); keys_out (nullable) = the R keys. */
+adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,
+                                  int64_t ld, int32_t k_strided, int32_t k, int32_t probe,
+                                  int32_t* idx_sorted, double* keys_out, void* ws,
+                                  size_t ws_bytes, adahop_stream_t stream);
+
+/* Block-scaled MXFP4 GEMM on canonical operands: C[M x N] (f32 or bf16, ldc) =
+ * deq(A codes/scales) · deq(B codes/scales)^T, using the production tcgen05 kernel. */
+adahop_status_t adahop_debug_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_scales,
+                                       const uint8_t* b_codes, const uint8_t* b_scales, void* C,
+                                       adahop_dtype_t out_dt, int64_t ldc, int64_t M, int64_t N,
+                                       int64_t K, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream);
+size_t adahop_debug_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* E2M1 element conversion used by the quantiser (hardware cvt.rn.satfinite.e2m1x2) and
+ * its software statement (nearest of {0,.5,1,1.5,2,3,4,6}, ties to even mantissa,
+ * saturating, sign = signbit): one code per input (device arrays of n). */
+adahop_status_t adahop_debug_e2m1(const float* v, int64_t n, uint8_t* codes_hw, uint8_t* codes_sw,
+                                  adahop_stream_t stream);
+/* Compare the two conversions on every finite fp32 bit pattern in [lo, hi) (hi <= 2^32);
+ * adds the mismatch count to *d_mismatches and atomically min-reduces the first bad
+ * pattern into *d_first_bad (both device, caller-initialised). */
+adahop_status_t adahop_debug_e2m1_exhaustive(uint64_t lo, uint64_t hi,
+                                             unsigned long long* d_mismatches,
+                                             uint32_t* d_first_bad, adahop_stream_t stream);
+
+/* Number of kernel launches the last successful hot-path call on this thread issued
+ * (host counter; used by bench.py to report gpu_launches). */
+int32_t adahop_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAHOP_H_ */

@@ -1,0 +1,277 @@
+"""Python binding of the AdaHOP C ABI (include/adahop.h) over torch tensors.
+
+Argument marshalling only: every arithmetic step runs in libadahop.so's sm_100a kernels.
+PyTorch provides device memory (the caching allocator), the current CUDA stream and,
+in ``dist.py``, the process group.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import Params, check, lib
+
+IHT, OE_LEFT_IHT, OE_RIGHT_IHT, BF16 = 0, 1, 2, 3
+STRATEGY = {"IHT": IHT, "OE_LEFT_IHT": OE_LEFT_IHT, "OE_RIGHT_IHT": OE_RIGHT_IHT, "BF16": BF16}
+STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
+PAT = {"N": 0, "R": 1, "C": 2}
+PAT_NAME = {0: "N", 1: "R", 2: "C"}
+PATH = {"fwd": 0, "dgrad": 1, "wgrad": 2}
+DT_BF16, DT_F32 = 0, 1
+
+__all__ = [
+    "Params", "IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16", "STRATEGY", "strategy_for_pair",
+    "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
+    "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant",
+    "debug_foid", "debug_gemm_mxf4", "last_launch_count", "Workspace",
+]
+
+
+def _strategy(s) -> int:
+    return STRATEGY[s] if isinstance(s, str) else int(s)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return DT_BF16
+    if t.dtype == torch.float32:
+        return DT_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+# ------------------------------------------------------------------------- host helpers
+def strategy_for_pair(left: str, right: str, level: int = 1) -> str:
+    return STRATEGY_NAME[lib.adahop_strategy_for_pair(PAT[left], PAT[right], level)]
+
+
+def majority_vote(patterns) -> str:
+    arr = (C.c_int32 * len(patterns))(*[PAT[p] for p in patterns])
+    return PAT_NAME[lib.adahop_majority_vote(arr, len(patterns))]
+
+
+def classify_cv(cv_row: float, cv_col: float, params: Params | None = None) -> str:
+    p = params or Params()
+    return PAT_NAME[lib.adahop_classify_cv(cv_row, cv_col, C.byref(p))]
+
+
+def last_launch_count() -> int:
+    return lib.adahop_last_launch_count()
+
+
+class Workspace:
+    """Caller-owned scratch (grown on demand; pointer stable once large enough)."""
+
+    def __init__(self, nbytes: int = 0, device=None):
+        self.buf = None
+        if nbytes:
+            self.ensure(nbytes, device)
+
+    def ensure(self, nbytes: int, device=None) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                   device=device or torch.cuda.current_device())
+        return self.buf
+
+
+_default_ws: dict = {}
+
+
+def _ws(nbytes: int, ws: Workspace | None, device) -> torch.Tensor:
+    if ws is None:
+        ws = _default_ws.setdefault(str(device), Workspace())
+    return ws.ensure(nbytes, device)
+
+
+# ------------------------------------------------------------------------- calibration
+def stats(t: torch.Tensor):
+    """Per-row and per-column {sum x, sum x^2, sum |x|, max |x|} (fp64) of a 2-D tensor."""
+    assert t.dim() == 2 and t.stride(1) == 1
+    rows, cols = t.shape
+    rs = torch.empty((rows, 4), dtype=torch.float64, device=t.device)
+    cs = torch.empty((cols, 4), dtype=torch.float64, device=t.device)
+    n = lib.adahop_stats_workspace_bytes(rows, cols)
+    w = torch.empty(n, dtype=torch.uint8, device=t.device)
+    check("adahop_stats", lib.adahop_stats(_ptr(t), _dt(t), rows, cols, t.stride(0), _ptr(rs), _ptr(cs),
+                                           _ptr(w), n, _stream()))
+    return rs, cs
+
+
+def classify(row_stats, col_stats, row_len: int, col_count: int, params: Params | None = None):
+    """CV sums (device, 2 doubles) and the single-rank pattern (device uint8)."""
+    p = params or Params()
+    dev = row_stats.device
+    cv = torch.empty(2, dtype=torch.float64, device=dev)
+    pat = torch.empty(1, dtype=torch.uint8, device=dev)
+    rows = row_stats.shape[0]
+    cols = col_stats.shape[0]
+    assert row_len == cols
+    check("adahop_classify", lib.adahop_classify(_ptr(row_stats), rows, _ptr(col_stats), cols, col_count,
+                                                 C.byref(p), _ptr(cv), _ptr(pat), _stream()))
+    return cv, pat
+
+
+def calibrate(t: torch.Tensor, params: Params | None = None):
+    """One calibration step of one tensor (App. A): returns (pattern 'R'|'C'|'N', cv_row, cv_col)."""
+    p = params or Params()
+    rows, cols = t.shape
+    n = lib.adahop_calibrate_workspace_bytes(rows, cols)
+    w = torch.empty(n, dtype=torch.uint8, device=t.device)
+    cv = torch.empty(2, dtype=torch.float64, device=t.device)
+    pat = torch.empty(1, dtype=torch.uint8, device=t.device)
+    check("adahop_calibrate", lib.adahop_calibrate(_ptr(t), _dt(t), rows, cols, t.stride(0), C.byref(p),
+                                                   _ptr(w), n, _ptr(cv), _ptr(pat), _stream()))
+    cvh = cv.cpu()
+    return PAT_NAME[int(pat.item())], float(cvh[0]) / rows, float(cvh[1]) / cols
+
+
+# ------------------------------------------------------------------------- hot path
+def gemm(a, a_kstrided: bool, b, b_kstrided: bool, M: int, N: int, K: int, strategy,
+         params: Params | None = None, out: torch.Tensor | None = None,
+         out_dtype=torch.bfloat16, ws: Workspace | None = None) -> torch.Tensor:
+    """C = A_store · B_store^T under `strategy` (stored-form GEMM of include/adahop.h)."""
+    p = params or Params()
+    s = _strategy(strategy)
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=a.device)
+    lda = a.stride(0)
+    ldb = b.stride(0)
+    n = lib.adahop_gemm_workspace_bytes(M, N, K, s, C.byref(p))
+    w = _ws(n, ws, a.device)
+    check("adahop_gemm", lib.adahop_gemm(_ptr(a), int(a_kstrided), lda, _ptr(b), int(b_kstrided), ldb,
+                                         _ptr(out), _dt(out), out.stride(0), M, N, K, s, C.byref(p),
+                                         _ptr(w), w.numel(), _stream()))
+    return out
+
+
+def workspace_bytes(path: str, T: int, d_in: int, d_out: int, strategy, params: Params | None = None) -> int:
+    p = params or Params()
+    return lib.adahop_workspace_bytes(PATH[path], T, d_in, d_out, _strategy(strategy), C.byref(p))
+
+
+def _linear(fn, path, a, b, T, d_in, d_out, shape, strategy, params, out, out_dtype, ws):
+    p = params or Params()
+    s = _strategy(strategy)
+    assert a.is_contiguous() and b.is_contiguous() and a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
+    if out is None:
+        out = torch.empty(shape, dtype=out_dtype, device=a.device)
+    n = lib.adahop_workspace_bytes(PATH[path], T, d_in, d_out, s, C.byref(p))
+    w = _ws(n, ws, a.device)
+    check(fn.__name__, fn(_ptr(a), _ptr(b), _ptr(out), _dt(out), T, d_in, d_out, s, C.byref(p), _ptr(w),
+                          w.numel(), _stream()))
+    return out
+
+
+def linear_fwd(x, w, strategy, params=None, out=None, out_dtype=torch.bfloat16, ws=None):
+    """Y = X W^T (eq:forward P:75). X: T x d_in, W: d_out x d_in (bf16)."""
+    T, d_in = x.shape
+    d_out = w.shape[0]
+    return _linear(lib.adahop_linear_fwd, "fwd", x, w, T, d_in, d_out, (T, d_out), strategy, params,
+                   out, out_dtype, ws)
+
+
+def linear_dgrad(gy, w, strategy, params=None, out=None, out_dtype=torch.bfloat16, ws=None):
+    """G_X = G_Y W (eq:backward_gx P:77). G_Y: T x d_out, W: d_out x d_in."""
+    T, d_out = gy.shape
+    d_in = w.shape[1]
+    return _linear(lib.adahop_linear_dgrad, "dgrad", gy, w, T, d_in, d_out, (T, d_in), strategy, params,
+                   out, out_dtype, ws)
+
+
+def linear_wgrad(gy, x, strategy, params=None, out=None, out_dtype=torch.float32, ws=None):
+    """G_W = G_Y^T X (eq:backward_gw P:76). G_Y: T x d_out, X: T x d_in."""
+    T, d_out = gy.shape
+    d_in = x.shape[1]
+    return _linear(lib.adahop_linear_wgrad, "wgrad", gy, x, T, d_in, d_out, (d_out, d_in), strategy, params,
+                   out, out_dtype, ws)
+
+
+def linear(path: str, strategy, x=None, w=None, gy=None, **kw):
+    if path == "fwd":
+        return linear_fwd(x, w, strategy, **kw)
+    if path == "dgrad":
+        return linear_dgrad(gy, w, strategy, **kw)
+    if path == "wgrad":
+        return linear_wgrad(gy, x, strategy, **kw)
+    raise ValueError(path)
+
+
+# ------------------------------------------------------------------------- debug entry points
+def debug_iht_quant(x: torch.Tensor, k_strided: bool = False, zero_rows=None, want_had: bool = False):
+    """Production IHT+quant kernel on a stored operand; canonical codes/scales (+ fp32 Hadamard)."""
+    if k_strided:
+        K, R = x.shape
+    else:
+        R, K = x.shape
+    dev = x.device
+    codes = torch.empty((R, K // 2), dtype=torch.uint8, device=dev)
+    scales = torch.empty((R, K // 32), dtype=torch.uint8, device=dev)
+    had = torch.empty((R, K), dtype=torch.float32, device=dev) if want_had else None
+    zr = None
+    nz = 0
+    if zero_rows is not None and len(zero_rows):
+        zr = torch.as_tensor(zero_rows, dtype=torch.int32, device=dev).contiguous()
+        nz = zr.numel()
+    n = lib.adahop_debug_workspace_bytes(R, K)
+    w = torch.empty(n, dtype=torch.uint8, device=dev)
+    check("adahop_debug_iht_quant",
+          lib.adahop_debug_iht_quant(_ptr(x), _dt(x), R, K, x.stride(0), int(k_strided), _ptr(zr), nz,
+                                     _ptr(had), _ptr(codes), _ptr(scales), _ptr(w), n, _stream()))
+    return codes, scales, had
+
+
+def debug_foid(x: torch.Tensor, k: int, probe: int = 64, k_strided: bool = False):
+    if k_strided:
+        K, R = x.shape
+    else:
+        R, K = x.shape
+    dev = x.device
+    kk = min(k, R)
+    idx = torch.empty(kk, dtype=torch.int32, device=dev)
+    keys = torch.empty(R, dtype=torch.float64, device=dev)
+    n = lib.adahop_debug_workspace_bytes(R, K)
+    w = torch.empty(n, dtype=torch.uint8, device=dev)
+    check("adahop_debug_foid", lib.adahop_debug_foid(_ptr(x), _dt(x), R, K, x.stride(0), int(k_strided), k,
+                                                     probe, _ptr(idx), _ptr(keys), _ptr(w), n, _stream()))
+    return idx, keys
+
+
+def debug_gemm_mxf4(a_codes, a_scales, b_codes, b_scales, out_dtype=torch.float32):
+    M, Kh = a_codes.shape
+    N = b_codes.shape[0]
+    K = 2 * Kh
+    dev = a_codes.device
+    out = torch.empty((M, N), dtype=out_dtype, device=dev)
+    n = lib.adahop_debug_gemm_workspace_bytes(M, N, K)
+    w = torch.empty(n, dtype=torch.uint8, device=dev)
+    check("adahop_debug_gemm_mxf4",
+          lib.adahop_debug_gemm_mxf4(_ptr(a_codes), _ptr(a_scales), _ptr(b_codes), _ptr(b_scales), _ptr(out),
+                                     _dt(out), out.stride(0), M, N, K, _ptr(w), n, _stream()))
+    return out
+
+
+def debug_e2m1(v: torch.Tensor):
+    """(hardware codes, software-rule codes) of fp32 values through the quantiser's conversion."""
+    v = v.contiguous().float()
+    hw = torch.empty(v.numel(), dtype=torch.uint8, device=v.device)
+    sw = torch.empty_like(hw)
+    check("adahop_debug_e2m1", lib.adahop_debug_e2m1(_ptr(v), v.numel(), _ptr(hw), _ptr(sw), _stream()))
+    return hw, sw
+
+
+def debug_e2m1_exhaustive(lo: int = 0, hi: int = 1 << 32, device=None):
+    """Mismatch count and first mismatching fp32 bit pattern between hw and sw conversion."""
+    dev = device or torch.cuda.current_device()
+    mism = torch.zeros(1, dtype=torch.int64, device=dev)
+    first = torch.full((1,), -1, dtype=torch.int32, device=dev)   # 0xFFFFFFFF
+    check("adahop_debug_e2m1_exhaustive",
+          lib.adahop_debug_e2m1_exhaustive(lo, hi, _ptr(mism), _ptr(first), _stream()))
+    return int(mism.item()), int(first.item()) & 0xFFFFFFFF

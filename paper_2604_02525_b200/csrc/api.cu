@@ -1,0 +1,555 @@
+// api.cu — the C ABI of libadahop (include/adahop.h): validation, strategy dispatch,
+// workspace carving and kernel sequencing. No allocation, no host sync on the hot path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/adahop.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace adahop;
+
+namespace {
+
+thread_local int32_t g_launches = 0;
+
+// ---------------------------------------------------------------------- driver / device
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  bool ok = false;
+};
+DevInfo dev_info() {
+  static DevInfo cache[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DevInfo{};
+  std::lock_guard<std::mutex> lk(mu);
+  if (!cache[dev].ok) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return DevInfo{};
+    cache[dev].sms = prop.multiProcessorCount;
+    cache[dev].major = prop.major;
+    cache[dev].ok = true;
+  }
+  return cache[dev];
+}
+
+adahop_status_t check_device(DevInfo* out) {
+  DevInfo d = dev_info();
+  if (!d.ok || d.major != 10) return ADAHOP_E_NO_DEVICE;
+  if (!encode_fn()) return ADAHOP_E_CUDA;
+  if (out) *out = d;
+  return ADAHOP_OK;
+}
+
+#define ADAHOP_LAUNCH(expr)                                 \
+  do {                                                      \
+    cudaError_t e_ = (expr);                                \
+    if (e_ != cudaSuccess) return ADAHOP_E_CUDA;            \
+  } while (0)
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------- workspace carving
+struct Carver {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    const size_t at = off;
+    off += bytes;
+    return at;
+  }
+};
+
+struct GemmPlan {
+  int kk = 0;               // extracted rows (0 = no OE)
+  int64_t rows_oe = 0;      // rows of the OE operand
+  int64_t mbig = 0;         // rows of the big operand of the outlier GEMM
+  int64_t npad = 0;
+  int splits = 1;
+  size_t qa_codes = 0, qa_sf = 0, qb_codes = 0, qb_sf = 0;
+  size_t keys = 0, cand_key = 0, cand_idx = 0, idx = 0, slice = 0, part = 0;
+  size_t total = 0;
+};
+
+bool plan_gemm(int64_t M, int64_t N, int64_t K, adahop_strategy_t s, const adahop_params_t* p,
+               int num_sms, GemmPlan* g) {
+  Carver c;
+  *g = GemmPlan{};
+  if (s == ADAHOP_BF16) {
+    g->total = 256;
+    return true;
+  }
+  g->qa_codes = c.take(size_t(M) * size_t(K / 2));
+  g->qa_sf = c.take(size_t(sf_bytes(M, K)));
+  g->qb_codes = c.take(size_t(N) * size_t(K / 2));
+  g->qb_sf = c.take(size_t(sf_bytes(N, K)));
+  const bool oe = (s == ADAHOP_OE_LEFT_IHT || s == ADAHOP_OE_RIGHT_IHT) && p->oe_k > 0;
+  if (oe) {
+    g->rows_oe = s == ADAHOP_OE_LEFT_IHT ? M : N;
+    g->mbig = s == ADAHOP_OE_LEFT_IHT ? N : M;
+    g->kk = int(std::min<int64_t>(p->oe_k, g->rows_oe));
+    const int64_t nch = (g->rows_oe + kFoidChunkRows - 1) / kFoidChunkRows;
+    g->keys = c.take(size_t(g->rows_oe) * 8);
+    g->cand_key = c.take(size_t(nch) * g->kk * 8);
+    g->cand_idx = c.take(size_t(nch) * g->kk * 4);
+    g->idx = c.take(size_t(g->kk) * 4);
+    g->slice = c.take(size_t(g->kk) * size_t(K) * 2);
+    g->npad = bf16_gemm_npad(g->kk);
+    g->splits = bf16_gemm_splits(g->mbig, K, num_sms);
+    g->part = c.take(size_t(g->splits) * size_t(g->mbig) * size_t(g->npad) * 4);
+  }
+  g->total = c.take(0) + 256;
+  return true;
+}
+
+adahop_status_t validate_params(const adahop_params_t* p) {
+  if (!p) return ADAHOP_E_INVALID_ARG;
+  if (p->had_block != 32) return ADAHOP_E_UNSUPPORTED;
+  if (p->oe_k < 0 || p->foid_probe < 1 || (p->level != 1 && p->level != 2))
+    return ADAHOP_E_INVALID_ARG;
+  if (p->oe_k > 256) return ADAHOP_E_UNSUPPORTED;
+  return ADAHOP_OK;
+}
+
+}  // namespace
+
+// ============================================================================ tensor maps
+namespace adahop {
+bool make_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                  uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                  CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace adahop
+
+// ============================================================================ C ABI
+extern "C" {
+
+void adahop_default_params(adahop_params_t* p) {
+  if (!p) return;
+  p->had_block = 32;
+  p->oe_k = 64;
+  p->foid_probe = 64;
+  p->level = 1;
+  p->tau = 2.0f;
+  p->eps = 1e-8f;
+}
+
+int32_t adahop_abi_version(void) { return ADAHOP_ABI_VERSION; }
+
+int32_t adahop_last_launch_count(void) { return g_launches; }
+
+const char* adahop_status_string(adahop_status_t s) {
+  switch (s) {
+    case ADAHOP_OK: return "ok";
+    case ADAHOP_E_INVALID_ARG: return "invalid argument";
+    case ADAHOP_E_SHAPE: return "shape error";
+    case ADAHOP_E_UNSUPPORTED: return "unsupported configuration";
+    case ADAHOP_E_WORKSPACE: return "workspace too small or misaligned";
+    case ADAHOP_E_CUDA: return "CUDA error";
+    case ADAHOP_E_NO_DEVICE: return "no sm_100 device";
+  }
+  return "unknown status";
+}
+
+adahop_strategy_t adahop_strategy_for_pair(adahop_pattern_t l, adahop_pattern_t r, int32_t level) {
+  const bool R_ = l == ADAHOP_PAT_ROW, lC = l == ADAHOP_PAT_COL, lN = l == ADAHOP_PAT_NONE;
+  const bool rR = r == ADAHOP_PAT_ROW, rC = r == ADAHOP_PAT_COL, rN = r == ADAHOP_PAT_NONE;
+  if (lC && rC) return level == 2 ? ADAHOP_BF16 : ADAHOP_OE_RIGHT_IHT;
+  if (R_ && (rN || rR)) return ADAHOP_OE_LEFT_IHT;                      // RN, RR
+  if ((R_ || lN) && rC) return ADAHOP_OE_RIGHT_IHT;                     // RC, NC
+  return ADAHOP_IHT;                                                    // CN, NN, CR, NR
+}
+
+adahop_pattern_t adahop_majority_vote(const int32_t* per_step, int32_t n) {
+  if (!per_step || n <= 0) return ADAHOP_PAT_NONE;
+  int cnt[3] = {0, 0, 0};
+  for (int i = 0; i < n; ++i)
+    if (per_step[i] >= 0 && per_step[i] <= 2) cnt[per_step[i]]++;
+  const int best = std::max(cnt[0], std::max(cnt[1], cnt[2]));
+  if (cnt[ADAHOP_PAT_ROW] == best) return ADAHOP_PAT_ROW;
+  if (cnt[ADAHOP_PAT_COL] == best) return ADAHOP_PAT_COL;
+  return ADAHOP_PAT_NONE;
+}
+
+adahop_pattern_t adahop_classify_cv(double cv_row, double cv_col, const adahop_params_t* p) {
+  const double tau = p ? p->tau : 2.0;
+  const bool row_hit = cv_col > tau, col_hit = cv_row > tau;
+  if (row_hit && (!col_hit || cv_col >= cv_row)) return ADAHOP_PAT_ROW;
+  if (col_hit) return ADAHOP_PAT_COL;
+  return ADAHOP_PAT_NONE;
+}
+
+// ------------------------------------------------------------------------ calibration
+size_t adahop_stats_workspace_bytes(int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return size_t(stats_chunks(rows)) * size_t(cols) * 32 + 256;
+}
+
+adahop_status_t adahop_stats(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
+                             int64_t ld, double* row_stats, double* col_stats, void* ws,
+                             size_t ws_bytes, adahop_stream_t stream) {
+  if (!T || !row_stats || !col_stats || !ws) return ADAHOP_E_INVALID_ARG;
+  if (dt != ADAHOP_DT_BF16 && dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
+  if (rows <= 0 || cols <= 0 || ld < cols) return ADAHOP_E_SHAPE;
+  if (ws_bytes < adahop_stats_workspace_bytes(rows, cols) || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ADAHOP_E_WORKSPACE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  g_launches = 0;
+  ADAHOP_LAUNCH(launch_stats(T, dt == ADAHOP_DT_F32, rows, cols, ld, row_stats, col_stats,
+                             static_cast<double*>(ws), reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 3;
+  return ADAHOP_OK;
+}
+
+adahop_status_t adahop_classify(const double* row_stats, int64_t rows, const double* col_stats,
+                                int64_t cols, int64_t col_count, const adahop_params_t* p,
+                                double* d_cv, uint8_t* d_pattern, adahop_stream_t stream) {
+  if (!row_stats || !col_stats || !d_cv || !d_pattern || !p) return ADAHOP_E_INVALID_ARG;
+  if (rows <= 0 || cols <= 0 || col_count <= 0) return ADAHOP_E_SHAPE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  ADAHOP_LAUNCH(launch_classify(row_stats, rows, cols, col_stats, cols, col_count, double(p->eps),
+                                double(p->tau), d_cv, d_pattern,
+                                reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 1;
+  return ADAHOP_OK;
+}
+
+size_t adahop_calibrate_workspace_bytes(int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return 0;
+  Carver c;
+  c.take(size_t(rows) * 32);
+  c.take(size_t(cols) * 32);
+  c.take(adahop_stats_workspace_bytes(rows, cols));
+  return c.take(0) + 256;
+}
+
+adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
+                                 int64_t ld, const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                 double* d_cv, uint8_t* d_pattern, adahop_stream_t stream) {
+  if (!T || !p || !ws || !d_cv || !d_pattern) return ADAHOP_E_INVALID_ARG;
+  if (rows <= 0 || cols <= 0 || ld < cols) return ADAHOP_E_SHAPE;
+  if (ws_bytes < adahop_calibrate_workspace_bytes(rows, cols) ||
+      (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ADAHOP_E_WORKSPACE;
+  Carver c;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  double* rs = reinterpret_cast<double*>(base + c.take(size_t(rows) * 32));
+  double* cs = reinterpret_cast<double*>(base + c.take(size_t(cols) * 32));
+  const size_t sw = adahop_stats_workspace_bytes(rows, cols);
+  void* sws = base + c.take(sw);
+  adahop_status_t st = adahop_stats(T, dt, rows, cols, ld, rs, cs, sws, sw, stream);
+  if (st != ADAHOP_OK) return st;
+  st = adahop_classify(rs, rows, cs, cols, rows, p, d_cv, d_pattern, stream);
+  g_launches = 4;
+  return st;
+}
+
+// ------------------------------------------------------------------------ hot path
+size_t adahop_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
+                                   const adahop_params_t* p) {
+  if (!p || M <= 0 || N <= 0 || K <= 0) return 0;
+  DevInfo d = dev_info();
+  GemmPlan g;
+  plan_gemm(M, N, K, s, p, d.ok ? d.sms : 148, &g);
+  return g.total;
+}
+
+adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, const void* B,
+                            int32_t b_kstrided, int64_t ldb, void* C, adahop_dtype_t out_dt,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
+                            const adahop_params_t* p, void* ws, size_t ws_bytes,
+                            adahop_stream_t stream) {
+  // ---- host-side validation (no launch happens before all checks pass)
+  if (!A || !B || !C || !p) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = validate_params(p);
+  if (st != ADAHOP_OK) return st;
+  if (s < ADAHOP_IHT || s > ADAHOP_BF16) return ADAHOP_E_INVALID_ARG;
+  if (out_dt != ADAHOP_DT_BF16 && out_dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
+  if (M <= 0 || N <= 0 || K <= 0) return ADAHOP_E_SHAPE;
+  if (K % 32 != 0) return ADAHOP_E_SHAPE;
+  if ((a_kstrided != 0 && a_kstrided != 1) || (b_kstrided != 0 && b_kstrided != 1))
+    return ADAHOP_E_INVALID_ARG;
+  if (lda < (a_kstrided ? M : K) || ldb < (b_kstrided ? N : K) || ldc < N) return ADAHOP_E_INVALID_ARG;
+  if ((lda % 8) || (ldb % 8) || !aligned16(A) || !aligned16(B) || !aligned16(C))
+    return ADAHOP_E_INVALID_ARG;
+  DevInfo dev;
+  st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  GemmPlan g;
+  plan_gemm(M, N, K, s, p, dev.sms, &g);
+  if (!ws || ws_bytes < g.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  if (g.kk > 0) {
+    const int64_t nch = (g.rows_oe + kFoidChunkRows - 1) / kFoidChunkRows;
+    if (nch * g.kk > 8192) return ADAHOP_E_UNSUPPORTED;
+  }
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const bool out_f32 = out_dt == ADAHOP_DT_F32;
+  int32_t launches = 0;
+
+  // ---- Lv2 CC: the whole product in BF16
+  if (s == ADAHOP_BF16) {
+    Bf16GemmArgs ga{};
+    ga.A = static_cast<const __nv_bfloat16*>(A); ga.a_mn = a_kstrided; ga.lda = lda;
+    ga.B = static_cast<const __nv_bfloat16*>(B); ga.b_mn = b_kstrided; ga.ldb = ldb;
+    ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = C; ga.out_f32 = out_f32; ga.ldc = ldc;
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    g_launches = 1;
+    return ADAHOP_OK;
+  }
+
+  uint8_t* qa = w + g.qa_codes;
+  uint8_t* qa_sf = w + g.qa_sf;
+  uint8_t* qb = w + g.qb_codes;
+  uint8_t* qb_sf = w + g.qb_sf;
+  int32_t* idx = g.kk > 0 ? reinterpret_cast<int32_t*>(w + g.idx) : nullptr;
+  const bool oe_left = g.kk > 0 && s == ADAHOP_OE_LEFT_IHT;
+  const bool oe_right = g.kk > 0 && s == ADAHOP_OE_RIGHT_IHT;
+
+  // Scale-factor padding (rows beyond R or K beyond the last 256-block) must hold finite
+  // scales: the padded codes are zero-filled by TMA, zero x finite scale = 0.
+  if ((M % 128) || (K % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(qa_sf, 0, size_t(sf_bytes(M, K)), cs));
+  if ((N % 128) || (K % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(qb_sf, 0, size_t(sf_bytes(N, K)), cs));
+
+  // ---- 1. FOID + outlier slice (P:760 stage 1)
+  const void* oe_src = oe_left ? A : B;
+  const int oe_ks = oe_left ? a_kstrided : b_kstrided;
+  const int64_t oe_ld = oe_left ? lda : ldb;
+  __nv_bfloat16* slice = g.kk > 0 ? reinterpret_cast<__nv_bfloat16*>(w + g.slice) : nullptr;
+  if (g.kk > 0) {
+    ADAHOP_LAUNCH(launch_foid(oe_src, false, g.rows_oe, K, oe_ld, oe_ks, g.kk, p->foid_probe,
+                              reinterpret_cast<double*>(w + g.keys),
+                              reinterpret_cast<double*>(w + g.cand_key),
+                              reinterpret_cast<int32_t*>(w + g.cand_idx), idx, cs));
+    ADAHOP_LAUNCH(launch_gather(oe_src, K, oe_ld, oe_ks, idx, g.kk, slice, cs));
+    launches += 4;
+  }
+  // ---- 2. IHT + MXFP4 quantisation of both operands (P:761 stage 2), residual masked
+  ADAHOP_LAUNCH(launch_iht_quant(A, false, M, K, lda, a_kstrided, oe_left ? idx : nullptr,
+                                 oe_left ? g.kk : 0, qa, qa_sf, nullptr, false, cs));
+  ADAHOP_LAUNCH(launch_iht_quant(B, false, N, K, ldb, b_kstrided, oe_right ? idx : nullptr,
+                                 oe_right ? g.kk : 0, qb, qb_sf, nullptr, false, cs));
+  launches += 2;
+  // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
+  Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K};
+  ADAHOP_LAUNCH(launch_gemm_mxf4(ma, dev.sms, cs));
+  launches += 1;
+  // ---- 4. BF16 outlier GEMM + scatter-add into C (P:762-763 stages 3-4)
+  if (g.kk > 0) {
+    Bf16GemmArgs ga{};
+    if (oe_right) {  // D[M x k] = A (M x K) . B_out^T
+      ga.A = static_cast<const __nv_bfloat16*>(A); ga.a_mn = a_kstrided; ga.lda = lda;
+    } else {         // D[N x k] = B_store (N x K) . A_out^T  (transposed OE-Left product)
+      ga.A = static_cast<const __nv_bfloat16*>(B); ga.a_mn = b_kstrided; ga.lda = ldb;
+    }
+    ga.B = slice; ga.b_mn = 0; ga.ldb = K;
+    ga.Mb = g.mbig; ga.Nb = g.kk; ga.K = K; ga.mode = 1;
+    ga.part = reinterpret_cast<float*>(w + g.part); ga.splits = g.splits; ga.npad = g.npad;
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    ADAHOP_LAUNCH(launch_outlier_reduce(ga.part, g.splits, g.mbig, g.npad, g.kk, idx, oe_right, C,
+                                        out_f32, ldc, cs));
+    launches += 2;
+  }
+  g_launches = launches;
+  return ADAHOP_OK;
+}
+
+size_t adahop_workspace_bytes(adahop_path_t path, int64_t T, int64_t d_in, int64_t d_out,
+                              adahop_strategy_t s, const adahop_params_t* p) {
+  switch (path) {
+    case ADAHOP_PATH_FWD: return adahop_gemm_workspace_bytes(T, d_out, d_in, s, p);
+    case ADAHOP_PATH_DGRAD: return adahop_gemm_workspace_bytes(T, d_in, d_out, s, p);
+    case ADAHOP_PATH_WGRAD: return adahop_gemm_workspace_bytes(d_out, d_in, T, s, p);
+  }
+  return 0;
+}
+
+adahop_status_t adahop_linear_fwd(const void* X, const void* W, void* Y, adahop_dtype_t out_dt,
+                                  int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                  const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                  adahop_stream_t stream) {
+  // Y = X W^T: A_store = X (T x d_in), B_store = W (d_out x d_in)
+  return adahop_gemm(X, 0, d_in, W, 0, d_in, Y, out_dt, d_out, T, d_out, d_in, s, p, ws, ws_bytes,
+                     stream);
+}
+
+adahop_status_t adahop_linear_dgrad(const void* GY, const void* W, void* GX, adahop_dtype_t out_dt,
+                                    int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                    const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                    adahop_stream_t stream) {
+  // G_X = G_Y W: A_store = G_Y (T x d_out), B_store = W^T (K-strided view of W)
+  return adahop_gemm(GY, 0, d_out, W, 1, d_in, GX, out_dt, d_in, T, d_in, d_out, s, p, ws,
+                     ws_bytes, stream);
+}
+
+adahop_status_t adahop_linear_wgrad(const void* GY, const void* X, void* GW, adahop_dtype_t out_dt,
+                                    int64_t T, int64_t d_in, int64_t d_out, adahop_strategy_t s,
+                                    const adahop_params_t* p, void* ws, size_t ws_bytes,
+                                    adahop_stream_t stream) {
+  // G_W = G_Y^T X: A_store = G_Y^T, B_store = X^T, both K-strided (K = tokens)
+  if (T % 32 != 0) return ADAHOP_E_SHAPE;
+  return adahop_gemm(GY, 1, d_out, X, 1, d_in, GW, out_dt, d_in, d_out, d_in, T, s, p, ws,
+                     ws_bytes, stream);
+}
+
+// ------------------------------------------------------------------------ debug entry points
+size_t adahop_debug_workspace_bytes(int64_t R, int64_t K) {
+  if (R <= 0 || K <= 0) return 0;
+  Carver c;
+  c.take(size_t(sf_bytes(R, K)));
+  c.take(size_t(R) * 8);                                   // FOID keys
+  const int64_t nch = (R + kFoidChunkRows - 1) / kFoidChunkRows;
+  c.take(size_t(nch) * 256 * 8);
+  c.take(size_t(nch) * 256 * 4);
+  return c.take(0) + 256;
+}
+
+adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,
+                                       int64_t ld, int32_t k_strided, const int32_t* zero_rows,
+                                       int32_t nzero, float* had_out, uint8_t* codes_canon,
+                                       uint8_t* scales_canon, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream) {
+  if (!in || !codes_canon || !scales_canon || !ws) return ADAHOP_E_INVALID_ARG;
+  if (nzero < 0 || (nzero > 0 && !zero_rows)) return ADAHOP_E_INVALID_ARG;
+  if (R <= 0 || K <= 0 || K % 32) return ADAHOP_E_SHAPE;
+  const int64_t esz = dt == ADAHOP_DT_F32 ? 4 : 2;
+  if (ld < (k_strided ? R : K) || (ld * esz) % 16 || !aligned16(in)) return ADAHOP_E_INVALID_ARG;
+  if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* sf = static_cast<uint8_t*>(ws);
+  ADAHOP_LAUNCH(launch_iht_quant(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, zero_rows, nzero,
+                                 codes_canon, sf, had_out, false, cs));
+  ADAHOP_LAUNCH(launch_sf_convert(sf, R, K, scales_canon, true, cs));
+  g_launches = 2;
+  return ADAHOP_OK;
+}
+
+adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,
+                                  int64_t ld, int32_t k_strided, int32_t k, int32_t probe,
+                                  int32_t* idx_sorted, double* keys_out, void* ws, size_t ws_bytes,
+                                  adahop_stream_t stream) {
+  if (!in || !idx_sorted || !ws) return ADAHOP_E_INVALID_ARG;
+  if (R <= 0 || K <= 0) return ADAHOP_E_SHAPE;
+  if (k < 1 || k > 256 || probe < 1) return ADAHOP_E_UNSUPPORTED;
+  if (ld < (k_strided ? R : K)) return ADAHOP_E_INVALID_ARG;
+  if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
+  const int64_t kk = std::min<int64_t>(k, R);
+  const int64_t nch = (R + kFoidChunkRows - 1) / kFoidChunkRows;
+  if (nch * kk > 8192) return ADAHOP_E_UNSUPPORTED;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  Carver c;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  c.take(size_t(sf_bytes(R, K)));
+  double* keys = reinterpret_cast<double*>(w + c.take(size_t(R) * 8));
+  double* ck = reinterpret_cast<double*>(w + c.take(size_t(nch) * 256 * 8));
+  int32_t* ci = reinterpret_cast<int32_t*>(w + c.take(size_t(nch) * 256 * 4));
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys, ck,
+                            ci, idx_sorted, cs));
+  if (keys_out)
+    ADAHOP_LAUNCH(cudaMemcpyAsync(keys_out, keys, size_t(R) * 8, cudaMemcpyDeviceToDevice, cs));
+  g_launches = 3;
+  return ADAHOP_OK;
+}
+
+size_t adahop_debug_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  Carver c;
+  c.take(size_t(sf_bytes(M, K)));
+  c.take(size_t(sf_bytes(N, K)));
+  return c.take(0) + 256;
+}
+
+adahop_status_t adahop_debug_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_scales,
+                                       const uint8_t* b_codes, const uint8_t* b_scales, void* C,
+                                       adahop_dtype_t out_dt, int64_t ldc, int64_t M, int64_t N,
+                                       int64_t K, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream) {
+  if (!a_codes || !a_scales || !b_codes || !b_scales || !C || !ws) return ADAHOP_E_INVALID_ARG;
+  if (M <= 0 || N <= 0 || K <= 0 || K % 32) return ADAHOP_E_SHAPE;
+  if (ldc < N || !aligned16(a_codes) || !aligned16(b_codes) || !aligned16(C))
+    return ADAHOP_E_INVALID_ARG;
+  if (ws_bytes < adahop_debug_gemm_workspace_bytes(M, N, K) ||
+      (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ADAHOP_E_WORKSPACE;
+  DevInfo dev;
+  adahop_status_t st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  Carver c;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  uint8_t* sfa = w + c.take(size_t(sf_bytes(M, K)));
+  uint8_t* sfb = w + c.take(size_t(sf_bytes(N, K)));
+  ADAHOP_LAUNCH(cudaMemsetAsync(sfa, 0, size_t(sf_bytes(M, K)), cs));
+  ADAHOP_LAUNCH(cudaMemsetAsync(sfb, 0, size_t(sf_bytes(N, K)), cs));
+  ADAHOP_LAUNCH(launch_sf_convert(a_scales, M, K, sfa, false, cs));
+  ADAHOP_LAUNCH(launch_sf_convert(b_scales, N, K, sfb, false, cs));
+  Mxf4GemmArgs ma{a_codes, sfa, b_codes, sfb, C, out_dt == ADAHOP_DT_F32, ldc, M, N, K};
+  ADAHOP_LAUNCH(launch_gemm_mxf4(ma, dev.sms, cs));
+  g_launches = 3;
+  return ADAHOP_OK;
+}
+
+adahop_status_t adahop_debug_e2m1(const float* v, int64_t n, uint8_t* codes_hw, uint8_t* codes_sw,
+                                  adahop_stream_t stream) {
+  if (!v || !codes_hw || !codes_sw || n < 0) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  if (n == 0) return ADAHOP_OK;
+  ADAHOP_LAUNCH(launch_e2m1_codes(v, n, codes_hw, codes_sw, reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 1;
+  return ADAHOP_OK;
+}
+
+adahop_status_t adahop_debug_e2m1_exhaustive(uint64_t lo, uint64_t hi,
+                                             unsigned long long* d_mismatches,
+                                             uint32_t* d_first_bad, adahop_stream_t stream) {
+  if (!d_mismatches || !d_first_bad || hi < lo || hi > (1ull << 32)) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  ADAHOP_LAUNCH(launch_e2m1_exhaustive(lo, hi, d_mismatches, d_first_bad,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 1;
+  return ADAHOP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// gemm_mxf4.cu — block-scaled MXFP4 GEMM on the 5th-gen tensor cores (sm_100a).
+//
+// C[M x N] = deq(A_store) · deq(B_store)^T, both operands K-major E2M1 (two codes per
+// byte, element 2j in the low nibble) with one UE8M0 scale per 32 elements along K
+// (the "MXFP4 matmul" of eq:inner_hadamard P:95 / eq:oe_left P:273 / eq:oe_right P:280).
+//
+// Design (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: A/B tiles (128 B x rows, 128B swizzle) + scale-factor
+//               chunks (1D bulk copies) into a kStages-deep smem ring (mbarrier full/empty)
+//   warp 1      MMA issuer (one thread): tcgen05.cp of the stage's scale factors into TMEM,
+//               then 4 x tcgen05.mma.kind::mxf4.block_scale.block32 (128 x BN x 64) per
+//               stage; tcgen05.commit frees the smem slot / publishes the accumulator
+//   warp 2      TMEM allocator (512 columns: 2 accumulator buffers + scale factors)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> global (fp32 or bf16), while
+//               the MMA warp already accumulates the next tile into the other buffer.
+#include "common.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace adahop {
+namespace mxf4 {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 256;                 // fp4 elements per stage (= 128 bytes per row)
+constexpr int kStages = 6;
+constexpr int kABytes = BM * BK / 2;    // 16 KB
+constexpr int kBBytes = BN * BK / 2;    // 16 KB
+constexpr int kSfaBytes = (BM / 128) * 2 * 512;  // 2 K-chunks of 128 rows
+constexpr int kSfbBytes = (BN / 128) * 2 * 512;
+constexpr int kStageBytes = kABytes + kBBytes + kSfaBytes + kSfbBytes;
+constexpr int kTmemCols = 512;
+constexpr int kAccCols = BN;            // per accumulator buffer
+constexpr int kSfCol = 2 * kAccCols;    // first TMEM column of the scale factors
+constexpr int kSfbColOff = 8;           // SFB after the 8 SFA columns
+constexpr int kThreads = 256;
+constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+// Instruction descriptor, kind::mxf4 block-scaled (E2M1 x E2M1, UE8M0, fp32 accumulate).
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
+  return (1u << 7)             // a_format = E2M1
+         | (1u << 10)          // b_format = E2M1
+         | (uint32_t(n >> 3) << 17)
+         | (1u << 23)          // scale format UE8M0
+         | (uint32_t(m >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_mxf4(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                const uint8_t* __restrict__ sfa, const uint8_t* __restrict__ sfb, void* C,
+                int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(kStages) * kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int64_t mblocks = (M + BM - 1) / BM;
+  const int64_t nblocks = (N + BN - 1) / BN;
+  const int64_t ntiles = mblocks * nblocks;
+  const int nks = int((K + BK - 1) / BK);
+  const int64_t kchunks = sf_kchunks(K);
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_a);
+    ptx::prefetch_tmap(&tm_b);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t mb = tile % mblocks, nb = tile / mblocks;
+      for (int ks = 0; ks < nks; ++ks) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + size_t(stage) * kStageBytes;
+        uint8_t* sb = sa + kABytes;
+        uint8_t* ssfa = sb + kBBytes;
+        uint8_t* ssfb = ssfa + kSfaBytes;
+        ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+        ptx::tma_load_2d(sa, &tm_a, &full[stage], ks * (BK / 2), int32_t(mb * BM));
+        ptx::tma_load_2d(sb, &tm_b, &full[stage], ks * (BK / 2), int32_t(nb * BN));
+        ptx::bulk_load(ssfa, sfa + (mb * kchunks + 2 * ks) * 512, kSfaBytes, &full[stage]);
+        ptx::bulk_load(ssfb, sfb + (nb * kchunks + 2 * ks) * 512, kSfbBytes, &full[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const uint32_t buf = uint32_t(lt & 1);
+      const uint32_t use = uint32_t(lt >> 1);
+      ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * kAccCols;
+      for (int ks = 0; ks < nks; ++ks) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        uint8_t* sa = smem + size_t(stage) * kStageBytes;
+        uint8_t* sb = sa + kABytes;
+        uint8_t* ssfa = sb + kBBytes;
+        uint8_t* ssfb = ssfa + kSfaBytes;
+        // scale factors -> TMEM (executes in order with the MMAs below)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          ptx::tmem_cp_32x128b_warpx4(tmem_base + kSfCol + 4 * c,
+                                      ptx::make_sdesc(ptx::smem_u32(ssfa + c * 512), 0, 128, 0));
+          ptx::tmem_cp_32x128b_warpx4(tmem_base + kSfCol + kSfbColOff + 4 * c,
+                                      ptx::make_sdesc(ptx::smem_u32(ssfb + c * 512), 0, 128, 0));
+        }
+        const uint32_t a_addr = ptx::smem_u32(sa), b_addr = ptx::smem_u32(sb);
+#pragma unroll
+        for (int j = 0; j < BK / 64; ++j) {
+          const uint32_t sf_id = uint32_t(j & 1) * 2;
+          const uint32_t sfa_t = (tmem_base + kSfCol + 4 * (j >> 1)) | (sf_id << 30);
+          const uint32_t sfb_t = (tmem_base + kSfCol + kSfbColOff + 4 * (j >> 1)) | (sf_id << 30);
+          const uint32_t id = idesc | (sf_id << 4) | (sf_id << 29);
+          const uint64_t adesc = ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2);
+          const uint64_t bdesc = ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2);
+          ptx::mma_mxf4(d_tmem, adesc, bdesc, id, sfa_t, sfb_t, (ks > 0 || j > 0) ? 1u : 0u);
+        }
+        ptx::tc_commit(&empty[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      ptx::tc_commit(&tfull[buf]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp
+    int64_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int64_t mb = tile % mblocks, nb = tile / mblocks;
+      const uint32_t buf = uint32_t(lt & 1);
+      const uint32_t use = uint32_t(lt >> 1);
+      ptx::mbar_wait(&tfull[buf], use & 1);
+      ptx::tc_fence_after();
+      const int64_t m = mb * BM + q * 32 + lane;
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + buf * kAccCols + c * 32, r);
+        ptx::tmem_ld_wait();
+        const int64_t n0 = nb * BN + c * 32;
+        if (m < M) {
+          if (out_f32) {
+            float* crow = static_cast<float*>(C) + m * ldc + n0;
+            if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                reinterpret_cast<uint4*>(crow)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+            } else {
+              for (int v = 0; v < 32 && n0 + v < N; ++v) crow[v] = __uint_as_float(r[v]);
+            }
+          } else {
+            __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(C) + m * ldc + n0;
+            if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint32_t w[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * t]),
+                                                           __uint_as_float(r[8 * v + 2 * t + 1]));
+                  w[t] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                reinterpret_cast<uint4*>(crow)[v] = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            } else {
+              for (int v = 0; v < 32 && n0 + v < N; ++v) crow[v] = __float2bfloat16_rn(__uint_as_float(r[v]));
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace mxf4
+
+cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st) {
+  using namespace mxf4;
+  CUtensorMap tma, tmb;
+  // FP4 codes as bytes: [rows][K/2], box 128 bytes x 128 rows, 128B swizzle.
+  if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
+                    uint64_t(a.K / 2), 128, BM, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
+                    uint64_t(a.K / 2), 128, BN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_mxf4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  const int grid = int(tiles < num_sms ? tiles : num_sms);
+  k_gemm_mxf4<<<grid, kThreads, kSmemBytes, st>>>(tma, tmb, a.a_sf, a.b_sf, a.C, a.out_f32 ? 1 : 0,
+                                                  a.ldc, a.M, a.N, a.K);
+  return cudaGetLastError();
+}
+
+}  // namespace adahop

@@ -1,0 +1,82 @@
+// kernels.h — host-side launchers of the AdaHOP sm_100a kernels (internal to libadahop).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace adahop {
+
+// quant.cu
+cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
+                             int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
+                             uint8_t* sf, float* had_out, bool sw_cvt, cudaStream_t st);
+cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
+                              bool to_canonical, cudaStream_t st);
+cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
+                        int kstrided, int k, int probe, double* keys, double* cand_key,
+                        int32_t* cand_idx, int32_t* idx_sorted, cudaStream_t st);
+constexpr int kFoidChunkRows = 2048;
+cudaError_t launch_gather(const void* in, int64_t K, int64_t ld, int kstrided, const int32_t* idx,
+                          int k, __nv_bfloat16* out, cudaStream_t st);
+int64_t stats_chunks(int64_t R);
+cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
+                         double* rs, double* cs, double* part, cudaStream_t st);
+cudaError_t launch_classify(const double* rs, int64_t rows, int64_t row_len, const double* cs,
+                            int64_t cols, int64_t col_len, double eps, double tau, double* d_cv,
+                            uint8_t* pattern, cudaStream_t st);
+
+cudaError_t launch_e2m1_codes(const float* v, int64_t n, uint8_t* hw, uint8_t* sw, cudaStream_t st);
+cudaError_t launch_e2m1_exhaustive(uint64_t lo, uint64_t hi, unsigned long long* mism,
+                                   unsigned int* first_bad, cudaStream_t st);
+
+// gemm_mxf4.cu — C[M x N] = deq(A) deq(B)^T, A/B MXFP4 K-major (codes + tcgen05 SF layout)
+struct Mxf4GemmArgs {
+  const uint8_t* a_codes;
+  const uint8_t* a_sf;
+  const uint8_t* b_codes;
+  const uint8_t* b_sf;
+  void* C;
+  bool out_f32;
+  int64_t ldc, M, N, K;
+};
+cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st);
+
+// gemm_bf16.cu — D[Mb x Nb] = A[Mb x K] B[Nb x K]^T in BF16 (fp32 accumulate).
+// A/B are K-major (a_mn = 0: A[m*lda + k]) or MN-major (a_mn = 1: A[k*lda + m]).
+// mode 0: D written densely to C (out dtype, ldc); mode 1: fp32 split-K partials to
+// part[split][Mb][npad] (npad = padded Nb), reduced afterwards by launch_outlier_reduce.
+struct Bf16GemmArgs {
+  const __nv_bfloat16* A;
+  int a_mn;
+  int64_t lda;
+  const __nv_bfloat16* B;
+  int b_mn;
+  int64_t ldb;
+  int64_t Mb, Nb, K;
+  int mode;
+  void* C;
+  bool out_f32;
+  int64_t ldc;
+  float* part;
+  int splits;
+  int64_t npad;
+};
+int64_t bf16_gemm_npad(int64_t Nb);
+int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms);
+cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st);
+// Scatter-add of the outlier product into C (fused "scatter-add" stage):
+// val(m, j) = sum_split part[split][m][j] (fixed order);
+// scatter_cols (OE-Right): C[m][idx[j]] = val;  else (OE-Left): C[idx[j]][m] = val.
+// The MXFP4 product is exactly 0 at those positions (disjoint support), so the store
+// equals the add.
+cudaError_t launch_outlier_reduce(const float* part, int splits, int64_t Mb, int64_t npad, int k,
+                                  const int32_t* idx, bool scatter_cols, void* C, bool out_f32,
+                                  int64_t ldc, cudaStream_t st);
+
+// tensor maps (api.cu)
+bool make_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                  uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                  CUtensorMapSwizzle swz);
+
+}  // namespace adahop

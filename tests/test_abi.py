@@ -1,0 +1,87 @@
+"""CPU tests of the C ABI boundary: the library loads, exports every symbol declared in
+include/adahop.h, and the pure host functions / host-side validation behave (no compute
+calls — there is no GPU here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import oracle as O
+from conftest import ROOT, golden
+
+ah = pytest.importorskip("paper_2604_02525_b200")
+from paper_2604_02525_b200 import _lib  # noqa: E402
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "adahop.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(adahop_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported_and_bound():
+    names = _declared_symbols()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(_lib.lib, n), n
+        assert n in _lib.SIGNATURES, f"{n} declared in adahop.h but not bound in _lib.py"
+    assert set(_lib.SIGNATURES) == set(names)
+
+
+def test_abi_version_and_defaults():
+    assert _lib.lib.adahop_abi_version() == 1
+    p = _lib.Params(0, 0, 0, 0, 0.0, 0.0)
+    _lib.lib.adahop_default_params(C.byref(p))
+    assert (p.had_block, p.oe_k, p.foid_probe, p.level) == (32, 64, 64, 1)
+    assert abs(p.tau - 2.0) < 1e-7 and abs(p.eps - 1e-8) < 1e-12
+
+
+def test_strategy_table_matches_golden_and_oracle():
+    for left, right, level, strat in golden("strategy_table.txt"):
+        assert ah.strategy_for_pair(left, right, int(level)) == strat
+        assert O.strategy_for_pair(left, right, int(level)) == strat
+
+
+def test_majority_vote_and_classify_cv_match_oracle():
+    for seq in (["R"] * 30, ["R"] * 16 + ["N"] * 14, ["R"] * 15 + ["C"] * 15, ["C"] * 3 + ["N"] * 3,
+                ["N"] * 5 + ["C"] * 4 + ["R"] * 4):
+        assert ah.majority_vote(seq) == O.majority_vote(seq)
+    for cr, cc in ((1.2, 1.3), (3.5, 1.2), (1.2, 3.5), (3.0, 3.0), (3.0, 4.0), (4.0, 3.0), (2.0, 2.0)):
+        want = "R" if (cc > 2 and (cr <= 2 or cc >= cr)) else ("C" if cr > 2 else "N")
+        assert ah.classify_cv(cr, cc) == want
+
+
+def test_status_strings():
+    for s in range(7):
+        assert _lib.lib.adahop_status_string(s)
+    assert b"shape" in _lib.lib.adahop_status_string(2)
+
+
+def test_host_validation_without_device():
+    p = _lib.Params()
+    f = _lib.lib
+    # null pointers -> invalid argument (checked before any device query)
+    assert f.adahop_gemm(None, 0, 64, None, 0, 64, None, 1, 64, 64, 64, 64, 0, C.byref(p), None, 0, None) == 1
+    # no device in this container -> the library reports it instead of falling back to the CPU
+    buf = (C.c_uint8 * 4096)()
+    ptr = C.cast(buf, C.c_void_p)
+    st = f.adahop_gemm(ptr, 0, 64, ptr, 0, 64, ptr, 1, 64, 64, 64, 64, 0, C.byref(p), ptr, 4096, None)
+    assert st in (6, 4)          # E_NO_DEVICE (or E_WORKSPACE if a device exists)
+    # K % 32 != 0 -> shape error before anything else
+    assert f.adahop_gemm(ptr, 0, 64, ptr, 0, 64, ptr, 1, 64, 64, 64, 48, 0, C.byref(p), ptr, 4096, None) == 2
+    # had_block != 32 -> unsupported
+    q = _lib.Params(had_block=16)
+    assert f.adahop_gemm(ptr, 0, 64, ptr, 0, 64, ptr, 1, 64, 64, 64, 64, 0, C.byref(q), ptr, 4096, None) == 3
+    # wgrad needs T % 32 == 0
+    assert f.adahop_linear_wgrad(ptr, ptr, ptr, 1, 48, 64, 64, 0, C.byref(p), ptr, 4096, None) == 2
+
+
+def test_workspace_sizes_are_host_computable():
+    p = _lib.Params()
+    n_iht = ah.workspace_bytes("fwd", 16384, 2048, 2048, "IHT", p)
+    n_oe = ah.workspace_bytes("fwd", 16384, 2048, 2048, "OE_RIGHT_IHT", p)
+    # FP4 codes + scales of both operands at least
+    assert n_iht >= (16384 + 2048) * 2048 // 2 + (16384 + 2048) * 2048 // 32
+    assert n_oe > n_iht
+    assert ah.workspace_bytes("fwd", 16384, 2048, 2048, "BF16", p) <= 512

@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs. Bit-exact for codes / scales / index sets; 1e-6 relative for the Hadamard
+output; 1e-3 relative Frobenius for linear outputs (north star), on fp32 outputs
+(a bf16 output alone carries ~1.7e-3 rounding).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2604_02525_b200 as ah  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TOL_OUT = 1e-3      # north star: linear outputs within 1e-3 relative Frobenius
+TOL_HAD = 1e-6      # north star: Hadamard outputs within 1e-6 relative
+
+
+def dev_bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, torch.bfloat16)
+
+
+def dev_f32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(DEV)
+
+
+def rel_fro(got, ref):
+    ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+# ======================================================================= E2M1 conversion
+def test_e2m1_hw_conversion_matches_oracle_rule():
+    ties = [0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0, 6.0, 7.0, 7.99, 8.0, 1e30, 0.0]
+    grid = np.linspace(-9, 9, 180001)
+    rnd = np.random.default_rng(0).standard_normal(1 << 20) * 3
+    v = np.concatenate([ties, -np.array(ties), grid, rnd, np.nextafter(np.array(ties), 10),
+                        np.nextafter(np.array(ties), -10)]).astype(np.float32)
+    hw, sw = ah.debug_e2m1(dev_f32(v))
+    want = O.e2m1_code(v.astype(np.float64))
+    np.testing.assert_array_equal(sw.cpu().numpy(), want)
+    np.testing.assert_array_equal(hw.cpu().numpy(), want)
+
+
+def test_e2m1_hw_vs_rule_exhaustive_fp32():
+    # every finite fp32 bit pattern: hardware cvt == the stated rounding rule
+    mism, first = ah.debug_e2m1_exhaustive(0, 1 << 32)
+    assert mism == 0, f"{mism} mismatches, first at bits 0x{first:08x}"
+
+
+# ======================================================================= IHT + quant
+def _quant_case(R, K, dtype, k_strided, pattern="C", case=0, zero_rows=None):
+    x, _ = synth.operand(R, K, pattern, "X", case_id=case, bf16=(dtype == "bf16"))
+    xin = x.T.copy() if k_strided else x
+    t = dev_bf16(xin) if dtype == "bf16" else dev_f32(xin)
+    codes, scales, had = ah.debug_iht_quant(t, k_strided=k_strided, zero_rows=zero_rows, want_had=True)
+    torch.cuda.synchronize()
+    xs = x.copy()
+    if zero_rows is not None and len(zero_rows):
+        xs[np.asarray(zero_rows)] = 0.0
+    return xs, codes.cpu().numpy(), scales.cpu().numpy(), had.cpu().numpy()
+
+
+@pytest.mark.parametrize("k_strided", [False, True])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("R,K", [(300, 1024), (77, 96), (128, 256), (1031, 2080)])
+def test_iht_quant_bitexact(R, K, dtype, k_strided):
+    xs, codes, scales, had = _quant_case(R, K, dtype, k_strided, case=R + K)
+    spec = O.fwht_fp32_spec(xs)
+    # (b) the GPU's fp32 Hadamard output equals the oracle's fp32 butterfly spec bitwise
+    np.testing.assert_array_equal(had.view(np.uint32), spec.view(np.uint32))
+    # Hadamard within 1e-6 relative of the fp64 dense transform
+    assert rel_fro(had, O.iht_dense(xs)) <= TOL_HAD
+    # (a) codes and E8M0 scales bit-exact given the same fp32 input
+    oc, osc = O.quantize_mxfp4(spec)
+    np.testing.assert_array_equal(scales, osc)
+    np.testing.assert_array_equal(codes, O.pack_codes(oc))
+
+
+@pytest.mark.parametrize("k_strided", [False, True])
+def test_iht_quant_residual_mask(k_strided):
+    zr = [0, 5, 6, 129, 299]
+    xs, codes, scales, had = _quant_case(300, 512, "bf16", k_strided, pattern="R", case=7, zero_rows=zr)
+    oc, osc = O.quantize_mxfp4(O.fwht_fp32_spec(xs))
+    np.testing.assert_array_equal(codes, O.pack_codes(oc))
+    np.testing.assert_array_equal(scales, osc)
+    assert np.all(codes[zr] == 0) and np.all(scales[zr] == 127)   # +0 codes, e = 0
+
+
+def test_iht_quant_extreme_magnitudes():
+    rng = np.random.default_rng(5)
+    R, K = 64, 256
+    x = rng.standard_normal((R, K)).astype(np.float32)
+    scale = np.float32(2.0) ** rng.integers(-140, 120, size=(R, 1)).astype(np.float32)
+    x = (x * scale).astype(np.float32)
+    x[3] = 0.0
+    x[4, :] = 0.0
+    x[4, 7] = np.float32(1e-45)        # smallest subnormal
+    x[5] = np.float32(3e38) * np.sign(x[5])
+    t = dev_f32(x)
+    codes, scales, had = ah.debug_iht_quant(t, want_had=True)
+    spec = O.fwht_fp32_spec(x)
+    finite = np.isfinite(spec).all(axis=1)
+    oc, osc = O.quantize_mxfp4(np.where(np.isfinite(spec), spec, 0))
+    np.testing.assert_array_equal(scales.cpu().numpy()[finite], osc[finite])
+    np.testing.assert_array_equal(codes.cpu().numpy()[finite], O.pack_codes(oc)[finite])
+
+
+# ======================================================================= FOID
+@pytest.mark.parametrize("k_strided", [False, True])
+@pytest.mark.parametrize("R,K,k,probe", [(5000, 128, 64, 64), (300, 96, 8, 64), (2048, 64, 256, 64),
+                                          (4100, 256, 16, 32), (50, 32, 64, 64)])
+def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
+    x, planted = synth.operand(R, K, "R", "X", case_id=R + k, count=min(5, R))
+    x[10] = x[11]                                  # an exact key tie
+    xin = x.T.copy() if k_strided else x
+    idx, keys = ah.debug_foid(dev_bf16(xin), k=k, probe=probe, k_strided=k_strided)
+    want_keys = O.foid_keys(x, probe)
+    np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), want_keys.view(np.uint64))
+    np.testing.assert_array_equal(idx.cpu().numpy(), O.foid_indices(x, k, probe))
+    assert set(planted.rows) <= set(idx.cpu().numpy().tolist())
+
+
+# ======================================================================= MXFP4 GEMM
+def _rand_mx(R, K, rng):
+    codes = rng.integers(0, 16, size=(R, K), dtype=np.uint8)
+    scales = rng.integers(127 - 6, 127 + 6, size=(R, K // 32), dtype=np.uint8)
+    return codes, scales
+
+
+def test_gemm_mxf4_one_hot_layout():
+    M, N, K = 256, 256, 512
+    for (r, n, k, ca, cb, ea, eb) in [(0, 0, 0, 2, 2, 127, 127), (5, 17, 33, 7, 3, 129, 120),
+                                      (130, 255, 511, 15, 9, 127, 140), (255, 128, 300, 4, 4, 100, 150)]:
+        a = np.zeros((M, K), np.uint8)
+        b = np.zeros((N, K), np.uint8)
+        a[r, k] = ca
+        b[n, k] = cb
+        sa = np.full((M, K // 32), 127, np.uint8)
+        sb = np.full((N, K // 32), 127, np.uint8)
+        sa[r, k // 32] = ea
+        sb[n, k // 32] = eb
+        c = ah.debug_gemm_mxf4(*(torch.from_numpy(v).to(DEV) for v in (O.pack_codes(a), sa, O.pack_codes(b), sb)))
+        c = c.cpu().numpy()
+        want = O.dequantize_mxfp4(a, sa) @ O.dequantize_mxfp4(b, sb).T
+        nz = np.argwhere(c != 0)
+        np.testing.assert_array_equal(c, want)
+        assert len(nz) <= 1
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 256), (300, 200, 544), (128, 384, 2048), (1000, 520, 1024)])
+@pytest.mark.parametrize("out", ["f32", "bf16"])
+def test_gemm_mxf4_random_vs_oracle(M, N, K, out):
+    rng = np.random.default_rng(M + N + K)
+    ca, sa = _rand_mx(M, K, rng)
+    cb, sb = _rand_mx(N, K, rng)
+    ops = [torch.from_numpy(v).to(DEV) for v in (O.pack_codes(ca), sa, O.pack_codes(cb), sb)]
+    c32 = ah.debug_gemm_mxf4(*ops, out_dtype=torch.float32).cpu().numpy()
+    want = O.dequantize_mxfp4(ca, sa) @ O.dequantize_mxfp4(cb, sb).T
+    assert rel_fro(c32, want) <= 1e-5
+    if out == "bf16":
+        c16 = ah.debug_gemm_mxf4(*ops, out_dtype=torch.bfloat16).float().cpu().numpy()
+        np.testing.assert_array_equal(c16, O.round_bf16(c32).astype(np.float32))
+
+
+# ======================================================================= end-to-end GEMM
+STRATS = ["IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16"]
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("a_ks,b_ks", [(0, 0), (0, 1), (1, 1), (1, 0)])
+def test_adahop_gemm_vs_oracle(strategy, a_ks, b_ks):
+    M, N, K, k = 384, 320, 512, 16
+    a, _ = synth.operand(M, K, "R", "X", case_id=31, count=4)          # A_store rows planted
+    b, _ = synth.operand(N, K, "R", "W", case_id=32, count=3)          # B_store rows = B columns
+    ta = dev_bf16(a.T.copy() if a_ks else a)
+    tb = dev_bf16(b.T.copy() if b_ks else b)
+    p = ah.Params(oe_k=k)
+    c = ah.gemm(ta, a_ks, tb, b_ks, M, N, K, strategy, p, out_dtype=torch.float32)
+    cb16 = ah.gemm(ta, a_ks, tb, b_ks, M, N, K, strategy, p, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    ref, parts = O.adahop_matmul(a, b, strategy, k=k, return_parts=True)
+    got = c.cpu().numpy()
+    assert rel_fro(got, ref) <= TOL_OUT
+    # bf16 output = RN_bf16(fp32 output): same accumulator, epilogue-only conversion
+    np.testing.assert_array_equal(cb16.float().cpu().numpy(), O.round_bf16(got).astype(np.float32))
+    if strategy in ("OE_LEFT_IHT", "OE_RIGHT_IHT"):
+        idx = parts["idx"]
+        sel = got[idx, :] if strategy == "OE_LEFT_IHT" else got[:, idx]
+        # disjoint support: the extracted rows/cols carry exactly the BF16 outlier product
+        assert rel_fro(sel, parts["c_out"]) <= 1e-5
+
+
+def test_adahop_gemm_k_clamp_and_k0():
+    M, N, K = 40, 72, 96
+    a, _ = synth.operand(M, K, "N", "X", case_id=41)
+    b, _ = synth.operand(N, K, "N", "W", case_id=42)
+    for strategy, k in (("OE_LEFT_IHT", 100), ("OE_RIGHT_IHT", 100), ("OE_LEFT_IHT", 0)):
+        c = ah.gemm(dev_bf16(a), 0, dev_bf16(b), 0, M, N, K, strategy, ah.Params(oe_k=k), out_dtype=torch.float32)
+        ref = O.adahop_matmul(a, b, strategy, k=k)
+        assert rel_fro(c.cpu().numpy(), ref) <= (1e-5 if k == 100 else TOL_OUT)
+
+
+def test_adahop_gemm_deterministic():
+    M, N, K = 512, 384, 1024
+    a, _ = synth.operand(M, K, "R", "X", case_id=51)
+    b, _ = synth.operand(N, K, "C", "W", case_id=52)
+    ta, tb = dev_bf16(a), dev_bf16(b)
+    outs = [ah.gemm(ta, 0, tb, 0, M, N, K, "OE_RIGHT_IHT", out_dtype=torch.float32).cpu().numpy() for _ in range(3)]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+
+
+# ======================================================================= linear paths, 9 pairs
+PAIRS = [(x, g) for x in "RCN" for g in "RCN"]
+
+
+@pytest.mark.parametrize("level", [1, 2])
+@pytest.mark.parametrize("path", ["fwd", "dgrad", "wgrad"])
+def test_linear_paths_all_pairs(path, level):
+    T, d_in, d_out = 512, 384, 256
+    for i, (pa, pb) in enumerate(PAIRS):
+        # choose tensor patterns so that the FED pair of this path is (pa, pb)
+        t = O.transpose_pattern
+        if path == "fwd":
+            px, pw, pg = pa, t(pb), "N"
+        elif path == "dgrad":
+            px, pw, pg = "N", pb, pa
+        else:
+            px, pw, pg = pb, "N", t(pa)
+        x, _ = synth.operand(T, d_in, px, "X", case_id=100 + i)
+        w, _ = synth.operand(d_out, d_in, pw, "W", case_id=200 + i)
+        gy, _ = synth.operand(T, d_out, pg, "GY", case_id=300 + i)
+        assert O.fed_patterns(path, px, pw, pg) == (pa, pb)
+        strategy = O.strategy_for_pair(pa, pb, level)
+        assert ah.strategy_for_pair(pa, pb, level) == strategy
+        p = ah.Params(oe_k=16, level=level)
+        got = ah.linear(path, strategy, x=dev_bf16(x), w=dev_bf16(w), gy=dev_bf16(gy), params=p,
+                        out_dtype=torch.float32).cpu().numpy()
+        ref = O.linear(path, strategy, x=x, w=w, gy=gy, k=16)
+        err = rel_fro(got, ref)
+        assert err <= TOL_OUT, (path, pa + pb, strategy, err)
+
+
+# ======================================================================= calibration
+@pytest.mark.parametrize("shape", [(256, 256), (2048, 512), (512, 4096)])
+def test_calibration_patterns_and_cv(shape):
+    rows, cols = shape
+    for i, p in enumerate("RCN"):
+        t, _ = synth.operand(rows, cols, p, "GY", case_id=60 + i)
+        pat, cvr, cvc = ah.calibrate(dev_bf16(t))
+        orow, ocol = O.cv_row_col(t)
+        assert abs(cvr - orow) <= 1e-9 * max(1, orow) and abs(cvc - ocol) <= 1e-9 * max(1, ocol)
+        assert pat == O.classify(t) == p
+
+
+# ======================================================================= full-size sampled parity
+@pytest.mark.slow
+@pytest.mark.parametrize("path,strategy,pats", [("fwd", "IHT", ("C", "N", "N")),
+                                                ("wgrad", "OE_RIGHT_IHT", ("C", "N", "C")),
+                                                ("dgrad", "OE_LEFT_IHT", ("N", "N", "R"))])
+def test_full_size_llama1b_sampled(path, strategy, pats):
+    T, d_in, d_out = 16384, 2048, 2048
+    px, pw, pg = pats
+    x, _ = synth.operand(T, d_in, px, "X", case_id=71)
+    w, _ = synth.operand(d_out, d_in, pw, "W", case_id=72)
+    gy, _ = synth.operand(T, d_out, pg, "GY", case_id=73)
+    got = ah.linear(path, strategy, x=dev_bf16(x), w=dev_bf16(w), gy=dev_bf16(gy), out_dtype=torch.float32)
+    got = got.cpu().numpy()
+    a_store, b_store = O.path_operands(path, x=x, w=w, gy=gy)
+    rng = np.random.default_rng(9)
+    rows = rng.integers(0, got.shape[0], 3000)
+    cols = rng.integers(0, got.shape[1], 3000)
+    if strategy != "IHT":
+        oe_store = a_store if strategy == "OE_LEFT_IHT" else b_store
+        idx = O.foid_indices(np.ascontiguousarray(oe_store), 64)
+        extra = rng.integers(0, got.shape[1 if strategy == "OE_LEFT_IHT" else 0], len(idx))
+        if strategy == "OE_LEFT_IHT":
+            rows, cols = np.concatenate([rows, idx]), np.concatenate([cols, extra])
+        else:
+            rows, cols = np.concatenate([rows, extra]), np.concatenate([cols, idx])
+    ref = O.sampled_entries(np.ascontiguousarray(a_store), np.ascontiguousarray(b_store), strategy, rows, cols)
+    assert rel_fro(got[rows, cols], ref) <= TOL_OUT
