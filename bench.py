@@ -1,0 +1,484 @@
+#!/usr/bin/env python
+"""AdaHOP MXFP4 linear benchmark (BASELINE.json metric, configs[1] workload).
+
+One STEP = the whole hot path over one batch: the 21 GEMMs of one Llama-3.2-1B
+transformer layer (q, k, v, o, gate, up, down x fwd / dgrad / wgrad) at T = 16384 tokens
+per GPU (seq 2048 x batch 8), each through the C ABI (FOID + IHT/quant + MXFP4 GEMM +
+BF16 outlier GEMM + scatter-add, strategy from the pattern pair, AdaHOP-Lv1, k = 64).
+Per-linear tensor patterns follow the Table-1 census classes (synth.LLAMA32_1B_LAYER_PATTERNS),
+which exercises the six pairs that occur in practice: CN, NN, RN, RC, NC, CC.
+
+value      = sum(2 M N K) over the step's GEMMs, all ranks / max-over-ranks device time
+e2e        = the same metric with inputs copied from pinned host memory and outputs read
+             back inside the timed region
+cublas     = the same 21 GEMMs with torch.matmul (cuBLAS BF16), same shapes / output dtype
+roofline   = dominant kernel (CUDA events recorded by the library between stages)
+cpu_baseline / --impl reference = the CPU oracle (oracle/) on a bounded sample
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl adahop|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "AdaHOP MXFP4 linear TFLOP/s (IHT+quant+OE+GEMM) and speedup vs BF16 cuBLAS"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="adahop", choices=["adahop", "reference"])
+    ap.add_argument("--workload", default="llama32_1b", choices=["llama32_1b", "llama3_8b"])
+    ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
+    ap.add_argument("--oe-k", type=int, default=64)
+    ap.add_argument("--level", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="oracle sample rows/cols per GEMM")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------- workload
+def transpose_pattern(p):
+    return {"R": "C", "C": "R", "N": "N"}[p]
+
+
+def fed_pair(path, px, pw, pg):
+    # fed orientation: fwd (X, W^T), dgrad (G_Y, W), wgrad (G_Y^T, X)
+    if path == "fwd":
+        return px, transpose_pattern(pw)
+    if path == "dgrad":
+        return pg, pw
+    return transpose_pattern(pg), px
+
+
+def workload_spec(name):
+    model = synth.LLAMA32_1B if name == "llama32_1b" else synth.LLAMA3_8B
+    pats = synth.LLAMA32_1B_LAYER_PATTERNS
+    return model, pats
+
+
+def gemm_list(model, pats, tokens):
+    out = []
+    for name, d_in, d_out in model["linears"]:
+        px, pg = pats[name]
+        for path in ("fwd", "dgrad", "wgrad"):
+            a, b = fed_pair(path, px, "N", pg)
+            M, N, K = {"fwd": (tokens, d_out, d_in), "dgrad": (tokens, d_in, d_out),
+                       "wgrad": (d_out, d_in, tokens)}[path]
+            out.append(dict(linear=name, path=path, pair=a + b, M=M, N=N, K=K, d_in=d_in, d_out=d_out))
+    return out
+
+
+# ------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------- peaks
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"],
+                "bf16_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
+
+
+# ------------------------------------------------------------------------------- oracle arm
+def oracle_sample_step(gemms, host, sample, rng):
+    """Oracle on a bounded sample: for every GEMM of the step, a sample x sample block of
+    output entries (FOID over the full operand, quantisation of the sampled rows only).
+    Returns the flops those entries represent (2 * K per entry)."""
+    import oracle as O
+    flops = 0.0
+    for g in gemms:
+        x, w, gy = host[g["linear"]]
+        a_store, b_store = O.path_operands(g["path"], x=x, w=w, gy=gy)
+        rows = rng.choice(g["M"], size=min(sample, g["M"]), replace=False)
+        cols = rng.choice(g["N"], size=min(sample, g["N"]), replace=False)
+        rr, cc = np.meshgrid(rows, cols, indexing="ij")
+        O.sampled_entries(a_store, b_store, g["strategy"], rr.ravel(), cc.ravel())
+        flops += 2.0 * rr.size * g["K"]
+    return flops
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on rank 0 only (host cores)."""
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (only for the seeded generator of the same inputs)
+    model, pats = workload_spec(args.workload)
+    gemms = gemm_list(model, pats, args.tokens)
+    for g in gemms:
+        g["strategy"] = _strategy_host(g["pair"], args.level)
+    host = make_host_inputs(model, pats, args.tokens)
+    rng = np.random.default_rng(0)
+    for _ in range(args.warmup):
+        oracle_sample_step(gemms, host, args.cpu_sample, rng)
+    t0 = time.perf_counter()
+    flops = 0.0
+    for _ in range(args.steps):
+        flops += oracle_sample_step(gemms, host, args.cpu_sample, rng)
+    dt = time.perf_counter() - t0
+    v = flops / dt / 1e12
+    cores = blas_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(args, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.cpu_sample}x{args.cpu_sample} output entries per GEMM x 21 GEMMs per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _strategy_host(pair, level):
+    # tab:strategy_summary; the product path asks the C ABI, this host copy is
+    # only used by the oracle arm so that it runs without a GPU library.
+    if pair == "CC":
+        return "OE_RIGHT_IHT" if level == 1 else "BF16"
+    return {"CN": "IHT", "NN": "IHT", "CR": "IHT", "NR": "IHT", "RN": "OE_LEFT_IHT", "RR": "OE_LEFT_IHT",
+            "RC": "OE_RIGHT_IHT", "NC": "OE_RIGHT_IHT"}[pair]
+
+
+def make_host_inputs(model, pats, tokens):
+    """Inputs of the same recipe and shapes as the GPU arm, drawn with torch's CPU generator."""
+    import torch
+    host = {}
+    for li, (name, d_in, d_out) in enumerate(model["linears"]):
+        px, pg = pats[name]
+        x = synth.operand_torch(tokens, d_in, px, "X", 1000 + li, "cpu").float().numpy()
+        w = synth.operand_torch(d_out, d_in, "N", "W", 2000 + li, "cpu").float().numpy()
+        gy = synth.operand_torch(tokens, d_out, pg, "GY", 3000 + li, "cpu").float().numpy()
+        host[name] = (x, w, gy)
+    del torch
+    return host
+
+
+def config_dict(args, world):
+    return {"workload": f"{args.workload}_layer_21gemm (7 linears x fwd/dgrad/wgrad)",
+            "tokens_per_gpu": args.tokens, "global_tokens": args.tokens * world,
+            "pairs": "CN NN RN RC NC CC (Table-1 census classes)", "oe_k": args.oe_k,
+            "level": args.level, "hadamard_block": 32, "out_dtype": "bf16",
+            "l2": "flushed between steps (256 MiB write, untimed)",
+            "parallelism": f"dp{world} token-sharded, NCCL all-reduce of wgrad" if world > 1 else "single GPU"}
+
+
+# ------------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2604_02525_b200 as ah
+
+    model, pats = workload_spec(args.workload)
+    T = args.tokens
+    gemms = gemm_list(model, pats, T)
+    params = ah.Params(oe_k=args.oe_k, level=args.level)
+    for g in gemms:
+        g["strategy"] = ah.strategy_for_pair(g["pair"][0], g["pair"][1], args.level)
+        g["flops"] = 2.0 * g["M"] * g["N"] * g["K"]
+
+    # inputs (seeded, synthetic, on the device) and outputs
+    lin = {}
+    for li, (name, d_in, d_out) in enumerate(model["linears"]):
+        px, pg = pats[name]
+        seed = 17 * rank
+        x = synth.operand_torch(T, d_in, px, "X", 1000 + li + seed, dev)
+        w = synth.operand_torch(d_out, d_in, "N", "W", 2000 + li, dev)       # W replicated
+        gy = synth.operand_torch(T, d_out, pg, "GY", 3000 + li + seed, dev)
+        lin[name] = dict(x=x, w=w, gy=gy,
+                         y=torch.empty(T, d_out, dtype=torch.bfloat16, device=dev),
+                         gx=torch.empty(T, d_in, dtype=torch.bfloat16, device=dev),
+                         gw=torch.empty(d_out, d_in, dtype=torch.bfloat16, device=dev))
+    ws_bytes = max(ah.workspace_bytes(g["path"], T, g["d_in"], g["d_out"], g["strategy"], params) for g in gemms)
+    ws = ah.Workspace(ws_bytes, dev)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    launches = [0]
+
+    def step_adahop(stage_events=None):
+        n = 0
+        for gi, g in enumerate(gemms):
+            L = lin[g["linear"]]
+            ctx = stage_events[gi] if stage_events is not None else None
+            if ctx is not None:
+                ctx.__enter__()
+            if g["path"] == "fwd":
+                ah.linear_fwd(L["x"], L["w"], g["strategy"], params, out=L["y"], ws=ws)
+            elif g["path"] == "dgrad":
+                ah.linear_dgrad(L["gy"], L["w"], g["strategy"], params, out=L["gx"], ws=ws)
+            else:
+                ah.linear_wgrad(L["gy"], L["x"], g["strategy"], params, out=L["gw"], ws=ws)
+                if world > 1:
+                    dist.all_reduce(L["gw"])
+            if ctx is not None:
+                ctx.__exit__()
+            n += ah.last_launch_count()
+        launches[0] += n
+
+    def step_cublas():
+        for g in gemms:
+            L = lin[g["linear"]]
+            if g["path"] == "fwd":
+                torch.mm(L["x"], L["w"].t(), out=L["y"])
+            elif g["path"] == "dgrad":
+                torch.mm(L["gy"], L["w"], out=L["gx"])
+            else:
+                torch.mm(L["gy"].t(), L["x"], out=L["gw"])
+                if world > 1:
+                    dist.all_reduce(L["gw"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(step_fn, steps, warmup, per_step_events=None, sampler=None):
+        for _ in range(warmup):
+            l2.zero_()
+            step_fn()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+        evs = []
+        for i in range(steps):
+            l2.zero_()                                   # untimed L2 flush
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            if per_step_events is not None:
+                step_fn(per_step_events[i])
+            else:
+                step_fn()
+            e.record()
+            evs.append((s, e))
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sampler else None
+        ms = sum(s.elapsed_time(e) for s, e in evs)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / steps, clocks
+
+    flops_step = sum(g["flops"] for g in gemms)
+
+    # ---- AdaHOP, device-resident inputs, per-stage events recorded by the library
+    stage_ev = [[ah.StageEvents() for _ in gemms] for _ in range(args.steps)]
+    step_adahop()                                          # compile-free warm start
+    launches[0] = 0
+    sampler = ClockSampler(local)
+    ms_ada, clocks = timed(step_adahop, args.steps, args.warmup, stage_ev, sampler)
+    launches_timed = launches[0] - 0
+    # launches counted in warmup + timed; keep the timed share
+    launches_per_step = launches_timed // (args.steps + args.warmup)
+    value = flops_step * world / (ms_ada * 1e-3) / 1e12
+
+    # per-stage breakdown (tab:latency analogue), summed over the step
+    stage_tot = {n: 0.0 for n in ah.StageEvents.NAMES}
+    per_gemm = []
+    for gi, g in enumerate(gemms):
+        acc = {n: 0.0 for n in ah.StageEvents.NAMES}
+        for i in range(args.steps):
+            for n, v in stage_ev[i][gi].times_ms().items():
+                acc[n] += v / args.steps
+        for n in acc:
+            stage_tot[n] += acc[n]
+        per_gemm.append(dict(linear=g["linear"], path=g["path"], pair=g["pair"], strategy=g["strategy"],
+                             M=g["M"], N=g["N"], K=g["K"], **{k: round(v, 4) for k, v in acc.items()}))
+
+    # ---- cuBLAS BF16 baseline (same GEMMs, same flush protocol)
+    ms_cub = None
+    if not args.no_cublas:
+        ms_cub, _ = timed(step_cublas, args.steps, args.warmup)
+
+    # ---- e2e: pinned host inputs in, outputs out, inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host_in = {k: {n: L[n].cpu().pin_memory() for n in ("x", "w", "gy")} for k, L in lin.items()}
+        host_out = {k: {n: torch.empty_like(L[n], device="cpu").pin_memory() for n in ("y", "gx", "gw")}
+                    for k, L in lin.items()}
+        h2d = sum(t.numel() * t.element_size() for d in host_in.values() for t in d.values())
+        d2h = sum(t.numel() * t.element_size() for d in host_out.values() for t in d.values())
+
+        def step_e2e():
+            for k, L in lin.items():
+                for n in ("x", "w", "gy"):
+                    L[n].copy_(host_in[k][n], non_blocking=True)
+            step_adahop()
+            for k, L in lin.items():
+                for n in ("y", "gx", "gw"):
+                    host_out[k][n].copy_(L[n], non_blocking=True)
+
+        ms_e2e, _ = timed(step_e2e, args.e2e_steps, 1)
+        e2e = {"value": flops_step * world / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the dominant kernel
+    peaks = load_peaks()
+    dom = max(stage_tot, key=stage_tot.get)
+    roof = roofline(dom, gemms, stage_tot, peaks, T)
+
+    # ---- CPU oracle baseline (rank 0, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host = {k: (L["x"].float().cpu().numpy(), L["w"].float().cpu().numpy(), L["gy"].float().cpu().numpy())
+                for k, L in lin.items()}
+        rng = np.random.default_rng(0)
+        t0 = time.perf_counter()
+        fl = oracle_sample_step(gemms, host, args.cpu_sample, rng)
+        dt = time.perf_counter() - t0
+        cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "seconds": round(dt, 2),
+               "sample": f"{args.cpu_sample}x{args.cpu_sample} output entries of each of the 21 GEMMs "
+                         "(FOID on the full operand, quantisation of the sampled rows)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_ada, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "mxfp4", "data": "synthetic", "config": config_dict(args, world),
+                "speedup_vs_cublas_bf16": (ms_cub / ms_ada) if ms_cub else None,
+                "cublas_bf16": {"value": flops_step * world / (ms_cub * 1e-3) / 1e12, "ms_per_step": ms_cub}
+                if ms_cub else None,
+                "stages_ms_per_step": {k: round(v, 4) for k, v in stage_tot.items()},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "gpu_launches": int(launches_per_step * args.steps)}
+        print(json.dumps(line), flush=True)
+        with open(os.path.join(ROOT, "gpurun_out", "bench_per_gemm.json") if os.path.isdir(
+                os.path.join(ROOT, "gpurun_out")) else os.devnull, "w") as f:
+            json.dump(per_gemm, f, indent=1)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(dom, gemms, stage_tot, peaks, T):
+    """Achieved = algorithmic work of the dominant stage per step / its measured time."""
+    fp4_peak = peaks["bf16_sustained"] * 4.0            # nominal fp4/bf16 dense ratio 9/2.25
+    if dom == "gemm_mxf4":
+        work = sum(g["flops"] for g in gemms if g["strategy"] != "BF16")
+        ach = work / (stage_tot[dom] * 1e-3) / 1e12
+        return {"kernel": "k_gemm_mxf4 (tcgen05 kind::mxf4)", "bound": "tensor", "achieved": ach,
+                "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak, "traffic": None,
+                "peak_src": f"{peaks['src']} bf16 sustained x 4 (nominal fp4/bf16)"}
+    if dom == "quant":
+        # 2 B in + 0.5 B codes + 1/32 B scale per element of both operands
+        by = sum((g["M"] + g["N"]) * g["K"] * (2 + 0.5 + 1 / 32) for g in gemms if g["strategy"] != "BF16")
+        ach = by / (stage_tot[dom] * 1e-3) / 1e9
+        return {"kernel": "k_iht_quant_row/col", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_src": peaks["src"]}
+    if dom == "outlier":
+        by = 0.0
+        for g in gemms:
+            if g["strategy"] == "OE_LEFT_IHT":
+                by += g["N"] * g["K"] * 2
+            elif g["strategy"] == "OE_RIGHT_IHT":
+                by += g["M"] * g["K"] * 2
+        ach = by / (stage_tot[dom] * 1e-3) / 1e9
+        return {"kernel": "k_gemm_bf16 (outlier) + k_outlier_reduce", "bound": "hbm", "achieved": ach,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+                "peak_src": peaks["src"]}
+    by = sum(g["M"] * 128 for g in gemms)   # FOID probe bytes (64 bf16 per row)
+    ach = by / (stage_tot[dom] * 1e-3) / 1e9
+    return {"kernel": "k_foid_*", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_src": peaks["src"]}
+
+
+if __name__ == "__main__":
+    main()

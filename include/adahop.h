@@ -219,6 +219,12 @@ adahop_status_t adahop_debug_e2m1_exhaustive(uint64_t lo, uint64_t hi,
  * (host counter; used by bench.py to report gpu_launches). */
 int32_t adahop_last_launch_count(void);
 
+/* Optional stage timing (tab:latency breakdown): `events` is a host array of 5
+ * cudaEvent_t (or NULL to disable) used by the following hot-path calls on this thread:
+ * [0] start, [1] after FOID + outlier gather, [2] after IHT+quant of both operands,
+ * [3] after the MXFP4 GEMM (or the Lv2 BF16 GEMM), [4] after the outlier GEMM + scatter. */
+void adahop_set_stage_events(void* events);
+
 #ifdef __cplusplus
 }
 #endif

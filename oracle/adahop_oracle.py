@@ -189,9 +189,9 @@ def foid_keys(store: np.ndarray, probe: int = FOID_PROBE) -> np.ndarray:
     P:760 "computing the variance of the first 64 elements along each row (or column)".
     Population variance, signed values, fp64, accumulated sequentially j = 0..p-1 with
     separate multiply and add (no FMA) [R5] so the key is bit-reproducible."""
-    x = np.asarray(store, dtype=np.float64)
-    r, k = x.shape
+    r, k = np.shape(store)
     p = min(probe, k)
+    x = np.asarray(np.asarray(store)[:, :p], dtype=np.float64)    # only the probe is read
     s = np.zeros(r, dtype=np.float64)
     for j in range(p):
         s = s + x[:, j]

@@ -59,6 +59,7 @@ SIGNATURES = {
     "adahop_debug_e2m1": (I32, [P, I64, P, P, P]),
     "adahop_debug_e2m1_exhaustive": (I32, [C.c_uint64, C.c_uint64, P, P, P]),
     "adahop_last_launch_count": (I32, []),
+    "adahop_set_stage_events": (None, [P]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

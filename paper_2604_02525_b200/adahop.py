@@ -24,7 +24,8 @@ __all__ = [
     "Params", "IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16", "STRATEGY", "strategy_for_pair",
     "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
     "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant",
-    "debug_foid", "debug_gemm_mxf4", "last_launch_count", "Workspace",
+    "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
+    "Workspace", "StageEvents",
 ]
 
 
@@ -275,3 +276,27 @@ def debug_e2m1_exhaustive(lo: int = 0, hi: int = 1 << 32, device=None):
     check("adahop_debug_e2m1_exhaustive",
           lib.adahop_debug_e2m1_exhaustive(lo, hi, _ptr(mism), _ptr(first), _stream()))
     return int(mism.item()), int(first.item()) & 0xFFFFFFFF
+
+
+class StageEvents:
+    """Five CUDA events recorded by the library between the hot-path stages of one call
+    (FOID | quant | MXFP4 GEMM | outlier GEMM + scatter), mirroring tab:latency."""
+
+    NAMES = ("foid", "quant", "gemm_mxf4", "outlier")
+
+    def __init__(self):
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        for e in self.events:      # materialise the cudaEvent_t handles
+            e.record()
+        self._arr = (C.c_void_p * 5)(*[e.cuda_event for e in self.events])
+
+    def __enter__(self):
+        lib.adahop_set_stage_events(C.cast(self._arr, C.c_void_p))
+        return self
+
+    def __exit__(self, *exc):
+        lib.adahop_set_stage_events(None)
+
+    def times_ms(self):
+        ev = self.events
+        return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(self.NAMES)}

@@ -16,6 +16,11 @@ using namespace adahop;
 namespace {
 
 thread_local int32_t g_launches = 0;
+thread_local cudaEvent_t* g_stage_events = nullptr;  // optional per-stage timing (bench)
+
+inline void stage_mark(int i, cudaStream_t st) {
+  if (g_stage_events) cudaEventRecord(g_stage_events[i], st);
+}
 
 // ---------------------------------------------------------------------- driver / device
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -172,6 +177,8 @@ int32_t adahop_abi_version(void) { return ADAHOP_ABI_VERSION; }
 
 int32_t adahop_last_launch_count(void) { return g_launches; }
 
+void adahop_set_stage_events(void* events) { g_stage_events = static_cast<cudaEvent_t*>(events); }
+
 const char* adahop_status_string(adahop_status_t s) {
   switch (s) {
     case ADAHOP_OK: return "ok";
@@ -323,13 +330,18 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   const bool out_f32 = out_dt == ADAHOP_DT_F32;
   int32_t launches = 0;
 
+  stage_mark(0, cs);
   // ---- Lv2 CC: the whole product in BF16
   if (s == ADAHOP_BF16) {
     Bf16GemmArgs ga{};
     ga.A = static_cast<const __nv_bfloat16*>(A); ga.a_mn = a_kstrided; ga.lda = lda;
     ga.B = static_cast<const __nv_bfloat16*>(B); ga.b_mn = b_kstrided; ga.ldb = ldb;
     ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = C; ga.out_f32 = out_f32; ga.ldc = ldc;
+    stage_mark(1, cs);
+    stage_mark(2, cs);
     ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    stage_mark(3, cs);
+    stage_mark(4, cs);
     g_launches = 1;
     return ADAHOP_OK;
   }
@@ -360,16 +372,19 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
     ADAHOP_LAUNCH(launch_gather(oe_src, K, oe_ld, oe_ks, idx, g.kk, slice, cs));
     launches += 4;
   }
+  stage_mark(1, cs);
   // ---- 2. IHT + MXFP4 quantisation of both operands (P:761 stage 2), residual masked
   ADAHOP_LAUNCH(launch_iht_quant(A, false, M, K, lda, a_kstrided, oe_left ? idx : nullptr,
                                  oe_left ? g.kk : 0, qa, qa_sf, nullptr, false, cs));
   ADAHOP_LAUNCH(launch_iht_quant(B, false, N, K, ldb, b_kstrided, oe_right ? idx : nullptr,
                                  oe_right ? g.kk : 0, qb, qb_sf, nullptr, false, cs));
   launches += 2;
+  stage_mark(2, cs);
   // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
   Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K};
   ADAHOP_LAUNCH(launch_gemm_mxf4(ma, dev.sms, cs));
   launches += 1;
+  stage_mark(3, cs);
   // ---- 4. BF16 outlier GEMM + scatter-add into C (P:762-763 stages 3-4)
   if (g.kk > 0) {
     Bf16GemmArgs ga{};
@@ -386,6 +401,7 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
                                         out_f32, ldc, cs));
     launches += 2;
   }
+  stage_mark(4, cs);
   g_launches = launches;
   return ADAHOP_OK;
 }
@@ -449,7 +465,9 @@ adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_
   if (nzero < 0 || (nzero > 0 && !zero_rows)) return ADAHOP_E_INVALID_ARG;
   if (R <= 0 || K <= 0 || K % 32) return ADAHOP_E_SHAPE;
   const int64_t esz = dt == ADAHOP_DT_F32 ? 4 : 2;
-  if (ld < (k_strided ? R : K) || (ld * esz) % 16 || !aligned16(in)) return ADAHOP_E_INVALID_ARG;
+  if (ld < (k_strided ? R : K)) return ADAHOP_E_INVALID_ARG;
+  // the row kernel uses 16-byte vector loads; the transposing kernel checks alignment itself
+  if (!k_strided && ((ld * esz) % 16 || !aligned16(in))) return ADAHOP_E_INVALID_ARG;
   if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
   adahop_status_t st = check_device(nullptr);
   if (st != ADAHOP_OK) return st;

@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(256) k_iht_quant_col(const T* __restrict__ in,
   const int64_t k0 = int64_t(blockIdx.y) * TK;
   constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte vector
   constexpr int kVecPerRow = TR / kVec;
-  const bool full = (r0 + TR <= R) && (k0 + TK <= K) && ((ld * sizeof(T)) % 16 == 0);
+  const bool full = (r0 + TR <= R) && (k0 + TK <= K) && ((ld * sizeof(T)) % 16 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
   if (full) {
     for (int v = threadIdx.x; v < TK * kVecPerRow; v += blockDim.x) {
       const int kr = v / kVecPerRow, c = (v % kVecPerRow) * kVec;
