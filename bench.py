@@ -23,7 +23,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -54,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64, help="oracle sample rows/cols per GEMM")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -91,56 +91,57 @@ def gemm_list(model, pats, tokens):
 
 # ------------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and throttle reasons through NVML every ~2 ms while running (the
+    timed region is only tens of milliseconds, too short for `nvidia-smi -lms`)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = repr(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "samples": len(sm),
-                "reasons": sorted(reasons)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
+        self.t.join()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "samples": len(self.samples), "reasons": sorted(self.reasons)}
 
 
 # ------------------------------------------------------------------------------- peaks
@@ -327,7 +328,24 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def timed(step_fn, steps, warmup, per_step_events=None, sampler=None):
+    def as_graph(fn):
+        """Capture one step into a CUDA graph (the library is capture-safe: no host sync,
+        no allocation on the hot path); returns a replay callable."""
+        if args.no_graph:
+            return fn
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g.replay
+
+    def timed(step_fn, steps, warmup, after_step=None, sampler=None):
         for _ in range(warmup):
             l2.zero_()
             step_fn()
@@ -336,22 +354,20 @@ def main():
         torch.cuda.synchronize()
         if sampler:
             sampler.start()
-        evs = []
+        ms = 0.0
         for i in range(steps):
             l2.zero_()                                   # untimed L2 flush
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            if per_step_events is not None:
-                step_fn(per_step_events[i])
-            else:
-                step_fn()
+            step_fn()
             e.record()
-            evs.append((s, e))
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()                     # between steps only; device-timed
+            ms += s.elapsed_time(e)
+            if after_step:
+                after_step()
         barrier()
         torch.cuda.synchronize()
         clocks = sampler.stop() if sampler else None
-        ms = sum(s.elapsed_time(e) for s, e in evs)
         if world > 1:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -360,34 +376,38 @@ def main():
 
     flops_step = sum(g["flops"] for g in gemms)
 
-    # ---- AdaHOP, device-resident inputs, per-stage events recorded by the library
-    stage_ev = [[ah.StageEvents() for _ in gemms] for _ in range(args.steps)]
-    step_adahop()                                          # compile-free warm start
+    # ---- AdaHOP, device-resident inputs; per-stage events recorded by the library
+    stage_ev = [ah.StageEvents() for _ in gemms]
+    step_adahop(stage_ev)                                  # first call: kernel attributes
+    torch.cuda.synchronize()
     launches[0] = 0
+    step_adahop(stage_ev)
+    launches_per_step = launches[0]
+    run_ada = as_graph(lambda: step_adahop(stage_ev))
+    acc = [{n: 0.0 for n in ah.StageEvents.NAMES} for _ in gemms]
+
+    def collect():
+        for gi in range(len(gemms)):
+            for n, v in stage_ev[gi].times_ms().items():
+                acc[gi][n] += v / args.steps
+
     sampler = ClockSampler(local)
-    ms_ada, clocks = timed(step_adahop, args.steps, args.warmup, stage_ev, sampler)
-    launches_timed = launches[0] - 0
-    # launches counted in warmup + timed; keep the timed share
-    launches_per_step = launches_timed // (args.steps + args.warmup)
+    ms_ada, clocks = timed(run_ada, args.steps, args.warmup, collect, sampler)
     value = flops_step * world / (ms_ada * 1e-3) / 1e12
 
     # per-stage breakdown (tab:latency analogue), summed over the step
     stage_tot = {n: 0.0 for n in ah.StageEvents.NAMES}
     per_gemm = []
     for gi, g in enumerate(gemms):
-        acc = {n: 0.0 for n in ah.StageEvents.NAMES}
-        for i in range(args.steps):
-            for n, v in stage_ev[i][gi].times_ms().items():
-                acc[n] += v / args.steps
-        for n in acc:
-            stage_tot[n] += acc[n]
+        for n in acc[gi]:
+            stage_tot[n] += acc[gi][n]
         per_gemm.append(dict(linear=g["linear"], path=g["path"], pair=g["pair"], strategy=g["strategy"],
-                             M=g["M"], N=g["N"], K=g["K"], **{k: round(v, 4) for k, v in acc.items()}))
+                             M=g["M"], N=g["N"], K=g["K"], **{k: round(v, 4) for k, v in acc[gi].items()}))
 
     # ---- cuBLAS BF16 baseline (same GEMMs, same flush protocol)
     ms_cub = None
     if not args.no_cublas:
-        ms_cub, _ = timed(step_cublas, args.steps, args.warmup)
+        ms_cub, _ = timed(as_graph(step_cublas), args.steps, args.warmup)
 
     # ---- e2e: pinned host inputs in, outputs out, inside the timed region
     e2e = None
@@ -439,7 +459,8 @@ def main():
                 if ms_cub else None,
                 "stages_ms_per_step": {k: round(v, 4) for k, v in stage_tot.items()},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-                "gpu_launches": int(launches_per_step * args.steps)}
+                "gpu_launches": int(launches_per_step * args.steps),
+                "launch": "eager" if args.no_graph else "cuda_graph"}
         print(json.dumps(line), flush=True)
         with open(os.path.join(ROOT, "gpurun_out", "bench_per_gemm.json") if os.path.isdir(
                 os.path.join(ROOT, "gpurun_out")) else os.devnull, "w") as f:

@@ -19,7 +19,14 @@ thread_local int32_t g_launches = 0;
 thread_local cudaEvent_t* g_stage_events = nullptr;  // optional per-stage timing (bench)
 
 inline void stage_mark(int i, cudaStream_t st) {
-  if (g_stage_events) cudaEventRecord(g_stage_events[i], st);
+  if (!g_stage_events) return;
+  // inside CUDA-graph capture an "external" record node keeps the event observable
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (cap == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(g_stage_events[i], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(g_stage_events[i], st);
 }
 
 // ---------------------------------------------------------------------- driver / device
@@ -96,7 +103,7 @@ struct GemmPlan {
   int64_t npad = 0;
   int splits = 1;
   size_t qa_codes = 0, qa_sf = 0, qb_codes = 0, qb_sf = 0;
-  size_t keys = 0, cand_key = 0, cand_idx = 0, idx = 0, slice = 0, part = 0;
+  size_t keys = 0, idx = 0, slice = 0, part = 0;
   size_t total = 0;
 };
 
@@ -117,10 +124,7 @@ bool plan_gemm(int64_t M, int64_t N, int64_t K, adahop_strategy_t s, const adaho
     g->rows_oe = s == ADAHOP_OE_LEFT_IHT ? M : N;
     g->mbig = s == ADAHOP_OE_LEFT_IHT ? N : M;
     g->kk = int(std::min<int64_t>(p->oe_k, g->rows_oe));
-    const int64_t nch = (g->rows_oe + kFoidChunkRows - 1) / kFoidChunkRows;
     g->keys = c.take(size_t(g->rows_oe) * 8);
-    g->cand_key = c.take(size_t(nch) * g->kk * 8);
-    g->cand_idx = c.take(size_t(nch) * g->kk * 4);
     g->idx = c.take(size_t(g->kk) * 4);
     g->slice = c.take(size_t(g->kk) * size_t(K) * 2);
     g->npad = bf16_gemm_npad(g->kk);
@@ -321,10 +325,6 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   GemmPlan g;
   plan_gemm(M, N, K, s, p, dev.sms, &g);
   if (!ws || ws_bytes < g.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
-  if (g.kk > 0) {
-    const int64_t nch = (g.rows_oe + kFoidChunkRows - 1) / kFoidChunkRows;
-    if (nch * g.kk > 8192) return ADAHOP_E_UNSUPPORTED;
-  }
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
   const bool out_f32 = out_dt == ADAHOP_DT_F32;
@@ -359,25 +359,25 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   if ((M % 128) || (K % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(qa_sf, 0, size_t(sf_bytes(M, K)), cs));
   if ((N % 128) || (K % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(qb_sf, 0, size_t(sf_bytes(N, K)), cs));
 
-  // ---- 1. FOID + outlier slice (P:760 stage 1)
+  // ---- 1. FOID (P:760 stage 1): probe keys + top-k indices (device-resident)
   const void* oe_src = oe_left ? A : B;
   const int oe_ks = oe_left ? a_kstrided : b_kstrided;
   const int64_t oe_ld = oe_left ? lda : ldb;
   __nv_bfloat16* slice = g.kk > 0 ? reinterpret_cast<__nv_bfloat16*>(w + g.slice) : nullptr;
   if (g.kk > 0) {
     ADAHOP_LAUNCH(launch_foid(oe_src, false, g.rows_oe, K, oe_ld, oe_ks, g.kk, p->foid_probe,
-                              reinterpret_cast<double*>(w + g.keys),
-                              reinterpret_cast<double*>(w + g.cand_key),
-                              reinterpret_cast<int32_t*>(w + g.cand_idx), idx, cs));
-    ADAHOP_LAUNCH(launch_gather(oe_src, K, oe_ld, oe_ks, idx, g.kk, slice, cs));
-    launches += 4;
+                              reinterpret_cast<double*>(w + g.keys), idx, cs));
+    launches += 2;
   }
   stage_mark(1, cs);
-  // ---- 2. IHT + MXFP4 quantisation of both operands (P:761 stage 2), residual masked
+  // ---- 2. IHT + MXFP4 quantisation of both operands (P:761 stage 2); the OE rows are
+  //         zeroed in the residual and gathered into the BF16 outlier slice in the same pass
   ADAHOP_LAUNCH(launch_iht_quant(A, false, M, K, lda, a_kstrided, oe_left ? idx : nullptr,
-                                 oe_left ? g.kk : 0, qa, qa_sf, nullptr, false, cs));
+                                 oe_left ? g.kk : 0, qa, qa_sf, nullptr, oe_left ? slice : nullptr,
+                                 false, cs));
   ADAHOP_LAUNCH(launch_iht_quant(B, false, N, K, ldb, b_kstrided, oe_right ? idx : nullptr,
-                                 oe_right ? g.kk : 0, qb, qb_sf, nullptr, false, cs));
+                                 oe_right ? g.kk : 0, qb, qb_sf, nullptr, oe_right ? slice : nullptr,
+                                 false, cs));
   launches += 2;
   stage_mark(2, cs);
   // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
@@ -450,9 +450,6 @@ size_t adahop_debug_workspace_bytes(int64_t R, int64_t K) {
   Carver c;
   c.take(size_t(sf_bytes(R, K)));
   c.take(size_t(R) * 8);                                   // FOID keys
-  const int64_t nch = (R + kFoidChunkRows - 1) / kFoidChunkRows;
-  c.take(size_t(nch) * 256 * 8);
-  c.take(size_t(nch) * 256 * 4);
   return c.take(0) + 256;
 }
 
@@ -474,7 +471,7 @@ adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* sf = static_cast<uint8_t*>(ws);
   ADAHOP_LAUNCH(launch_iht_quant(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, zero_rows, nzero,
-                                 codes_canon, sf, had_out, false, cs));
+                                 codes_canon, sf, had_out, nullptr, false, cs));
   ADAHOP_LAUNCH(launch_sf_convert(sf, R, K, scales_canon, true, cs));
   g_launches = 2;
   return ADAHOP_OK;
@@ -490,19 +487,15 @@ adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, 
   if (ld < (k_strided ? R : K)) return ADAHOP_E_INVALID_ARG;
   if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
   const int64_t kk = std::min<int64_t>(k, R);
-  const int64_t nch = (R + kFoidChunkRows - 1) / kFoidChunkRows;
-  if (nch * kk > 8192) return ADAHOP_E_UNSUPPORTED;
   adahop_status_t st = check_device(nullptr);
   if (st != ADAHOP_OK) return st;
   Carver c;
   uint8_t* w = static_cast<uint8_t*>(ws);
   c.take(size_t(sf_bytes(R, K)));
   double* keys = reinterpret_cast<double*>(w + c.take(size_t(R) * 8));
-  double* ck = reinterpret_cast<double*>(w + c.take(size_t(nch) * 256 * 8));
-  int32_t* ci = reinterpret_cast<int32_t*>(w + c.take(size_t(nch) * 256 * 4));
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-  ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys, ck,
-                            ci, idx_sorted, cs));
+  ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys,
+                            idx_sorted, cs));
   if (keys_out)
     ADAHOP_LAUNCH(cudaMemcpyAsync(keys_out, keys, size_t(R) * 8, cudaMemcpyDeviceToDevice, cs));
   g_launches = 3;

@@ -30,16 +30,16 @@ __device__ __forceinline__ float load_as_float(const __nv_bfloat16* p, int64_t i
 }
 __device__ __forceinline__ float load_as_float(const float* p, int64_t i) { return p[i]; }
 
-// Binary search in a sorted device list of at most a few hundred indices.
-__device__ __forceinline__ bool in_sorted(const int32_t* idx, int n, int64_t v) {
+// Position of v in a sorted device list of at most a few hundred indices, or -1.
+__device__ __forceinline__ int find_sorted(const int32_t* idx, int n, int64_t v) {
   int lo = 0, hi = n - 1;
   while (lo <= hi) {
-    int mid = (lo + hi) >> 1;
-    int64_t x = idx[mid];
-    if (x == v) return true;
+    const int mid = (lo + hi) >> 1;
+    const int64_t x = __ldg(idx + mid);
+    if (x == v) return mid;
     if (x < v) lo = mid + 1; else hi = mid - 1;
   }
-  return false;
+  return -1;
 }
 
 }  // namespace adahop

@@ -12,6 +12,7 @@
 // issuer, warp 2 = TMEM allocator, all 4 warps run the epilogue.
 #include "common.cuh"
 #include "kernels.h"
+#include "epilogue.cuh"
 #include "ptx.cuh"
 
 namespace adahop {
@@ -38,7 +39,7 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 4 * kEpiStageBytes + 1024 + 256;
 };
 
 // Load one operand tile of `rows` x 64(K) into smem (128B swizzle).
@@ -69,7 +70,8 @@ __global__ void __launch_bounds__(kThreads)
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(kStages) * G::kStageBytes);
+  uint8_t* epi_smem = smem + size_t(kStages) * G::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + 4 * kEpiStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* done = bars + 2 * kStages;
@@ -137,28 +139,55 @@ __global__ void __launch_bounds__(kThreads)
     ptx::tc_fence_after();
   }
   __syncwarp();
-  const int64_t m = m0 + warp * 32 + lane;
-  for (int c = 0; c < BN / 32 + (BN % 32 ? 1 : 0); ++c) {
-    uint32_t r[32];
+  // coalesced store through the per-warp smem stage (epilogue.cuh)
+  uint8_t* stg = epi_smem + warp * kEpiStageBytes;
+  const int64_t mw = m0 + warp * 32;
+  const int rows_valid = int(Mb - mw < 32 ? (Mb - mw > 0 ? Mb - mw : 0) : 32);
+  char* cbase;
+  int64_t ldb_bytes, ncols;
+  int elt;
+  if (mode == 1) {
+    elt = 4;
+    cbase = reinterpret_cast<char*>(part + (int64_t(split) * Mb + mw) * npad);
+    ldb_bytes = npad * 4;
+    ncols = npad;
+  } else {
+    elt = out_f32 ? 4 : 2;
+    cbase = static_cast<char*>(C) + mw * ldc * elt;
+    ldb_bytes = ldc * elt;
+    ncols = Nb;
+  }
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(cbase) | uintptr_t(ldb_bytes)) & 15) == 0;
+  const int cols_per_grp = 128 / elt;
+#pragma unroll 1
+  for (int g = 0; g < (BN + cols_per_grp - 1) / cols_per_grp; ++g) {
+    const int64_t nc = n0 + g * cols_per_grp;
+    uint32_t w[32];
+    uint32_t r0[32], r1[32];
+    const uint32_t tb = tmem_base + ((warp * 32) << 16) + g * cols_per_grp;
     if (has_k) {
-      ptx::tmem_ld_32x32b_x32(tmem_base + ((warp * 32) << 16) + c * 32, r);
+      ptx::tmem_ld_32x32b_x32(tb, r0);
+      if (elt == 2) ptx::tmem_ld_32x32b_x32(tb + 32, r1);
       ptx::tmem_ld_wait();
     } else {
 #pragma unroll
-      for (int v = 0; v < 32; ++v) r[v] = 0u;
+      for (int v = 0; v < 32; ++v) { r0[v] = 0u; r1[v] = 0u; }
     }
-    if (m >= Mb) continue;
-    const int64_t nc = n0 + c * 32;
-    if (mode == 1) {
-      float* prow = part + (int64_t(split) * Mb + m) * npad + nc;
-      for (int v = 0; v < 32 && nc + v < npad; ++v) prow[v] = __uint_as_float(r[v]);
-    } else if (out_f32) {
-      float* crow = static_cast<float*>(C) + m * ldc + nc;
-      for (int v = 0; v < 32 && nc + v < Nb; ++v) crow[v] = __uint_as_float(r[v]);
+    if (elt == 4) {
+#pragma unroll
+      for (int v = 0; v < 32; ++v) w[v] = r0[v];
     } else {
-      __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(C) + m * ldc + nc;
-      for (int v = 0; v < 32 && nc + v < Nb; ++v) crow[v] = __float2bfloat16_rn(__uint_as_float(r[v]));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        w[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
+        w[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
+      }
     }
+    const int64_t nrem = ncols - nc;
+    const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
+    if (rows_valid > 0 && bytes_valid > 0)
+      epi_store_rows128(stg, w, cbase + nc * elt, ldb_bytes, rows_valid, bytes_valid,
+                        elt, vec_ok);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -168,19 +197,45 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Deterministic split-K fold + scatter into C.
-__global__ void k_outlier_reduce(const float* __restrict__ part, int splits, int64_t Mb,
-                                 int64_t npad, int k, const int32_t* __restrict__ idx,
-                                 int scatter_cols, void* C, int out_f32, int64_t ldc) {
-  const int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y;
-  if (m >= Mb || j >= k) return;
-  float v = 0.f;
-  for (int s = 0; s < splits; ++s) v += part[(int64_t(s) * Mb + m) * npad + j];
-  const int64_t col = idx[j];
-  const int64_t off = scatter_cols ? m * ldc + col : col * ldc + m;
-  if (out_f32) static_cast<float*>(C)[off] = v;
-  else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(v);
+// Deterministic split-K fold + scatter into C, through a 32 x 32 smem tile so that both
+// the partial reads (along j) and the OE-Left row writes (along m) are coalesced.
+__global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict__ part, int splits,
+                                                        int64_t Mb, int64_t npad, int k,
+                                                        const int32_t* __restrict__ idx,
+                                                        int scatter_cols, void* C, int out_f32,
+                                                        int64_t ldc) {
+  __shared__ float tile[32][33];
+  const int64_t m0 = int64_t(blockIdx.x) * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int mm = ty; mm < 32; mm += 8) {
+    const int64_t m = m0 + mm;
+    const int j = j0 + tx;
+    float v = 0.f;
+    if (m < Mb && j < k)
+      for (int s = 0; s < splits; ++s) v += part[(int64_t(s) * Mb + m) * npad + j];
+    tile[mm][tx] = v;
+  }
+  __syncthreads();
+  if (scatter_cols) {  // OE-Right: C[m][idx[j]]
+    for (int mm = ty; mm < 32; mm += 8) {
+      const int64_t m = m0 + mm;
+      const int j = j0 + tx;
+      if (m >= Mb || j >= k) continue;
+      const int64_t off = m * ldc + idx[j];
+      if (out_f32) static_cast<float*>(C)[off] = tile[mm][tx];
+      else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(tile[mm][tx]);
+    }
+  } else {             // OE-Left (transposed product): C[idx[j]][m]
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int j = j0 + jj;
+      const int64_t m = m0 + tx;
+      if (m >= Mb || j >= k) continue;
+      const int64_t off = int64_t(idx[j]) * ldc + m;
+      if (out_f32) static_cast<float*>(C)[off] = tile[tx][jj];
+      else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(tile[tx][jj]);
+    }
+  }
 }
 
 }  // namespace bf16g
@@ -195,7 +250,7 @@ int64_t bf16_gemm_npad(int64_t Nb) {
 int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms) {
   const int64_t mt = (Mb + bf16g::BM - 1) / bf16g::BM;
   const int64_t nks = (K + bf16g::BK - 1) / bf16g::BK;
-  int64_t s = (2 * num_sms + mt - 1) / mt;  // ~2 CTAs per SM
+  int64_t s = (2 * num_sms) / mt;            // one full wave of ~2 CTAs per SM
   if (s > nks) s = nks;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
@@ -256,8 +311,8 @@ cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st) {
 cudaError_t launch_outlier_reduce(const float* part, int splits, int64_t Mb, int64_t npad, int k,
                                   const int32_t* idx, bool scatter_cols, void* C, bool out_f32,
                                   int64_t ldc, cudaStream_t st) {
-  dim3 grid(unsigned((Mb + 255) / 256), unsigned(k));
-  bf16g::k_outlier_reduce<<<grid, 256, 0, st>>>(part, splits, Mb, npad, k, idx, scatter_cols ? 1 : 0,
+  dim3 grid(unsigned((Mb + 31) / 32), unsigned((k + 31) / 32));
+  bf16g::k_outlier_reduce<<<grid, dim3(32, 8), 0, st>>>(part, splits, Mb, npad, k, idx, scatter_cols ? 1 : 0,
                                                 C, out_f32 ? 1 : 0, ldc);
   return cudaGetLastError();
 }

@@ -15,6 +15,7 @@
 //               the MMA warp already accumulates the next tile into the other buffer.
 #include "common.cuh"
 #include "kernels.h"
+#include "epilogue.cuh"
 #include "ptx.cuh"
 
 namespace adahop {
@@ -34,7 +35,8 @@ constexpr int kAccCols = BN;            // per accumulator buffer
 constexpr int kSfCol = 2 * kAccCols;    // first TMEM column of the scale factors
 constexpr int kSfbColOff = 8;           // SFB after the 8 SFA columns
 constexpr int kThreads = 256;
-constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kEpiBytes = 4 * kEpiStageBytes;   // one staging block per epilogue warp
+constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 // Instruction descriptor, kind::mxf4 block-scaled (E2M1 x E2M1, UE8M0, fp32 accumulate).
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
@@ -51,7 +53,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(kStages) * kStageBytes);
+  uint8_t* epi_smem = smem + size_t(kStages) * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
@@ -157,41 +160,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = uint32_t(lt >> 1);
       ptx::mbar_wait(&tfull[buf], use & 1);
       ptx::tc_fence_after();
-      const int64_t m = mb * BM + q * 32 + lane;
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + buf * kAccCols + c * 32, r);
-        ptx::tmem_ld_wait();
-        const int64_t n0 = nb * BN + c * 32;
-        if (m < M) {
-          if (out_f32) {
-            float* crow = static_cast<float*>(C) + m * ldc + n0;
-            if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+      // coalesced store through the per-warp smem stage: 128 bytes of each row at a time
+      uint8_t* stg = epi_smem + q * kEpiStageBytes;
+      const int64_t m0 = mb * BM + q * 32;
+      const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
+      const int elt = out_f32 ? 4 : 2;
+      const int cols_per_grp = 128 / elt;            // 32 fp32 or 64 bf16 columns
+      const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
+#pragma unroll 1
+      for (int g = 0; g < BN / cols_per_grp; ++g) {
+        const int64_t n0 = nb * BN + g * cols_per_grp;
+        const uint32_t tbase = tmem_base + ((q * 32) << 16) + buf * kAccCols + g * cols_per_grp;
+        uint32_t w[32];
+        if (out_f32) {
+          ptx::tmem_ld_32x32b_x32(tbase, w);
+          ptx::tmem_ld_wait();
+        } else {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld_32x32b_x32(tbase, r0);
+          ptx::tmem_ld_32x32b_x32(tbase + 32, r1);
+          ptx::tmem_ld_wait();
 #pragma unroll
-              for (int v = 0; v < 8; ++v)
-                reinterpret_cast<uint4*>(crow)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-            } else {
-              for (int v = 0; v < 32 && n0 + v < N; ++v) crow[v] = __uint_as_float(r[v]);
-            }
-          } else {
-            __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(C) + m * ldc + n0;
-            if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
-#pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint32_t w[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * t]),
-                                                           __uint_as_float(r[8 * v + 2 * t + 1]));
-                  w[t] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                reinterpret_cast<uint4*>(crow)[v] = make_uint4(w[0], w[1], w[2], w[3]);
-              }
-            } else {
-              for (int v = 0; v < 32 && n0 + v < N; ++v) crow[v] = __float2bfloat16_rn(__uint_as_float(r[v]));
-            }
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
+            w[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
           }
         }
+        const int64_t nrem = N - n0;
+        const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
+        if (rows_valid > 0 && bytes_valid > 0)
+          epi_store_rows128(stg, w, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid,
+                            bytes_valid, elt, vec_ok);
       }
       ptx::tc_fence_before();
       __syncwarp();

@@ -8,17 +8,18 @@
 namespace adahop {
 
 // quant.cu
+// zero_rows (sorted, nzero) are the OE rows: masked to +0 in the residual and, when
+// slice != nullptr, copied raw (bf16) into slice[slot][0..K) — the outlier gather is fused.
 cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
-                             uint8_t* sf, float* had_out, bool sw_cvt, cudaStream_t st);
+                             uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
+                             cudaStream_t st);
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
+// FOID: probe keys (keys[R], fp64) + single-CTA radix top-k -> idx_sorted[min(k,R)].
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
-                        int kstrided, int k, int probe, double* keys, double* cand_key,
-                        int32_t* cand_idx, int32_t* idx_sorted, cudaStream_t st);
-constexpr int kFoidChunkRows = 2048;
-cudaError_t launch_gather(const void* in, int64_t K, int64_t ld, int kstrided, const int32_t* idx,
-                          int k, __nv_bfloat16* out, cudaStream_t st);
+                        int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
+                        cudaStream_t st);
 int64_t stats_chunks(int64_t R);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);

@@ -130,6 +130,21 @@ __device__ __forceinline__ void load32(const float* p, float (&x)[32]) {
   }
 }
 
+// 32 raw values -> 64 contiguous bytes of the bf16 outlier slice (RN for fp32 inputs).
+__device__ __forceinline__ void store_slice32(__nv_bfloat16* dst, const float (&x)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t w[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(x[8 * j + 2 * t], x[8 * j + 2 * t + 1]);
+      w[t] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    d[j] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 // Row variant: stored row r is in[r*ld + 0..K). One thread per (row, 32-block).
 template <typename T, bool kHad, bool kSwCvt>
 __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in, int64_t R,
@@ -137,18 +152,21 @@ __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in,
                                                        const int32_t* __restrict__ zero_rows,
                                                        int nzero, uint8_t* __restrict__ codes,
                                                        uint8_t* __restrict__ sf, int64_t kchunks,
-                                                       float* __restrict__ had_out) {
+                                                       float* __restrict__ had_out,
+                                                       __nv_bfloat16* __restrict__ slice) {
   const int64_t nkb = K / kBlk;
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= R * nkb) return;
   const int64_t r = t / nkb;
   const int64_t kb = t - r * nkb;
   float x[32];
-  if (nzero > 0 && in_sorted(zero_rows, nzero, r)) {
+  load32(in + r * ld + kb * kBlk, x);
+  const int slot = nzero > 0 ? find_sorted(zero_rows, nzero, r) : -1;
+  if (slot >= 0) {
+    // OE: the raw row goes to the BF16 outlier slice, the residual row is zero
+    if (slice) store_slice32(slice + int64_t(slot) * K + kb * kBlk, x);
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = 0.f;
-  } else {
-    load32(in + r * ld + kb * kBlk, x);
   }
   uint4 c;
   uint32_t s;
@@ -165,7 +183,8 @@ __global__ void __launch_bounds__(256) k_iht_quant_col(const T* __restrict__ in,
                                                        const int32_t* __restrict__ zero_rows,
                                                        int nzero, uint8_t* __restrict__ codes,
                                                        uint8_t* __restrict__ sf, int64_t kchunks,
-                                                       float* __restrict__ had_out) {
+                                                       float* __restrict__ had_out,
+                                                       __nv_bfloat16* __restrict__ slice) {
   constexpr int TK = 64, TR = 128;
   __shared__ __align__(16) T tile[TK][TR];
   const int64_t r0 = int64_t(blockIdx.x) * TR;
@@ -194,12 +213,13 @@ __global__ void __launch_bounds__(256) k_iht_quant_col(const T* __restrict__ in,
   const int64_t kb = k0 / kBlk + kbl;
   if (r >= R || kb * kBlk >= K) return;
   float x[32];
-  if (nzero > 0 && in_sorted(zero_rows, nzero, r)) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = float(tile[kbl * 32 + i][rr]);
+  const int slot = nzero > 0 ? find_sorted(zero_rows, nzero, r) : -1;
+  if (slot >= 0) {
+    if (slice) store_slice32(slice + int64_t(slot) * K + kb * kBlk, x);
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = 0.f;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = float(tile[kbl * 32 + i][rr]);
   }
   uint4 c;
   uint32_t s;
@@ -212,27 +232,28 @@ __global__ void __launch_bounds__(256) k_iht_quant_col(const T* __restrict__ in,
 template <typename T, bool kHad, bool kSw>
 static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld, int kstrided,
                                   const int32_t* zero_rows, int nzero, uint8_t* codes, uint8_t* sf,
-                                  float* had_out, cudaStream_t st) {
+                                  float* had_out, __nv_bfloat16* slice, cudaStream_t st) {
   const int64_t kch = sf_kchunks(K);
   if (!kstrided) {
     const int64_t n = R * (K / kBlk);
     const int64_t blocks = (n + 255) / 256;
     k_iht_quant_row<T, kHad, kSw><<<dim3(unsigned(blocks)), 256, 0, st>>>(
-        in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out);
+        in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out, slice);
   } else {
     dim3 grid(unsigned((R + 127) / 128), unsigned((K + 63) / 64));
     k_iht_quant_col<T, kHad, kSw><<<grid, 256, 0, st>>>(in, R, K, ld, zero_rows, nzero, codes,
-                                                         sf, kch, had_out);
+                                                         sf, kch, had_out, slice);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
-                             uint8_t* sf, float* had_out, bool sw_cvt, cudaStream_t st) {
+                             uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
+                             cudaStream_t st) {
 #define ADAHOP_Q(T, H, S)                                                                   \
   return launch_quant_t<T, H, S>(static_cast<const T*>(in), R, K, ld, kstrided, zero_rows, \
-                                 nzero, codes, sf, had_out, st)
+                                 nzero, codes, sf, had_out, slice, st)
   const bool had = had_out != nullptr;
   if (in_f32) {
     if (had) { if (sw_cvt) ADAHOP_Q(float, true, true); else ADAHOP_Q(float, true, false); }
@@ -273,152 +294,198 @@ cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t*
 // ================================================================== FOID
 // Key of stored row r: population variance of its first p K-elements, fp64, summed
 // sequentially with separate multiply and add (no FMA), matching the oracle bitwise.
-template <typename T>
-__global__ void k_foid_keys(const T* __restrict__ in, int64_t R, int64_t ld, int kstrided, int p,
-                            double* __restrict__ keys) {
-  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= R) return;
+__device__ __forceinline__ double foid_key_seq(const float* x, int p) {
   double s = 0.0;
-  for (int j = 0; j < p; ++j) {
-    const double x = double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j));
-    s = __dadd_rn(s, x);
-  }
+  for (int j = 0; j < p; ++j) s = __dadd_rn(s, double(x[j]));
   const double mu = s / double(p);
   double v = 0.0;
   for (int j = 0; j < p; ++j) {
-    const double x = double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j));
-    const double d = __dsub_rn(x, mu);
+    const double d = __dsub_rn(double(x[j]), mu);
     v = __dadd_rn(v, __dmul_rn(d, d));
   }
-  keys[r] = v / double(p);
+  return v / double(p);
 }
 
-// (key, index) order: larger key first, equal keys -> lower index first.
-__device__ __forceinline__ bool foid_before(double ka, int32_t ia, double kb, int32_t ib) {
-  return ka > kb || (ka == kb && ia < ib);
+constexpr int kProbeMax = 64;  // probe lengths above this take the generic path
+
+// K-strided operand (stored row r = column r of a [K][R] array): the probe is the first p
+// rows of the source, read coalesced (thread per r).
+// K-contiguous operand: a warp stages the probes of its 32 rows into shared memory with
+// 16-byte loads, then each lane folds its own row.
+template <typename T>
+__global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int64_t R, int64_t ld,
+                                                   int kstrided, int p, double* __restrict__ keys) {
+  __shared__ __align__(16) float stage[4][32][kProbeMax + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p > kProbeMax) {  // generic (slow) path
+    if (r >= R) return;
+    double s = 0.0;
+    for (int j = 0; j < p; ++j)
+      s = __dadd_rn(s, double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)));
+    const double mu = s / double(p);
+    double v = 0.0;
+    for (int j = 0; j < p; ++j) {
+      const double d = __dsub_rn(double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)), mu);
+      v = __dadd_rn(v, __dmul_rn(d, d));
+    }
+    keys[r] = v / double(p);
+    return;
+  }
+  float* mine = stage[warp][lane];
+  if (kstrided) {
+    if (r < R)
+      for (int j = 0; j < p; ++j) mine[j] = load_as_float(in, int64_t(j) * ld + r);
+  } else {
+    const int64_t rw = int64_t(blockIdx.x) * blockDim.x + warp * 32;  // first row of this warp
+    // cooperative: lane handles element (row = rw + e / p, col = e % p) for e strided by 32
+    for (int e = lane; e < 32 * p; e += 32) {
+      const int rr = e / p, c = e % p;
+      if (rw + rr < R) stage[warp][rr][c] = load_as_float(in, (rw + rr) * ld + c);
+    }
+    __syncwarp();
+  }
+  if (r < R) keys[r] = foid_key_seq(mine, p);
 }
 
-// Bitonic sort of n (power of two) (key, idx) pairs in shared memory, "before" order.
-__device__ void bitonic_sort_pairs(double* key, int32_t* idx, int n) {
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool up = (i & size) == 0;
-          const bool sw = up ? foid_before(key[j], idx[j], key[i], idx[i])
-                             : foid_before(key[i], idx[i], key[j], idx[j]);
-          if (sw) {
-            const double tk = key[i]; key[i] = key[j]; key[j] = tk;
-            const int32_t ti = idx[i]; idx[i] = idx[j]; idx[j] = ti;
+// Top-k by (key desc, index asc), written as ascending indices. One CTA: an 8-pass MSB-first
+// radix select (8-bit digits of the fp64 key bits, order-preserving for keys >= 0) finds the
+// k-th largest key T; then all keys > T plus the lowest-indexed keys == T are taken, and a
+// block scan in index order writes them sorted.
+constexpr int kSelThreads = 1024;
+constexpr int64_t kSelSmemKeys = 24576;   // keys staged in smem up to this many rows
+
+__device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[32]*/, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sbuf[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (blockDim.x >> 5) ? sbuf[lane] : 0;
+    int ws = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += y;
+    }
+    sbuf[lane] = ws - w;               // exclusive warp offsets
+    if (lane == 31) sbuf[32] = ws;     // total
+  }
+  __syncthreads();
+  const int res = sbuf[warp] + x - v;
+  *total = sbuf[32];
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __restrict__ keys, int64_t R,
+                                                             int k, int32_t* __restrict__ idx_sorted) {
+  extern __shared__ __align__(16) unsigned long long skeys[];
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_kr;
+  __shared__ int sbuf[33];
+  const bool in_smem = R <= kSelSmemKeys;
+  const unsigned long long* kb = in_smem ? skeys : reinterpret_cast<const unsigned long long*>(keys);
+  if (in_smem)
+    for (int64_t i = threadIdx.x; i < R; i += blockDim.x)
+      skeys[i] = __double_as_longlong(keys[i]);
+  const int kk = int(int64_t(k) < R ? int64_t(k) : R);
+  unsigned long long prefix = 0;
+  int kr = kk;
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < R; i += blockDim.x) {
+      const unsigned long long u = kb[i];
+      if (pass == 0 || (u >> (shift + 8)) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // lane l owns digits 255-8l .. 248-8l (descending); find the digit holding rank kr
+      const int lane = threadIdx.x;
+      int cnt[8], tot = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { cnt[t] = int(hist[255 - 8 * lane - t]); tot += cnt[t]; }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - tot;
+      if (excl < kr && kr <= incl) {
+        int c = excl;
+        for (int t = 0; t < 8; ++t) {
+          if (c + cnt[t] >= kr) {
+            s_prefix = (prefix << 8) | (unsigned long long)(255 - 8 * lane - t);
+            s_kr = kr - c;
+            break;
           }
+          c += cnt[t];
         }
       }
-      __syncthreads();
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    kr = s_kr;
+    __syncthreads();
+  }
+  const unsigned long long T = prefix;   // the kk-th largest key; take kr of the keys == T
+  // per-thread contiguous index segment
+  const int64_t seg = (R + blockDim.x - 1) / blockDim.x;
+  const int64_t i0 = (int64_t(threadIdx.x) * seg < R ? int64_t(threadIdx.x) * seg : R);
+  const int64_t i1 = (i0 + seg < R ? i0 + seg : R);
+  int n_eq = 0;
+  for (int64_t i = i0; i < i1; ++i) n_eq += kb[i] == T;
+  int tot_eq;
+  int eq_before = block_excl_scan(n_eq, sbuf, &tot_eq);
+  int n_sel = 0;
+  {
+    int e = eq_before;
+    for (int64_t i = i0; i < i1; ++i) {
+      const unsigned long long u = kb[i];
+      if (u > T) ++n_sel;
+      else if (u == T) { if (e < kr) ++n_sel; ++e; }
+    }
+  }
+  int tot_sel;
+  int pos = block_excl_scan(n_sel, sbuf, &tot_sel);
+  {
+    int e = eq_before;
+    for (int64_t i = i0; i < i1; ++i) {
+      const unsigned long long u = kb[i];
+      bool take = false;
+      if (u > T) take = true;
+      else if (u == T) { take = e < kr; ++e; }
+      if (take) idx_sorted[pos++] = int32_t(i);
     }
   }
 }
 
-constexpr int kFoidChunk = 2048;
-
-// Top-k of each chunk of kFoidChunk rows.
-__global__ void __launch_bounds__(1024) k_foid_chunk_topk(const double* __restrict__ keys, int64_t R,
-                                                          int k, double* __restrict__ cand_key,
-                                                          int32_t* __restrict__ cand_idx) {
-  __shared__ double skey[kFoidChunk];
-  __shared__ int32_t sidx[kFoidChunk];
-  const int64_t base = int64_t(blockIdx.x) * kFoidChunk;
-  for (int i = threadIdx.x; i < kFoidChunk; i += blockDim.x) {
-    const int64_t r = base + i;
-    skey[i] = r < R ? keys[r] : -1.0;
-    sidx[i] = r < R ? int32_t(r) : INT32_MAX;
-  }
-  __syncthreads();
-  bitonic_sort_pairs(skey, sidx, kFoidChunk);
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    cand_key[int64_t(blockIdx.x) * k + i] = skey[i];
-    cand_idx[int64_t(blockIdx.x) * k + i] = sidx[i];
-  }
-}
-
-// Merge the candidates (ncand <= 8192), keep the global top-k, write indices ascending.
-__global__ void __launch_bounds__(1024) k_foid_merge(const double* __restrict__ cand_key,
-                                                     const int32_t* __restrict__ cand_idx,
-                                                     int ncand, int npow2, int k, int64_t R,
-                                                     int32_t* __restrict__ idx_sorted) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* skey = reinterpret_cast<double*>(smem_raw);
-  int32_t* sidx = reinterpret_cast<int32_t*>(skey + npow2);
-  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-    skey[i] = i < ncand ? cand_key[i] : -1.0;
-    sidx[i] = i < ncand ? cand_idx[i] : INT32_MAX;
-  }
-  __syncthreads();
-  bitonic_sort_pairs(skey, sidx, npow2);
-  // rank-sort the first kk indices ascending
-  const int kk = int(int64_t(k) < R ? int64_t(k) : R);
-  __shared__ int32_t top[256];
-  for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = sidx[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
-    int rank = 0;
-    for (int j = 0; j < kk; ++j) rank += top[j] < top[i];
-    idx_sorted[rank] = top[i];
-  }
-}
-
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
-                        int kstrided, int k, int probe, double* keys, double* cand_key,
-                        int32_t* cand_idx, int32_t* idx_sorted, cudaStream_t st) {
+                        int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
+                        cudaStream_t st) {
   const int p = int(std::min<int64_t>(probe, K));
-  const unsigned kb = unsigned((R + 255) / 256);
-  if (in_f32) k_foid_keys<float><<<kb, 256, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
-  else k_foid_keys<__nv_bfloat16><<<kb, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
-  const int kk = int(std::min<int64_t>(k, R));
-  const int nchunks = int((R + kFoidChunk - 1) / kFoidChunk);
-  k_foid_chunk_topk<<<nchunks, 1024, 0, st>>>(keys, R, kk, cand_key, cand_idx);
-  const int ncand = nchunks * kk;
-  int npow2 = 1;
-  while (npow2 < ncand) npow2 <<= 1;
-  const size_t smem = size_t(npow2) * (sizeof(double) + sizeof(int32_t));
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_foid_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const unsigned kb = unsigned((R + 127) / 128);
+  if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
+  else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
+  const size_t smem = R <= kSelSmemKeys ? size_t(R) * 8 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSelSmemKeys * 8));
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
-  k_foid_merge<<<1, 1024, smem, st>>>(cand_key, cand_idx, ncand, npow2, kk, R, idx_sorted);
-  return cudaGetLastError();
-}
-
-// Outlier slice (bf16, k x K, K contiguous): out[s][j] = store(idx[s], j).
-__global__ void k_gather_rows_kc(const __nv_bfloat16* __restrict__ in, int64_t K, int64_t ld,
-                                 const int32_t* __restrict__ idx, __nv_bfloat16* __restrict__ out) {
-  const int s = blockIdx.y;
-  const int64_t r = idx[s];
-  const uint4* src = reinterpret_cast<const uint4*>(in + r * ld);
-  uint4* dst = reinterpret_cast<uint4*>(out + int64_t(s) * K);
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < K / 8;
-       v += int64_t(gridDim.x) * blockDim.x)
-    dst[v] = __ldg(src + v);
-}
-__global__ void k_gather_rows_ks(const __nv_bfloat16* __restrict__ in, int64_t K, int64_t ld,
-                                 const int32_t* __restrict__ idx, int k,
-                                 __nv_bfloat16* __restrict__ out) {
-  // warp w of the CTA handles slot s = blockIdx.y*8 + w, 32 consecutive k-positions per lane-loop
-  const int s = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (s >= k) return;
-  const int64_t r = idx[s];
-  for (int64_t t = int64_t(blockIdx.x) * 32 + (threadIdx.x & 31); t < K; t += int64_t(gridDim.x) * 32)
-    out[int64_t(s) * K + t] = in[t * ld + r];
-}
-cudaError_t launch_gather(const void* in, int64_t K, int64_t ld, int kstrided,
-                          const int32_t* idx, int k, __nv_bfloat16* out, cudaStream_t st) {
-  const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(in);
-  if (!kstrided) {
-    const unsigned gx = unsigned(std::min<int64_t>((K / 8 + 255) / 256, int64_t(64)));
-    k_gather_rows_kc<<<dim3(gx, unsigned(k)), 256, 0, st>>>(src, K, ld, idx, out);
-  } else {
-    const unsigned gx = unsigned(std::min<int64_t>((K + 31) / 32, int64_t(512)));
-    k_gather_rows_ks<<<dim3(gx, unsigned((k + 7) / 8)), 256, 0, st>>>(src, K, ld, idx, k, out);
-  }
+  k_foid_select<<<1, kSelThreads, smem, st>>>(keys, R, k, idx_sorted);
   return cudaGetLastError();
 }
 

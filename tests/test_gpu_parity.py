@@ -115,7 +115,8 @@ def test_iht_quant_extreme_magnitudes():
 # ======================================================================= FOID
 @pytest.mark.parametrize("k_strided", [False, True])
 @pytest.mark.parametrize("R,K,k,probe", [(5000, 128, 64, 64), (300, 96, 8, 64), (2048, 64, 256, 64),
-                                          (4100, 256, 16, 32), (50, 32, 64, 64)])
+                                          (4100, 256, 16, 32), (50, 32, 64, 64), (30000, 64, 64, 64),
+                                          (16384, 512, 64, 64)])
 def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
     x, planted = synth.operand(R, K, "R", "X", case_id=R + k, count=min(5, R))
     x[10] = x[11]                                  # an exact key tie
