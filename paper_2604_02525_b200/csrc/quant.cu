@@ -338,10 +338,27 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
       for (int j = 0; j < p; ++j) mine[j] = load_as_float(in, int64_t(j) * ld + r);
   } else {
     const int64_t rw = int64_t(blockIdx.x) * blockDim.x + warp * 32;  // first row of this warp
-    // cooperative: lane handles element (row = rw + e / p, col = e % p) for e strided by 32
-    for (int e = lane; e < 32 * p; e += 32) {
-      const int rr = e / p, c = e % p;
-      if (rw + rr < R) stage[warp][rr][c] = load_as_float(in, (rw + rr) * ld + c);
+    if (sizeof(T) == 2 && p == 64 && ((ld * 2) % 16) == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
+      // 32 rows x 128 B: 256 16-byte chunks, 8 per lane, 8 lanes per row -> full lines
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = lane + 32 * i, rr = c >> 3, c8 = (c & 7) * 8;
+        if (rw + rr < R) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + (rw + rr) * ld + c8));
+          const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            stage[warp][rr][c8 + 2 * t] = __uint_as_float(wv[t] << 16);
+            stage[warp][rr][c8 + 2 * t + 1] = __uint_as_float(wv[t] & 0xFFFF0000u);
+          }
+        }
+      }
+    } else {
+      // cooperative: lane handles element (row = rw + e / p, col = e % p), e strided by 32
+      for (int e = lane; e < 32 * p; e += 32) {
+        const int rr = e / p, c = e % p;
+        if (rw + rr < R) stage[warp][rr][c] = load_as_float(in, (rw + rr) * ld + c);
+      }
     }
     __syncwarp();
   }
@@ -403,9 +420,17 @@ __global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __res
     const int shift = 56 - 8 * pass;
     if (threadIdx.x < 256) hist[threadIdx.x] = 0;
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < R; i += blockDim.x) {
-      const unsigned long long u = kb[i];
-      if (pass == 0 || (u >> (shift + 8)) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    // warp-aggregated histogram update: the leading digits of nearby variances coincide, so
+    // lanes with equal digits are merged before the shared-memory atomic
+    const int64_t Rup = (R + 31) & ~int64_t(31);
+    for (int64_t i = threadIdx.x; i < Rup; i += blockDim.x) {
+      int digit = -1;
+      if (i < R) {
+        const unsigned long long u = kb[i];
+        if (pass == 0 || (u >> (shift + 8)) == prefix) digit = int((u >> shift) & 255u);
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, digit);
+      if (digit >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&hist[digit], unsigned(__popc(grp)));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
