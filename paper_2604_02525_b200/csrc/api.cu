@@ -314,6 +314,8 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   if (out_dt != ADAHOP_DT_BF16 && out_dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
   if (M <= 0 || N <= 0 || K <= 0) return ADAHOP_E_SHAPE;
   if (K % 32 != 0) return ADAHOP_E_SHAPE;
+  if (M * (K / 64 + 1) >= (int64_t(1) << 31) || N * (K / 64 + 1) >= (int64_t(1) << 31))
+    return ADAHOP_E_UNSUPPORTED;   // 32-bit block indexing in the quant kernels
   if ((a_kstrided != 0 && a_kstrided != 1) || (b_kstrided != 0 && b_kstrided != 1))
     return ADAHOP_E_INVALID_ARG;
   if (lda < (a_kstrided ? M : K) || ldb < (b_kstrided ? N : K) || ldc < N) return ADAHOP_E_INVALID_ARG;
@@ -374,10 +376,10 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   //         zeroed in the residual and gathered into the BF16 outlier slice in the same pass
   ADAHOP_LAUNCH(launch_iht_quant(A, false, M, K, lda, a_kstrided, oe_left ? idx : nullptr,
                                  oe_left ? g.kk : 0, qa, qa_sf, nullptr, oe_left ? slice : nullptr,
-                                 false, cs));
+                                 false, dev.sms, cs));
   ADAHOP_LAUNCH(launch_iht_quant(B, false, N, K, ldb, b_kstrided, oe_right ? idx : nullptr,
                                  oe_right ? g.kk : 0, qb, qb_sf, nullptr, oe_right ? slice : nullptr,
-                                 false, cs));
+                                 false, dev.sms, cs));
   launches += 2;
   stage_mark(2, cs);
   // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
@@ -461,17 +463,19 @@ adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_
   if (!in || !codes_canon || !scales_canon || !ws) return ADAHOP_E_INVALID_ARG;
   if (nzero < 0 || (nzero > 0 && !zero_rows)) return ADAHOP_E_INVALID_ARG;
   if (R <= 0 || K <= 0 || K % 32) return ADAHOP_E_SHAPE;
+  if (R * (K / 64 + 1) >= (int64_t(1) << 31)) return ADAHOP_E_UNSUPPORTED;
   const int64_t esz = dt == ADAHOP_DT_F32 ? 4 : 2;
   if (ld < (k_strided ? R : K)) return ADAHOP_E_INVALID_ARG;
   // the row kernel uses 16-byte vector loads; the transposing kernel checks alignment itself
   if (!k_strided && ((ld * esz) % 16 || !aligned16(in))) return ADAHOP_E_INVALID_ARG;
   if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
-  adahop_status_t st = check_device(nullptr);
+  DevInfo dev;
+  adahop_status_t st = check_device(&dev);
   if (st != ADAHOP_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* sf = static_cast<uint8_t*>(ws);
   ADAHOP_LAUNCH(launch_iht_quant(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, zero_rows, nzero,
-                                 codes_canon, sf, had_out, nullptr, false, cs));
+                                 codes_canon, sf, had_out, nullptr, false, dev.sms, cs));
   ADAHOP_LAUNCH(launch_sf_convert(sf, R, K, scales_canon, true, cs));
   g_launches = 2;
   return ADAHOP_OK;

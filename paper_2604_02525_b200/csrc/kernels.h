@@ -13,7 +13,7 @@ namespace adahop {
 cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
                              uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
-                             cudaStream_t st);
+                             int num_sms, cudaStream_t st);
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
 // FOID: probe keys (keys[R], fp64) + single-CTA radix top-k -> idx_sorted[min(k,R)].

@@ -6,6 +6,7 @@
 //   * layout converters used only by the debug / parity entry points
 #include "common.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 #include <algorithm>
 
 namespace adahop {
@@ -43,95 +44,126 @@ __device__ __forceinline__ uint32_t e2m1x8_sw(const float* v) {
   return out;
 }
 
-// In-register IHT + MX quantisation of one 32-element block.
-// x: raw values (residual mask already applied). On return: codes (16 bytes, element
-// 2j in the low nibble), the biased E8M0 scale byte, and (kHad) y = the fp32 Hadamard
-// output that enters the quantiser.
+// ------------------------------------------------------------------------------------
+// Packed fp32x2 arithmetic (sm_100 FADD2 / FMUL2): two independent IEEE round-to-nearest
+// operations per instruction, bit-identical to the scalar ones. A thread quantises TWO
+// 32-element blocks at once (two stored rows in the column variant, two adjacent K-blocks
+// of one row in the row variant) with lane 0 / lane 1 of every pair holding block 0 / 1.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(uint32_t(v)); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
+
+// E8M0 exponent of a block from max|fwht| (before the 1/sqrt(32) scaling):
+// e = floor(log2 RN(amax c)) - 2, clamped; zero block -> 0.
+__device__ __forceinline__ int mx_exponent(float amax_raw) {
+  const float amax_y = __fmul_rn(amax_raw, ADAHOP_INV_SQRT32);  // == max|RN(x c)| (RN monotone)
+  const uint32_t bits = __float_as_uint(amax_y);
+  int e;
+  if (amax_y == 0.f) e = 0;
+  else if ((bits >> 23) != 0) e = int(bits >> 23) - 127 - 2;
+  else e = (31 - __clz(int(bits))) - 149 - 2;  // subnormal amax
+  return max(-127, min(127, e));
+}
+__device__ __forceinline__ float pow2f(int e) { return __uint_as_float(uint32_t(127 + e) << 23); }
+
+template <bool kSwCvt>
+__device__ __forceinline__ uint32_t cvt8(const float* v) {
+  return kSwCvt ? e2m1x8_sw(v) : e2m1x8_hw(v);
+}
+
+// IHT + MX quantisation of two blocks packed in P[i] = (block0[i], block1[i]).
+// Radix-2 butterflies with strides 1,2,4,8,16 (natural-order Walsh–Hadamard) in fp32 RN,
+// then y = RN(x c) with c = RN32(1/sqrt 32), then v = y 2^-e (exact), E2M1 RNE satfinite.
 template <bool kHad, bool kSwCvt>
-__device__ __forceinline__ void iht_quant32(float (&x)[32], uint4& codes, uint32_t& sbyte,
-                                            float* y_out) {
-  // Radix-2 butterflies, strides 1,2,4,8,16 (natural-order Walsh–Hadamard), fp32 RN.
+__device__ __forceinline__ void iht_quant_pair(uint64_t (&P)[32], uint4& codes0, uint4& codes1,
+                                               uint32_t& s0, uint32_t& s1, float* y0, float* y1) {
 #pragma unroll
   for (int h = 1; h < 32; h <<= 1) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       if ((i & h) == 0) {
-        const float a = x[i], b = x[i + h];
-        x[i] = __fadd_rn(a, b);
-        x[i + h] = __fsub_rn(a, b);
+        const uint64_t a = P[i], b = P[i + h];
+        P[i] = f2_add(a, b);
+        P[i + h] = f2_sub(a, b);
       }
     }
   }
-  float amax = 0.f;
+  float m0 = 0.f, m1 = 0.f;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(x[i]));
-  const float c = ADAHOP_INV_SQRT32;
-  // max |RN(x_i c)| == RN(max|x_i| c) since RN is monotone.
-  const float amax_y = __fmul_rn(amax, c);
-  const uint32_t bits = __float_as_uint(amax_y);
-  int e;
-  if (amax_y == 0.f) {
-    e = 0;
-  } else if ((bits >> 23) != 0) {
-    e = int(bits >> 23) - 127 - 2;            // floor(log2 amax) - emax(E2M1)
-  } else {
-    e = (31 - __clz(int(bits))) - 149 - 2;    // subnormal amax
+  for (int i = 0; i < 32; ++i) {
+    m0 = fmaxf(m0, fabsf(f2_lo(P[i])));
+    m1 = fmaxf(m1, fabsf(f2_hi(P[i])));
   }
-  e = max(-127, min(127, e));
-  sbyte = uint32_t(e + 127);
-  float v[32];
-  if (kHad || e > 120 || e < -100) {
-    // exact two-step path: y = RN(x c); v = y * 2^-e (exact power-of-two scaling)
-    const float s = __uint_as_float(uint32_t(127 - e) << 23);
+  const int e0 = mx_exponent(m0), e1 = mx_exponent(m1);
+  s0 = uint32_t(e0 + 127);
+  s1 = uint32_t(e1 + 127);
+  const float c = ADAHOP_INV_SQRT32;
+  if (kHad || e0 > 120 || e0 < -100 || e1 > 120 || e1 < -100) {
+    // exact two-step path: y = RN(x c); v = y * 2^-e (power-of-two scaling, exact)
+    float v0[32], v1[32];
+    const uint64_t cc = f2_pack(c, c);
+    const uint64_t ss = f2_pack(pow2f(-e0), pow2f(-e1));
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float y = __fmul_rn(x[i], c);
-      if (kHad) y_out[i] = y;
-      v[i] = __fmul_rn(y, s);
+      const uint64_t y = f2_mul(P[i], cc);
+      if (kHad) {
+        y0[i] = f2_lo(y);
+        y1[i] = f2_hi(y);
+      }
+      const uint64_t v = f2_mul(y, ss);
+      v0[i] = f2_lo(v);
+      v1[i] = f2_hi(v);
     }
+    codes0 = make_uint4(cvt8<kSwCvt>(v0), cvt8<kSwCvt>(v0 + 8), cvt8<kSwCvt>(v0 + 16), cvt8<kSwCvt>(v0 + 24));
+    codes1 = make_uint4(cvt8<kSwCvt>(v1), cvt8<kSwCvt>(v1 + 8), cvt8<kSwCvt>(v1 + 16), cvt8<kSwCvt>(v1 + 24));
   } else {
-    // fused: RN(x (c 2^-e)) == RN(x c) 2^-e for every value that can reach a nonzero code
-    const float cs = __fmul_rn(c, __uint_as_float(uint32_t(127 - e) << 23));
+    // fused: RN(x (c 2^-e)) == RN(x c) 2^-e for every value that can reach a nonzero code;
+    // converted 8 at a time to keep register pressure low
+    const uint64_t cs = f2_pack(__fmul_rn(c, pow2f(-e0)), __fmul_rn(c, pow2f(-e1)));
+    uint32_t w0[4], w1[4];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(x[i], cs);
-  }
-  if (kSwCvt) {
-    codes.x = e2m1x8_sw(v + 0);
-    codes.y = e2m1x8_sw(v + 8);
-    codes.z = e2m1x8_sw(v + 16);
-    codes.w = e2m1x8_sw(v + 24);
-  } else {
-    codes.x = e2m1x8_hw(v + 0);
-    codes.y = e2m1x8_hw(v + 8);
-    codes.z = e2m1x8_hw(v + 16);
-    codes.w = e2m1x8_hw(v + 24);
+    for (int g = 0; g < 4; ++g) {
+      float a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t v = f2_mul(P[8 * g + i], cs);
+        a[i] = f2_lo(v);
+        b[i] = f2_hi(v);
+      }
+      w0[g] = cvt8<kSwCvt>(a);
+      w1[g] = cvt8<kSwCvt>(b);
+    }
+    codes0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    codes1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
   }
 }
 
-__device__ __forceinline__ void load32(const __nv_bfloat16* p, float (&x)[32]) {
-  const uint4* q = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint4 u = __ldg(q + j);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      x[j * 8 + 2 * t] = __uint_as_float(w[t] << 16);
-      x[j * 8 + 2 * t + 1] = __uint_as_float(w[t] & 0xFFFF0000u);
-    }
-  }
-}
-__device__ __forceinline__ void load32(const float* p, float (&x)[32]) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 u = __ldg(q + j);
-    x[4 * j] = u.x; x[4 * j + 1] = u.y; x[4 * j + 2] = u.z; x[4 * j + 3] = u.w;
-  }
-}
+// bf16 / fp32 element -> fp32 (exact)
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // 32 raw values -> 64 contiguous bytes of the bf16 outlier slice (RN for fp32 inputs).
-__device__ __forceinline__ void store_slice32(__nv_bfloat16* dst, const float (&x)[32]) {
+__device__ __forceinline__ void store_slice32(__nv_bfloat16* dst, const float* x) {
   uint4* d = reinterpret_cast<uint4*>(dst);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -145,9 +177,42 @@ __device__ __forceinline__ void store_slice32(__nv_bfloat16* dst, const float (&
   }
 }
 
-// Row variant: stored row r is in[r*ld + 0..K). One thread per (row, 32-block).
+// Raw 64 contiguous elements (two K-blocks) of one row, as 16-byte vectors.
+template <typename T> struct RowRaw;
+template <> struct RowRaw<__nv_bfloat16> {
+  uint4 v[8];
+  __device__ __forceinline__ void load(const __nv_bfloat16* p, bool two) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldg(q + j);
+#pragma unroll
+    for (int j = 4; j < 8; ++j) v[j] = two ? __ldg(q + j) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ float get(int b, int i) const {  // block b, element i
+    const uint4& u = v[b * 4 + (i >> 3)];
+    const uint32_t w = ((i >> 1) & 3) == 0 ? u.x : ((i >> 1) & 3) == 1 ? u.y : ((i >> 1) & 3) == 2 ? u.z : u.w;
+    return (i & 1) ? bf16hi(w) : bf16lo(w);
+  }
+};
+template <> struct RowRaw<float> {
+  float4 v[16];
+  __device__ __forceinline__ void load(const float* p, bool two) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(q + j);
+#pragma unroll
+    for (int j = 8; j < 16; ++j) v[j] = two ? __ldg(q + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ __forceinline__ float get(int b, int i) const {
+    const float4& u = v[b * 8 + (i >> 2)];
+    return (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
+  }
+};
+
+// Row variant: stored row r is in[r*ld + 0..K). One thread per (row, pair of K-blocks),
+// persistent grid-stride loop with the next pair's 128 B prefetched into registers.
 template <typename T, bool kHad, bool kSwCvt>
-__global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in, int64_t R,
+__global__ void __launch_bounds__(256, 2) k_iht_quant_row(const T* __restrict__ in, int64_t R,
                                                        int64_t K, int64_t ld,
                                                        const int32_t* __restrict__ zero_rows,
                                                        int nzero, uint8_t* __restrict__ codes,
@@ -155,94 +220,199 @@ __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in,
                                                        float* __restrict__ had_out,
                                                        __nv_bfloat16* __restrict__ slice) {
   const int64_t nkb = K / kBlk;
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= R * nkb) return;
-  const int64_t r = t / nkb;
-  const int64_t kb = t - r * nkb;
-  float x[32];
-  load32(in + r * ld + kb * kBlk, x);
-  const int slot = nzero > 0 ? find_sorted(zero_rows, nzero, r) : -1;
-  if (slot >= 0) {
-    // OE: the raw row goes to the BF16 outlier slice, the residual row is zero
-    if (slice) store_slice32(slice + int64_t(slot) * K + kb * kBlk, x);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = 0.f;
+  const int64_t npair = (nkb + 1) / 2;
+  const int64_t total = R * npair;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  // 32-bit index math (the host guarantees total < 2^31)
+  const uint32_t np32 = uint32_t(npair);
+  RowRaw<T> cur, nxt;
+  {
+    const int64_t r = uint32_t(t) / np32, q = t - r * npair;
+    cur.load(in + r * ld + q * 2 * kBlk, 2 * q + 1 < nkb);
   }
-  uint4 c;
-  uint32_t s;
-  iht_quant32<kHad, kSwCvt>(x, c, s, kHad ? had_out + r * K + kb * kBlk : nullptr);
-  *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c;
-  sf[sf_offset(r, kb, kchunks)] = uint8_t(s);
+  for (; t < total; t += stride) {
+    const int64_t r = uint32_t(t) / np32, q = t - r * npair;
+    const int64_t kb0 = 2 * q;
+    const bool two = kb0 + 1 < nkb;
+    const int64_t tn = t + stride;
+    if (tn < total) {
+      const int64_t rn = uint32_t(tn) / np32, qn = tn - rn * npair;
+      nxt.load(in + rn * ld + qn * 2 * kBlk, 2 * qn + 1 < nkb);
+    }
+    uint64_t P[32];
+    const int slot = nzero > 0 ? find_sorted(zero_rows, nzero, r) : -1;
+    if (slot >= 0) {
+      // OE row: raw values -> BF16 outlier slice, residual row = +0
+      if (slice) {
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = cur.get(0, i);
+        store_slice32(slice + int64_t(slot) * K + kb0 * kBlk, x);
+        if (two) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = cur.get(1, i);
+          store_slice32(slice + int64_t(slot) * K + (kb0 + 1) * kBlk, x);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) P[i] = 0ull;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) P[i] = f2_pack(cur.get(0, i), cur.get(1, i));
+    }
+    uint4 c0, c1;
+    uint32_t s0, s1;
+    float* y0 = kHad ? had_out + r * K + kb0 * kBlk : nullptr;
+    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, y0, kHad ? y0 + kBlk : nullptr);
+    uint8_t* cdst = codes + r * (K / 2) + kb0 * 16;
+    if (two) {
+      reinterpret_cast<uint4*>(cdst)[0] = c0;
+      reinterpret_cast<uint4*>(cdst)[1] = c1;
+    } else {
+      reinterpret_cast<uint4*>(cdst)[0] = c0;
+    }
+    sf[sf_offset(r, kb0, kchunks)] = uint8_t(s0);
+    if (two) sf[sf_offset(r, kb0 + 1, kchunks)] = uint8_t(s1);
+    cur = nxt;
+  }
 }
 
-// Column (transposing) variant: stored row r is in[k*ld + r], k = 0..K. A CTA transposes
-// a 64(k) x 128(r) tile through shared memory; thread (r, kb) then owns one 32-block.
+// Column (transposing) variant: stored row r is in[k*ld + r], k = 0..K. Persistent CTAs
+// walk TK(k) x TR(r) tiles that TMA double-buffers into shared memory (OOB zero fill);
+// thread (r-pair, K-block) reads 2 adjacent stored rows per 4/8-byte word (bank-conflict
+// free) and quantises both blocks with packed fp32x2 arithmetic.
+template <typename T> struct ColTile;
+template <> struct ColTile<__nv_bfloat16> { static constexpr int TK = 128, TR = 128; };
+template <> struct ColTile<float> { static constexpr int TK = 64, TR = 256; };
+
 template <typename T, bool kHad, bool kSwCvt>
-__global__ void __launch_bounds__(256) k_iht_quant_col(const T* __restrict__ in, int64_t R,
-                                                       int64_t K, int64_t ld,
-                                                       const int32_t* __restrict__ zero_rows,
+__global__ void __launch_bounds__(256, 2) k_iht_quant_col(const __grid_constant__ CUtensorMap tm, int64_t R,
+                                                       int64_t K, const int32_t* __restrict__ zero_rows,
                                                        int nzero, uint8_t* __restrict__ codes,
                                                        uint8_t* __restrict__ sf, int64_t kchunks,
                                                        float* __restrict__ had_out,
                                                        __nv_bfloat16* __restrict__ slice) {
-  constexpr int TK = 64, TR = 128;
-  __shared__ __align__(16) T tile[TK][TR];
-  const int64_t r0 = int64_t(blockIdx.x) * TR;
-  const int64_t k0 = int64_t(blockIdx.y) * TK;
-  constexpr int kVec = 16 / sizeof(T);  // elements per 16-byte vector
-  constexpr int kVecPerRow = TR / kVec;
-  const bool full = (r0 + TR <= R) && (k0 + TK <= K) && ((ld * sizeof(T)) % 16 == 0) &&
-                    ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
-  if (full) {
-    for (int v = threadIdx.x; v < TK * kVecPerRow; v += blockDim.x) {
-      const int kr = v / kVecPerRow, c = (v % kVecPerRow) * kVec;
-      *reinterpret_cast<uint4*>(&tile[kr][c]) =
-          __ldg(reinterpret_cast<const uint4*>(in + (k0 + kr) * ld + r0 + c));
-    }
-  } else {
-    for (int v = threadIdx.x; v < TK * TR; v += blockDim.x) {
-      const int kr = v / TR, c = v % TR;
-      const bool ok = (k0 + kr < K) && (r0 + c < R);
-      tile[kr][c] = ok ? in[(k0 + kr) * ld + r0 + c] : T(0.f);
-    }
+  constexpr int TK = ColTile<T>::TK, TR = ColTile<T>::TR;
+  constexpr int kTileBytes = TK * TR * int(sizeof(T));
+  constexpr int NKB = TK / kBlk;                  // K-blocks per tile
+  static_assert((TR / 2) * NKB == 256, "one (pair, block) per thread");
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  T* tiles = reinterpret_cast<T*>(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2 * kTileBytes);
+  const int64_t rtiles = (R + TR - 1) / TR, ktiles = (K + TK - 1) / TK;
+  const int64_t ntiles = rtiles * ktiles;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tm);
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
   }
   __syncthreads();
-  const int rr = threadIdx.x % TR;
-  const int kbl = threadIdx.x / TR;  // 0 or 1
-  const int64_t r = r0 + rr;
-  const int64_t kb = k0 / kBlk + kbl;
-  if (r >= R || kb * kBlk >= K) return;
-  float x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = float(tile[kbl * 32 + i][rr]);
-  const int slot = nzero > 0 ? find_sorted(zero_rows, nzero, r) : -1;
-  if (slot >= 0) {
-    if (slice) store_slice32(slice + int64_t(slot) * K + kb * kBlk, x);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = 0.f;
+  auto issue = [&](int64_t tile, int b) {
+    const int64_t rt = tile % rtiles, kt = tile / rtiles;
+    ptx::mbar_arrive_expect_tx(&bar[b], kTileBytes);
+    ptx::tma_load_2d(tiles + size_t(b) * TK * TR, &tm, &bar[b], int32_t(rt * TR), int32_t(kt * TK));
+  };
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  if (tid == 0) {
+    if (first < ntiles) issue(first, 0);
+    if (first + stride < ntiles) issue(first + stride, 1);
   }
-  uint4 c;
-  uint32_t s;
-  iht_quant32<kHad, kSwCvt>(x, c, s, kHad ? had_out + r * K + kb * kBlk : nullptr);
-  *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c;
-  sf[sf_offset(r, kb, kchunks)] = uint8_t(s);
+  const int p = tid % (TR / 2);   // r-pair within the tile
+  const int kbl = tid / (TR / 2); // K-block within the tile
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += stride, ++it) {
+    const int b = it & 1;
+    ptx::mbar_wait(&bar[b], uint32_t((it >> 1) & 1));
+    const int64_t rt = tile % rtiles, kt = tile / rtiles;
+    const int64_t r = rt * TR + 2 * p;
+    const int64_t kb = kt * NKB + kbl;
+    const T* tb = tiles + size_t(b) * TK * TR;
+    uint64_t P[32];
+    float xa[32], xb[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (sizeof(T) == 2) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(tb + (kbl * 32 + i) * TR + 2 * p);
+        xa[i] = bf16lo(w);
+        xb[i] = bf16hi(w);
+      } else {
+        const float2 w = *reinterpret_cast<const float2*>(tb + (kbl * 32 + i) * TR + 2 * p);
+        xa[i] = w.x;
+        xb[i] = w.y;
+      }
+    }
+    const bool va = r < R && kb * kBlk < K, vb = r + 1 < R && kb * kBlk < K;
+    if (nzero > 0) {
+      const int sa = va ? find_sorted(zero_rows, nzero, r) : -1;
+      const int sb = vb ? find_sorted(zero_rows, nzero, r + 1) : -1;
+      if (sa >= 0) {
+        if (slice) store_slice32(slice + int64_t(sa) * K + kb * kBlk, xa);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xa[i] = 0.f;
+      }
+      if (sb >= 0) {
+        if (slice) store_slice32(slice + int64_t(sb) * K + kb * kBlk, xb);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xb[i] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) P[i] = f2_pack(xa[i], xb[i]);
+    __syncthreads();                       // every thread has consumed buffer b
+    if (tid == 0 && tile + 2 * stride < ntiles) issue(tile + 2 * stride, b);
+    uint4 c0, c1;
+    uint32_t s0, s1;
+    float* y0 = kHad ? had_out + r * K + kb * kBlk : nullptr;
+    float yb[32];
+    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, kHad ? (va ? y0 : yb) : nullptr,
+                                 kHad ? (vb ? y0 + K : yb) : nullptr);
+    if (va) {
+      *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c0;
+      sf[sf_offset(r, kb, kchunks)] = uint8_t(s0);
+    }
+    if (vb) {
+      *reinterpret_cast<uint4*>(codes + (r + 1) * (K / 2) + kb * 16) = c1;
+      sf[sf_offset(r + 1, kb, kchunks)] = uint8_t(s1);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------ launchers
 template <typename T, bool kHad, bool kSw>
 static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld, int kstrided,
                                   const int32_t* zero_rows, int nzero, uint8_t* codes, uint8_t* sf,
-                                  float* had_out, __nv_bfloat16* slice, cudaStream_t st) {
+                                  float* had_out, __nv_bfloat16* slice, int num_sms, cudaStream_t st) {
   const int64_t kch = sf_kchunks(K);
   if (!kstrided) {
-    const int64_t n = R * (K / kBlk);
-    const int64_t blocks = (n + 255) / 256;
-    k_iht_quant_row<T, kHad, kSw><<<dim3(unsigned(blocks)), 256, 0, st>>>(
+    const int64_t total = R * ((K / kBlk + 1) / 2);
+    const int64_t want = (total + 255) / 256;
+    const int64_t cap = int64_t(num_sms) * 8;   // 8 x 256 threads per SM, grid-stride
+    k_iht_quant_row<T, kHad, kSw><<<unsigned(want < cap ? want : cap), 256, 0, st>>>(
         in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out, slice);
   } else {
-    dim3 grid(unsigned((R + 127) / 128), unsigned((K + 63) / 64));
-    k_iht_quant_col<T, kHad, kSw><<<grid, 256, 0, st>>>(in, R, K, ld, zero_rows, nzero, codes,
-                                                         sf, kch, had_out, slice);
+    constexpr int TK = ColTile<T>::TK, TR = ColTile<T>::TR;
+    CUtensorMap tm;
+    const CUtensorMapDataType dt = sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    if (!make_tmap_2d(&tm, dt, in, uint64_t(R), uint64_t(K), uint64_t(ld) * sizeof(T), TR, TK,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
+    const size_t smem = 2 * size_t(TK) * TR * sizeof(T) + 64;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_iht_quant_col<T, kHad, kSw>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int64_t ntiles = ((R + TR - 1) / TR) * ((K + TK - 1) / TK);
+    const int per_sm = sizeof(T) == 2 ? 2 : 1;
+    const int64_t cap = int64_t(num_sms) * per_sm;
+    k_iht_quant_col<T, kHad, kSw><<<unsigned(ntiles < cap ? ntiles : cap), 256, smem, st>>>(
+        tm, R, K, zero_rows, nzero, codes, sf, kch, had_out, slice);
   }
   return cudaGetLastError();
 }
@@ -250,10 +420,10 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
 cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
                              uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
-                             cudaStream_t st) {
+                             int num_sms, cudaStream_t st) {
 #define ADAHOP_Q(T, H, S)                                                                   \
   return launch_quant_t<T, H, S>(static_cast<const T*>(in), R, K, ld, kstrided, zero_rows, \
-                                 nzero, codes, sf, had_out, slice, st)
+                                 nzero, codes, sf, had_out, slice, num_sms, st)
   const bool had = had_out != nullptr;
   if (in_f32) {
     if (had) { if (sw_cvt) ADAHOP_Q(float, true, true); else ADAHOP_Q(float, true, false); }
