@@ -381,6 +381,69 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_col(const __grid_constant_
   }
 }
 
+// Generic transposing variant for sources whose row pitch is not 16-byte aligned (TMA
+// cannot address them): one 64(k) x 256(r) tile per CTA through dynamic shared memory.
+template <typename T, bool kHad, bool kSwCvt>
+__global__ void __launch_bounds__(256) k_iht_quant_col_generic(const T* __restrict__ in, int64_t R,
+                                                               int64_t K, int64_t ld,
+                                                               const int32_t* __restrict__ zero_rows,
+                                                               int nzero, uint8_t* __restrict__ codes,
+                                                               uint8_t* __restrict__ sf, int64_t kchunks,
+                                                               float* __restrict__ had_out,
+                                                               __nv_bfloat16* __restrict__ slice) {
+  constexpr int TK = 64, TR = 256;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  const int64_t r0 = int64_t(blockIdx.x) * TR, k0 = int64_t(blockIdx.y) * TK;
+  for (int v = threadIdx.x; v < TK * TR; v += blockDim.x) {
+    const int kr = v / TR, c = v % TR;
+    const bool ok = (k0 + kr < K) && (r0 + c < R);
+    tile[kr * TR + c] = ok ? in[(k0 + kr) * ld + r0 + c] : T(0.f);
+  }
+  __syncthreads();
+  const int p = threadIdx.x % (TR / 2), kbl = threadIdx.x / (TR / 2);
+  const int64_t r = r0 + 2 * p, kb = k0 / kBlk + kbl;
+  const bool va = r < R && kb * kBlk < K, vb = r + 1 < R && kb * kBlk < K;
+  if (!va && !vb) return;
+  float xa[32], xb[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    xa[i] = float(tile[(kbl * 32 + i) * TR + 2 * p]);
+    xb[i] = float(tile[(kbl * 32 + i) * TR + 2 * p + 1]);
+  }
+  if (nzero > 0) {
+    const int sa = va ? find_sorted(zero_rows, nzero, r) : -1;
+    const int sb = vb ? find_sorted(zero_rows, nzero, r + 1) : -1;
+    if (sa >= 0) {
+      if (slice) store_slice32(slice + int64_t(sa) * K + kb * kBlk, xa);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) xa[i] = 0.f;
+    }
+    if (sb >= 0) {
+      if (slice) store_slice32(slice + int64_t(sb) * K + kb * kBlk, xb);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) xb[i] = 0.f;
+    }
+  }
+  uint64_t P[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) P[i] = f2_pack(xa[i], xb[i]);
+  uint4 c0, c1;
+  uint32_t s0, s1;
+  float yb[32];
+  float* y0 = kHad ? had_out + r * K + kb * kBlk : nullptr;
+  iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, kHad ? (va ? y0 : yb) : nullptr,
+                               kHad ? (vb ? y0 + K : yb) : nullptr);
+  if (va) {
+    *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c0;
+    sf[sf_offset(r, kb, kchunks)] = uint8_t(s0);
+  }
+  if (vb) {
+    *reinterpret_cast<uint4*>(codes + (r + 1) * (K / 2) + kb * 16) = c1;
+    sf[sf_offset(r + 1, kb, kchunks)] = uint8_t(s1);
+  }
+}
+
 // ------------------------------------------------------------------------ launchers
 template <typename T, bool kHad, bool kSw>
 static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld, int kstrided,
@@ -393,6 +456,18 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
     const int64_t cap = int64_t(num_sms) * 8;   // 8 x 256 threads per SM, grid-stride
     k_iht_quant_row<T, kHad, kSw><<<unsigned(want < cap ? want : cap), 256, 0, st>>>(
         in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out, slice);
+  } else if ((ld * int64_t(sizeof(T))) % 16 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0) {
+    const size_t smem = size_t(64) * 256 * sizeof(T);
+    static bool attr_g = false;
+    if (!attr_g) {
+      cudaError_t e = cudaFuncSetAttribute(k_iht_quant_col_generic<T, kHad, kSw>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr_g = true;
+    }
+    dim3 grid(unsigned((R + 255) / 256), unsigned((K + 63) / 64));
+    k_iht_quant_col_generic<T, kHad, kSw><<<grid, 256, smem, st>>>(in, R, K, ld, zero_rows, nzero, codes,
+                                                                    sf, kch, had_out, slice);
   } else {
     constexpr int TK = ColTile<T>::TK, TR = ColTile<T>::TR;
     CUtensorMap tm;
@@ -504,8 +579,17 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
   }
   float* mine = stage[warp][lane];
   if (kstrided) {
-    if (r < R)
+    if (r < R) {
+      if (p == kProbeMax) {
+        float x[kProbeMax];  // all loads issued before the first use (no serialised latency)
+#pragma unroll
+        for (int j = 0; j < kProbeMax; ++j) x[j] = load_as_float(in, int64_t(j) * ld + r);
+        keys[r] = foid_key_seq(x, kProbeMax);
+        return;
+      }
+#pragma unroll 16
       for (int j = 0; j < p; ++j) mine[j] = load_as_float(in, int64_t(j) * ld + r);
+    }
   } else {
     const int64_t rw = int64_t(blockIdx.x) * blockDim.x + warp * 32;  // first row of this warp
     if (sizeof(T) == 2 && p == 64 && ((ld * 2) % 16) == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
