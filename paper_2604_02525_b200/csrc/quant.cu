@@ -212,7 +212,7 @@ template <> struct RowRaw<float> {
 // Row variant: stored row r is in[r*ld + 0..K). One thread per (row, pair of K-blocks),
 // persistent grid-stride loop with the next pair's 128 B prefetched into registers.
 template <typename T, bool kHad, bool kSwCvt>
-__global__ void __launch_bounds__(256, 2) k_iht_quant_row(const T* __restrict__ in, int64_t R,
+__global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in, int64_t R,
                                                        int64_t K, int64_t ld,
                                                        const int32_t* __restrict__ zero_rows,
                                                        int nzero, uint8_t* __restrict__ codes,
@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_row(const T* __restrict__ 
     uint4 c0, c1;
     uint32_t s0, s1;
     float* y0 = kHad ? had_out + r * K + kb0 * kBlk : nullptr;
-    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, y0, kHad ? y0 + kBlk : nullptr);
+    float ytail[kHad ? 32 : 1];   // sink for the missing partner block of an odd K/32
+    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, y0, kHad ? (two ? y0 + kBlk : ytail) : nullptr);
     uint8_t* cdst = codes + r * (K / 2) + kb0 * 16;
     if (two) {
       reinterpret_cast<uint4*>(cdst)[0] = c0;
@@ -279,104 +280,119 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_row(const T* __restrict__ 
   }
 }
 
-// Column (transposing) variant: stored row r is in[k*ld + r], k = 0..K. Persistent CTAs
-// walk TK(k) x TR(r) tiles that TMA double-buffers into shared memory (OOB zero fill);
-// thread (r-pair, K-block) reads 2 adjacent stored rows per 4/8-byte word (bank-conflict
-// free) and quantises both blocks with packed fp32x2 arithmetic.
-template <typename T> struct ColTile;
-template <> struct ColTile<__nv_bfloat16> { static constexpr int TK = 128, TR = 128; };
-template <> struct ColTile<float> { static constexpr int TK = 64, TR = 256; };
+// TMA-ring variant for bf16 sources with 16-byte aligned pitch (the production path).
+// Persistent CTAs (one per SM, 256 threads) walk 32-KB tiles that a kStages-deep TMA ring
+// keeps in flight; each thread quantises two 32-blocks per tile with fp32x2 arithmetic.
+//  row (K-contiguous): tile = 256 stored rows x 64 K, 128B-swizzled, thread = one row's
+//       pair of blocks; the swizzle makes the per-row 128-byte reads bank-conflict free.
+//  col (K-strided, transposing): tile = 128 K x 128 stored rows, thread = (row pair, block),
+//       reading both rows of a pair from one 4-byte word.
+constexpr int kQStages = 4;
+constexpr int kQTileBytes = 32768;
 
-template <typename T, bool kHad, bool kSwCvt>
-__global__ void __launch_bounds__(256, 2) k_iht_quant_col(const __grid_constant__ CUtensorMap tm, int64_t R,
-                                                       int64_t K, const int32_t* __restrict__ zero_rows,
-                                                       int nzero, uint8_t* __restrict__ codes,
-                                                       uint8_t* __restrict__ sf, int64_t kchunks,
-                                                       float* __restrict__ had_out,
-                                                       __nv_bfloat16* __restrict__ slice) {
-  constexpr int TK = ColTile<T>::TK, TR = ColTile<T>::TR;
-  constexpr int kTileBytes = TK * TR * int(sizeof(T));
-  constexpr int NKB = TK / kBlk;                  // K-blocks per tile
-  static_assert((TR / 2) * NKB == 256, "one (pair, block) per thread");
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  T* tiles = reinterpret_cast<T*>(smem_raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2 * kTileBytes);
+template <bool kCol, bool kHad, bool kSwCvt>
+__global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant__ CUtensorMap tm, int64_t R,
+                                                          int64_t K, const int32_t* __restrict__ zero_rows,
+                                                          int nzero, uint8_t* __restrict__ codes,
+                                                          uint8_t* __restrict__ sf, int64_t kchunks,
+                                                          float* __restrict__ had_out,
+                                                          __nv_bfloat16* __restrict__ slice) {
+  // row: TR = 256 rows, TK = 64; col: TR = 128 rows, TK = 128
+  constexpr int TR = kCol ? 128 : 256, TK = kCol ? 128 : 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQStages * kQTileBytes);
   const int64_t rtiles = (R + TR - 1) / TR, ktiles = (K + TK - 1) / TK;
   const int64_t ntiles = rtiles * ktiles;
   const int tid = threadIdx.x;
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
-    ptx::mbar_init(&bar[0], 1);
-    ptx::mbar_init(&bar[1], 1);
+    for (int i = 0; i < kQStages; ++i) ptx::mbar_init(&full[i], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int64_t tile, int b) {
-    const int64_t rt = tile % rtiles, kt = tile / rtiles;
-    ptx::mbar_arrive_expect_tx(&bar[b], kTileBytes);
-    ptx::tma_load_2d(tiles + size_t(b) * TK * TR, &tm, &bar[b], int32_t(rt * TR), int32_t(kt * TK));
-  };
   const int64_t first = blockIdx.x, stride = gridDim.x;
-  if (tid == 0) {
-    if (first < ntiles) issue(first, 0);
-    if (first + stride < ntiles) issue(first + stride, 1);
-  }
-  const int p = tid % (TR / 2);   // r-pair within the tile
-  const int kbl = tid / (TR / 2); // K-block within the tile
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t rt = tile % rtiles, kt = tile / rtiles;
+    ptx::mbar_arrive_expect_tx(&full[st], kQTileBytes);
+    if (kCol) ptx::tma_load_2d(ring + st * kQTileBytes, &tm, &full[st], int32_t(rt * TR), int32_t(kt * TK));
+    else ptx::tma_load_2d(ring + st * kQTileBytes, &tm, &full[st], int32_t(kt * TK), int32_t(rt * TR));
+  };
+  if (tid == 0)
+    for (int i = 0; i < kQStages; ++i)
+      if (first + i * stride < ntiles) issue(first + i * stride, i);
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += stride, ++it) {
-    const int b = it & 1;
-    ptx::mbar_wait(&bar[b], uint32_t((it >> 1) & 1));
+    const int st = it % kQStages;
+    ptx::mbar_wait(&full[st], uint32_t((it / kQStages) & 1));
     const int64_t rt = tile % rtiles, kt = tile / rtiles;
-    const int64_t r = rt * TR + 2 * p;
-    const int64_t kb = kt * NKB + kbl;
-    const T* tb = tiles + size_t(b) * TK * TR;
-    uint64_t P[32];
+    const uint8_t* tb = ring + st * kQTileBytes;
     float xa[32], xb[32];
+    int64_t ra, rb, kba, kbb;   // (stored row, K-block) of the two blocks
+    if (kCol) {
+      const int p = tid % (TR / 2), kbl = tid / (TR / 2);
+      ra = rt * TR + 2 * p;
+      rb = ra + 1;
+      kba = kbb = kt * (TK / kBlk) + kbl;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(tb) + (kbl * 32) * (TR / 2) + p;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (sizeof(T) == 2) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(tb + (kbl * 32 + i) * TR + 2 * p);
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t w = src[i * (TR / 2)];
         xa[i] = bf16lo(w);
         xb[i] = bf16hi(w);
-      } else {
-        const float2 w = *reinterpret_cast<const float2*>(tb + (kbl * 32 + i) * TR + 2 * p);
-        xa[i] = w.x;
-        xb[i] = w.y;
+      }
+    } else {
+      ra = rb = rt * TR + tid;
+      kba = kt * 2;
+      kbb = kba + 1;
+      const uint8_t* row = tb + tid * 128;
+      const int sw = tid & 7;   // 128B swizzle: 16-byte chunk j lives at j ^ (row % 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 u = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
+        const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+        float* dst = j < 4 ? xa + 8 * j : xb + 8 * (j - 4);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          dst[2 * t] = bf16lo(wv[t]);
+          dst[2 * t + 1] = bf16hi(wv[t]);
+        }
       }
     }
-    const bool va = r < R && kb * kBlk < K, vb = r + 1 < R && kb * kBlk < K;
+    __syncthreads();                                   // stage consumed by every thread
+    if (tid == 0 && tile + kQStages * stride < ntiles) issue(tile + kQStages * stride, st);
+    const bool va = ra < R && kba * kBlk < K;
+    const bool vb = rb < R && kbb * kBlk < K;
     if (nzero > 0) {
-      const int sa = va ? find_sorted(zero_rows, nzero, r) : -1;
-      const int sb = vb ? find_sorted(zero_rows, nzero, r + 1) : -1;
+      const int sa = va ? find_sorted(zero_rows, nzero, ra) : -1;
+      const int sb = vb ? (kCol ? find_sorted(zero_rows, nzero, rb) : sa) : -1;
       if (sa >= 0) {
-        if (slice) store_slice32(slice + int64_t(sa) * K + kb * kBlk, xa);
+        if (slice) store_slice32(slice + int64_t(sa) * K + kba * kBlk, xa);
 #pragma unroll
         for (int i = 0; i < 32; ++i) xa[i] = 0.f;
       }
       if (sb >= 0) {
-        if (slice) store_slice32(slice + int64_t(sb) * K + kb * kBlk, xb);
+        if (slice) store_slice32(slice + int64_t(sb) * K + kbb * kBlk, xb);
 #pragma unroll
         for (int i = 0; i < 32; ++i) xb[i] = 0.f;
       }
     }
+    uint64_t P[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) P[i] = f2_pack(xa[i], xb[i]);
-    __syncthreads();                       // every thread has consumed buffer b
-    if (tid == 0 && tile + 2 * stride < ntiles) issue(tile + 2 * stride, b);
     uint4 c0, c1;
     uint32_t s0, s1;
-    float* y0 = kHad ? had_out + r * K + kb * kBlk : nullptr;
-    float yb[32];
-    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, kHad ? (va ? y0 : yb) : nullptr,
-                                 kHad ? (vb ? y0 + K : yb) : nullptr);
+    float ysink[kHad ? 64 : 1];
+    float* ya = kHad ? (va ? had_out + ra * K + kba * kBlk : ysink) : nullptr;
+    float* yb = kHad ? (vb ? had_out + rb * K + kbb * kBlk : ysink + (kHad ? 32 : 0)) : nullptr;
+    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, ya, yb);
     if (va) {
-      *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c0;
-      sf[sf_offset(r, kb, kchunks)] = uint8_t(s0);
+      *reinterpret_cast<uint4*>(codes + ra * (K / 2) + kba * 16) = c0;
+      sf[sf_offset(ra, kba, kchunks)] = uint8_t(s0);
     }
     if (vb) {
-      *reinterpret_cast<uint4*>(codes + (r + 1) * (K / 2) + kb * 16) = c1;
-      sf[sf_offset(r + 1, kb, kchunks)] = uint8_t(s1);
+      *reinterpret_cast<uint4*>(codes + rb * (K / 2) + kbb * 16) = c1;
+      sf[sf_offset(rb, kbb, kchunks)] = uint8_t(s1);
     }
   }
 }
@@ -450,13 +466,44 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
                                   const int32_t* zero_rows, int nzero, uint8_t* codes, uint8_t* sf,
                                   float* had_out, __nv_bfloat16* slice, int num_sms, cudaStream_t st) {
   const int64_t kch = sf_kchunks(K);
-  if (!kstrided) {
+  const bool tma_ok = sizeof(T) == 2 && (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  if (tma_ok) {
+    CUtensorMap tm;
+    bool ok;
+    int64_t ntiles;
+    if (kstrided) {   // [K][R] source, box 128 rows(r) x 128 k
+      ok = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(R), uint64_t(K), uint64_t(ld) * 2,
+                        128, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+      ntiles = ((R + 127) / 128) * ((K + 127) / 128);
+    } else {          // [R][K] source, box 64 k x 256 rows, 128B swizzle
+      ok = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(K), uint64_t(R), uint64_t(ld) * 2,
+                        64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
+      ntiles = ((R + 255) / 256) * ((K + 63) / 64);
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64;
+    static bool attr[2] = {false, false};
+    if (!attr[kstrided]) {
+      cudaError_t e = kstrided
+          ? cudaFuncSetAttribute(k_iht_quant_tma<true, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))
+          : cudaFuncSetAttribute(k_iht_quant_tma<false, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr[kstrided] = true;
+    }
+    const unsigned grid = unsigned(ntiles < num_sms ? ntiles : num_sms);
+    if (kstrided)
+      k_iht_quant_tma<true, kHad, kSw><<<grid, 256, smem, st>>>(tm, R, K, zero_rows, nzero, codes, sf, kch,
+                                                                 had_out, slice);
+    else
+      k_iht_quant_tma<false, kHad, kSw><<<grid, 256, smem, st>>>(tm, R, K, zero_rows, nzero, codes, sf, kch,
+                                                                  had_out, slice);
+  } else if (!kstrided) {
     const int64_t total = R * ((K / kBlk + 1) / 2);
     const int64_t want = (total + 255) / 256;
-    const int64_t cap = int64_t(num_sms) * 8;   // 8 x 256 threads per SM, grid-stride
+    const int64_t cap = int64_t(num_sms) * 8;   // grid-stride
     k_iht_quant_row<T, kHad, kSw><<<unsigned(want < cap ? want : cap), 256, 0, st>>>(
         in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out, slice);
-  } else if ((ld * int64_t(sizeof(T))) % 16 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0) {
+  } else {
     const size_t smem = size_t(64) * 256 * sizeof(T);
     static bool attr_g = false;
     if (!attr_g) {
@@ -468,26 +515,6 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
     dim3 grid(unsigned((R + 255) / 256), unsigned((K + 63) / 64));
     k_iht_quant_col_generic<T, kHad, kSw><<<grid, 256, smem, st>>>(in, R, K, ld, zero_rows, nzero, codes,
                                                                     sf, kch, had_out, slice);
-  } else {
-    constexpr int TK = ColTile<T>::TK, TR = ColTile<T>::TR;
-    CUtensorMap tm;
-    const CUtensorMapDataType dt = sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    if (!make_tmap_2d(&tm, dt, in, uint64_t(R), uint64_t(K), uint64_t(ld) * sizeof(T), TR, TK,
-                      CU_TENSOR_MAP_SWIZZLE_NONE))
-      return cudaErrorInvalidValue;
-    const size_t smem = 2 * size_t(TK) * TR * sizeof(T) + 64;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_iht_quant_col<T, kHad, kSw>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    const int64_t ntiles = ((R + TR - 1) / TR) * ((K + TK - 1) / TK);
-    const int per_sm = sizeof(T) == 2 ? 2 : 1;
-    const int64_t cap = int64_t(num_sms) * per_sm;
-    k_iht_quant_col<T, kHad, kSw><<<unsigned(ntiles < cap ? ntiles : cap), 256, smem, st>>>(
-        tm, R, K, zero_rows, nzero, codes, sf, kch, had_out, slice);
   }
   return cudaGetLastError();
 }
