@@ -47,6 +47,21 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
          | (uint32_t(m >> 4) << 24);
 }
 
+// Grouped rasterisation: tiles are walked in groups of kGroupM m-blocks with n fastest
+// inside a group, so the ~148 tiles in flight share a few A panels and the B panels stay
+// L2-resident (plain m-fastest order streams all of A once per n-block).
+constexpr int64_t kGroupM = 8;
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t nblocks, int64_t& mb,
+                                            int64_t& nb) {
+  const int64_t per_group = kGroupM * nblocks;
+  const int64_t g = t / per_group;
+  const int64_t first_m = g * kGroupM;
+  const int64_t gm = mblocks - first_m < kGroupM ? mblocks - first_m : kGroupM;
+  const int64_t local = t - g * per_group;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                 const uint8_t* __restrict__ sfa, const uint8_t* __restrict__ sfb, void* C,
@@ -92,7 +107,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t mb = tile % mblocks, nb = tile / mblocks;
+      int64_t mb, nb;
+      tile_coords(tile, mblocks, nblocks, mb, nb);
       for (int ks = 0; ks < nks; ++ks) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + size_t(stage) * kStageBytes;
@@ -155,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp
     int64_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
-      const int64_t mb = tile % mblocks, nb = tile / mblocks;
+      int64_t mb, nb;
+      tile_coords(tile, mblocks, nblocks, mb, nb);
       const uint32_t buf = uint32_t(lt & 1);
       const uint32_t use = uint32_t(lt >> 1);
       ptx::mbar_wait(&tfull[buf], use & 1);

@@ -158,6 +158,11 @@ __device__ __forceinline__ void iht_quant_pair(uint64_t (&P)[32], uint4& codes0,
   }
 }
 
+__device__ __forceinline__ void store_f32x32(float* dst, const float* y) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) dst[i] = y[i];
+}
+
 // bf16 / fp32 element -> fp32 (exact)
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -264,9 +269,12 @@ __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in,
     }
     uint4 c0, c1;
     uint32_t s0, s1;
-    float* y0 = kHad ? had_out + r * K + kb0 * kBlk : nullptr;
-    float ytail[kHad ? 32 : 1];   // sink for the missing partner block of an odd K/32
-    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, y0, kHad ? (two ? y0 + kBlk : ytail) : nullptr);
+    float ya[kHad ? 32 : 1], yb[kHad ? 32 : 1];
+    iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, ya, yb);
+    if (kHad) {
+      store_f32x32(had_out + r * K + kb0 * kBlk, ya);
+      if (two) store_f32x32(had_out + r * K + (kb0 + 1) * kBlk, yb);
+    }
     uint8_t* cdst = codes + r * (K / 2) + kb0 * 16;
     if (two) {
       reinterpret_cast<uint4*>(cdst)[0] = c0;
@@ -287,11 +295,11 @@ __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in,
 //       pair of blocks; the swizzle makes the per-row 128-byte reads bank-conflict free.
 //  col (K-strided, transposing): tile = 128 K x 128 stored rows, thread = (row pair, block),
 //       reading both rows of a pair from one 4-byte word.
-constexpr int kQStages = 4;
+constexpr int kQStages = 3;
 constexpr int kQTileBytes = 32768;
 
 template <bool kCol, bool kHad, bool kSwCvt>
-__global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant__ CUtensorMap tm, int64_t R,
+__global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant__ CUtensorMap tm, int64_t R,
                                                           int64_t K, const int32_t* __restrict__ zero_rows,
                                                           int nzero, uint8_t* __restrict__ codes,
                                                           uint8_t* __restrict__ sf, int64_t kchunks,
@@ -327,8 +335,8 @@ __global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant_
     ptx::mbar_wait(&full[st], uint32_t((it / kQStages) & 1));
     const int64_t rt = tile % rtiles, kt = tile / rtiles;
     const uint8_t* tb = ring + st * kQTileBytes;
-    float xa[32], xb[32];
-    int64_t ra, rb, kba, kbb;   // (stored row, K-block) of the two blocks
+    uint64_t P[32];            // P[i] = (block a element i, block b element i), raw values
+    int64_t ra, rb, kba, kbb;  // (stored row, K-block) of the two blocks
     if (kCol) {
       const int p = tid % (TR / 2), kbl = tid / (TR / 2);
       ra = rt * TR + 2 * p;
@@ -338,8 +346,7 @@ __global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant_
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const uint32_t w = src[i * (TR / 2)];
-        xa[i] = bf16lo(w);
-        xb[i] = bf16hi(w);
+        P[i] = f2_pack(bf16lo(w), bf16hi(w));
       }
     } else {
       ra = rb = rt * TR + tid;
@@ -348,14 +355,15 @@ __global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant_
       const uint8_t* row = tb + tid * 128;
       const int sw = tid & 7;   // 128B swizzle: 16-byte chunk j lives at j ^ (row % 8)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint4 u = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
-        const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
-        float* dst = j < 4 ? xa + 8 * j : xb + 8 * (j - 4);
+      for (int j = 0; j < 4; ++j) {
+        const uint4 ua = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
+        const uint4 ub = *reinterpret_cast<const uint4*>(row + (((j + 4) ^ sw) << 4));
+        const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w};
+        const uint32_t wb[4] = {ub.x, ub.y, ub.z, ub.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          dst[2 * t] = bf16lo(wv[t]);
-          dst[2 * t + 1] = bf16hi(wv[t]);
+          P[8 * j + 2 * t] = f2_pack(bf16lo(wa[t]), bf16lo(wb[t]));
+          P[8 * j + 2 * t + 1] = f2_pack(bf16hi(wa[t]), bf16hi(wb[t]));
         }
       }
     }
@@ -366,26 +374,30 @@ __global__ void __launch_bounds__(256, 1) k_iht_quant_tma(const __grid_constant_
     if (nzero > 0) {
       const int sa = va ? find_sorted(zero_rows, nzero, ra) : -1;
       const int sb = vb ? (kCol ? find_sorted(zero_rows, nzero, rb) : sa) : -1;
-      if (sa >= 0) {
-        if (slice) store_slice32(slice + int64_t(sa) * K + kba * kBlk, xa);
+      if (sa >= 0 || sb >= 0) {
+        float x[32];
+        if (sa >= 0 && slice) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) xa[i] = 0.f;
-      }
-      if (sb >= 0) {
-        if (slice) store_slice32(slice + int64_t(sb) * K + kbb * kBlk, xb);
+          for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
+          store_slice32(slice + int64_t(sa) * K + kba * kBlk, x);
+        }
+        if (sb >= 0 && slice) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) xb[i] = 0.f;
+          for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
+          store_slice32(slice + int64_t(sb) * K + kbb * kBlk, x);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) P[i] = f2_pack(sa >= 0 ? 0.f : f2_lo(P[i]), sb >= 0 ? 0.f : f2_hi(P[i]));
       }
     }
-    uint64_t P[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) P[i] = f2_pack(xa[i], xb[i]);
     uint4 c0, c1;
     uint32_t s0, s1;
-    float ysink[kHad ? 64 : 1];
-    float* ya = kHad ? (va ? had_out + ra * K + kba * kBlk : ysink) : nullptr;
-    float* yb = kHad ? (vb ? had_out + rb * K + kbb * kBlk : ysink + (kHad ? 32 : 0)) : nullptr;
+    float ya[kHad ? 32 : 1], yb[kHad ? 32 : 1];   // debug: the fp32 Hadamard output
     iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, ya, yb);
+    if (kHad) {
+      if (va) store_f32x32(had_out + ra * K + kba * kBlk, ya);
+      if (vb) store_f32x32(had_out + rb * K + kbb * kBlk, yb);
+    }
     if (va) {
       *reinterpret_cast<uint4*>(codes + ra * (K / 2) + kba * 16) = c0;
       sf[sf_offset(ra, kba, kchunks)] = uint8_t(s0);
@@ -408,8 +420,8 @@ __global__ void __launch_bounds__(256) k_iht_quant_col_generic(const T* __restri
                                                                float* __restrict__ had_out,
                                                                __nv_bfloat16* __restrict__ slice) {
   constexpr int TK = 64, TR = 256;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  T* tile = reinterpret_cast<T*>(smem_raw);
+  extern __shared__ __align__(1024) uint8_t smem_gen[];
+  T* tile = reinterpret_cast<T*>(smem_gen);
   const int64_t r0 = int64_t(blockIdx.x) * TR, k0 = int64_t(blockIdx.y) * TK;
   for (int v = threadIdx.x; v < TK * TR; v += blockDim.x) {
     const int kr = v / TR, c = v % TR;
@@ -446,10 +458,12 @@ __global__ void __launch_bounds__(256) k_iht_quant_col_generic(const T* __restri
   for (int i = 0; i < 32; ++i) P[i] = f2_pack(xa[i], xb[i]);
   uint4 c0, c1;
   uint32_t s0, s1;
-  float yb[32];
-  float* y0 = kHad ? had_out + r * K + kb * kBlk : nullptr;
-  iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, kHad ? (va ? y0 : yb) : nullptr,
-                               kHad ? (vb ? y0 + K : yb) : nullptr);
+  float ya[kHad ? 32 : 1], yb[kHad ? 32 : 1];
+  iht_quant_pair<kHad, kSwCvt>(P, c0, c1, s0, s1, ya, yb);
+  if (kHad) {
+    if (va) store_f32x32(had_out + r * K + kb * kBlk, ya);
+    if (vb) store_f32x32(had_out + (r + 1) * K + kb * kBlk, yb);
+  }
   if (va) {
     *reinterpret_cast<uint4*>(codes + r * (K / 2) + kb * 16) = c0;
     sf[sf_offset(r, kb, kchunks)] = uint8_t(s0);
@@ -490,7 +504,8 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
       if (e != cudaSuccess) return e;
       attr[kstrided] = true;
     }
-    const unsigned grid = unsigned(ntiles < num_sms ? ntiles : num_sms);
+    const int64_t cap = int64_t(num_sms) * 2;   // two persistent CTAs per SM
+    const unsigned grid = unsigned(ntiles < cap ? ntiles : cap);
     if (kstrided)
       k_iht_quant_tma<true, kHad, kSw><<<grid, 256, smem, st>>>(tm, R, K, zero_rows, nzero, codes, sf, kch,
                                                                  had_out, slice);
