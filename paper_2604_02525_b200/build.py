@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libadahop.so")
-SOURCES = ["api.cu", "quant.cu", "gemm_mxf4.cu", "gemm_bf16.cu"]
+SOURCES = ["api.cu", "quant.cu", "gemm_mxf4.cu", "gemm_mxf4_2sm.cu", "gemm_bf16.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

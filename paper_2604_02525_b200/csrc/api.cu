@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/adahop.h"
@@ -84,6 +85,21 @@ adahop_status_t check_device(DevInfo* out) {
   } while (0)
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// MXFP4 GEMM kernel choice: ADAHOP_GEMM_VARIANT = 1 (1-CTA 128x128), 128 or 256 (CTA pairs).
+int gemm_variant() {
+  static int v = [] {
+    const char* e = getenv("ADAHOP_GEMM_VARIANT");
+    return e ? atoi(e) : 256;
+  }();
+  return v;
+}
+
+cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
+  const int v = gemm_variant();
+  if (v == 1 || a.M <= 128) return launch_gemm_mxf4(a, sms, st);
+  return launch_gemm_mxf4_2sm(a, sms, v, st);
+}
 
 // ---------------------------------------------------------------------- workspace carving
 struct Carver {
@@ -384,7 +400,7 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   stage_mark(2, cs);
   // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
   Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K};
-  ADAHOP_LAUNCH(launch_gemm_mxf4(ma, dev.sms, cs));
+  ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
   launches += 1;
   stage_mark(3, cs);
   // ---- 4. BF16 outlier GEMM + scatter-add into C (P:762-763 stages 3-4)
@@ -539,7 +555,7 @@ adahop_status_t adahop_debug_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_
   ADAHOP_LAUNCH(launch_sf_convert(a_scales, M, K, sfa, false, cs));
   ADAHOP_LAUNCH(launch_sf_convert(b_scales, N, K, sfb, false, cs));
   Mxf4GemmArgs ma{a_codes, sfa, b_codes, sfb, C, out_dt == ADAHOP_DT_F32, ldc, M, N, K};
-  ADAHOP_LAUNCH(launch_gemm_mxf4(ma, dev.sms, cs));
+  ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
   g_launches = 3;
   return ADAHOP_OK;
 }

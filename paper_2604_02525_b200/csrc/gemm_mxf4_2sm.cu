@@ -1,0 +1,280 @@
+// gemm_mxf4_2sm.cu — block-scaled MXFP4 GEMM on CTA pairs (tcgen05 cta_group::2, sm_100a).
+//
+// Same operation as gemm_mxf4.cu (C = deq(A_store) · deq(B_store)^T, E2M1 with UE8M0 per 32
+// along K — the MXFP4 matmul of eq:inner_hadamard P:95 / eq:oe_left P:273 / eq:oe_right
+// P:280) but each output tile is 256 x BN and is computed by a 2-CTA cluster: CTA r holds
+// rows [128 r, 128 r + 128) of the A tile and rows [BN/2 r, BN/2 (r+1)) of the B tile, the
+// leader CTA issues tcgen05.mma.cta_group::2 (M = 256) and each CTA's TMEM receives its own
+// 128 x BN accumulator half. Per SM this halves the operand bytes per flop of the 1-CTA
+// 128 x 128 kernel, which was bound by the latency of refilling its smem ring from L2.
+//
+// Roles (384 threads per CTA): warp 0 TMA producer (both CTAs; completion is signalled on
+// the leader's barrier), warp 1 MMA issuer (leader only), warp 2 TMEM allocator, warps 4..11
+// epilogue (2 warps per TMEM lane quadrant, each owning half of the columns).
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace adahop {
+namespace mxf4x2 {
+
+constexpr int BK = 256;  // fp4 elements per stage
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
+
+template <int BN, int BUFS>
+struct Cfg {
+  static constexpr int kA = 128 * BK / 2;             // 16 KB: this CTA's 128 rows of A
+  static constexpr int kB = (BN / 2) * BK / 2;        // this CTA's BN/2 rows of B
+  static constexpr int kSfa = 1024;                   // 128 rows x 8 K-blocks
+  static constexpr int kSfb = (BN / 128) * 1024;      // all BN rows (duplicated in both CTAs)
+  static constexpr int kStage = kA + kB + kSfa + kSfb;
+  static constexpr int kStages = BN == 256 ? 5 : 7;
+  static constexpr int kAccCols = BN;
+  static constexpr int kSfaCol = 256;                 // after the accumulator buffers
+  static constexpr int kSfbCol = 264;
+  static constexpr size_t kSmem = size_t(kStages) * kStage + kEpiWarps * kEpiStageBytes + 1024 + 512;
+  static_assert(BUFS * BN <= 256, "accumulators must fit below the scale-factor columns");
+};
+
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
+  return (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(m >> 4) << 24);
+}
+
+constexpr int64_t kGroupM = 8;  // grouped rasterisation (see gemm_mxf4.cu)
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t nblocks, int64_t& mb,
+                                            int64_t& nb) {
+  const int64_t per_group = kGroupM * nblocks;
+  const int64_t g = t / per_group;
+  const int64_t first_m = g * kGroupM;
+  const int64_t gm = mblocks - first_m < kGroupM ? mblocks - first_m : kGroupM;
+  const int64_t local = t - g * per_group;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
+template <int BN, int BUFS>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
+                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
+  using G = Cfg<BN, BUFS>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_smem = smem + size_t(G::kStages) * G::kStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiWarps * kEpiStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + G::kStages;
+  uint64_t* tfull = bars + 2 * G::kStages;
+  uint64_t* tempty = tfull + BUFS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + BUFS);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t mblocks = (M + 255) / 256;
+  const int64_t nblocks = (N + BN - 1) / BN;
+  const int64_t ntiles = mblocks * nblocks;
+  const int nks = int((K + BK - 1) / BK);
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_a);
+    ptx::prefetch_tmap(&tm_b);
+    ptx::prefetch_tmap(&tm_sfa);
+    ptx::prefetch_tmap(&tm_sfb);
+    for (int s = 0; s < G::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < BUFS; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 2 * kEpiWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = cluster; tile < ntiles; tile += nclusters) {
+      int64_t mb, nb;
+      tile_coords(tile, mblocks, nblocks, mb, nb);
+      for (int ks = 0; ks < nks; ++ks) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + size_t(stage) * G::kStage;
+        uint8_t* sb = sa + G::kA;
+        uint8_t* ssfa = sb + G::kB;
+        uint8_t* ssfb = ssfa + G::kSfa;
+        const uint32_t fb = ptx::mapa(&full[stage], 0);
+        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * G::kStage);
+        ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + rank * 128));
+        ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + rank * (BN / 2)));
+        ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + rank));
+        ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
+        if (++stage == G::kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    constexpr uint32_t idesc = make_idesc(256, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t lt = 0;
+    for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
+      const uint32_t buf = uint32_t(lt % BUFS);
+      const uint32_t use = uint32_t(lt / BUFS);
+      ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * G::kAccCols;
+      for (int ks = 0; ks < nks; ++ks) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        uint8_t* sa = smem + size_t(stage) * G::kStage;
+        uint8_t* sb = sa + G::kA;
+        uint8_t* ssfa = sb + G::kB;
+        uint8_t* ssfb = ssfa + G::kSfa;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfaCol + 4 * c,
+                                          ptx::make_sdesc(ptx::smem_u32(ssfa + c * 512), 0, 128, 0));
+#pragma unroll
+          for (int g = 0; g < BN / 128; ++g)
+            ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfbCol + (BN / 32) * c + 4 * g,
+                                            ptx::make_sdesc(ptx::smem_u32(ssfb + g * 1024 + c * 512), 0, 128, 0));
+        }
+        const uint32_t a_addr = ptx::smem_u32(sa), b_addr = ptx::smem_u32(sb);
+#pragma unroll
+        for (int j = 0; j < BK / 64; ++j) {
+          const uint32_t sf_id = uint32_t(j & 1) * 2;
+          const uint32_t sfa_t = (tmem_base + G::kSfaCol + 4 * (j >> 1)) | (sf_id << 30);
+          const uint32_t sfb_t = (tmem_base + G::kSfbCol + (BN / 32) * (j >> 1)) | (sf_id << 30);
+          const uint32_t id = idesc | (sf_id << 4) | (sf_id << 29);
+          ptx::mma_mxf4_2sm(d_tmem, ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2),
+                            ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2), id, sfa_t, sfb_t,
+                            (ks > 0 || j > 0) ? 1u : 0u);
+        }
+        ptx::tc_commit_2sm(&empty[stage]);
+        if (++stage == G::kStages) { stage = 0; phase ^= 1; }
+      }
+      ptx::tc_commit_2sm(&tfull[buf]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (8 warps per CTA)
+    const uint32_t q = warp & 3;            // TMEM lane quadrant
+    const uint32_t half = (warp - 4) >> 2;  // column half of the tile
+    uint8_t* stg = epi_smem + (warp - 4) * kEpiStageBytes;
+    const int elt = out_f32 ? 4 : 2;
+    const int cols_per_grp = 128 / elt;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
+    const uint32_t empty_leader = ptx::mapa(&tempty[0], 0);
+    int64_t lt = 0;
+    for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
+      int64_t mb, nb;
+      tile_coords(tile, mblocks, nblocks, mb, nb);
+      const uint32_t buf = uint32_t(lt % BUFS);
+      const uint32_t use = uint32_t(lt / BUFS);
+      ptx::mbar_wait(&tfull[buf], use & 1);
+      ptx::tc_fence_after();
+      const int64_t m0 = mb * 256 + rank * 128 + q * 32;
+      const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
+#pragma unroll 1
+      for (int g = 0; g < (BN / 2) / cols_per_grp; ++g) {
+        const int col = half * (BN / 2) + g * cols_per_grp;
+        const int64_t n0 = nb * BN + col;
+        const uint32_t tbase = tmem_base + ((q * 32) << 16) + buf * G::kAccCols + col;
+        uint32_t w[32];
+        if (out_f32) {
+          ptx::tmem_ld_32x32b_x32(tbase, w);
+          ptx::tmem_ld_wait();
+        } else {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld_32x32b_x32(tbase, r0);
+          ptx::tmem_ld_32x32b_x32(tbase + 32, r1);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
+            w[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
+        if (g == (BN / 2) / cols_per_grp - 1) {
+          // last TMEM read of this warp: hand the accumulator back before the stores
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
+        }
+        const int64_t nrem = N - n0;
+        const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
+        if (rows_valid > 0 && bytes_valid > 0)
+          epi_store_rows128(stg, w, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid,
+                            bytes_valid, elt, vec_ok);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
+}  // namespace mxf4x2
+
+template <int BN, int BUFS>
+static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st) {
+  using G = mxf4x2::Cfg<BN, BUFS>;
+  CUtensorMap tma, tmb, tsfa, tsfb;
+  const int64_t kch = sf_kchunks(a.K);
+  if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
+                    uint64_t(a.K / 2), 128, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
+                    uint64_t(a.K / 2), 128, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  // scale factors as uint32 rows of one 128-row group: [groups][kch * 128] u32
+  if (!make_tmap_2d(&tsfa, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.a_sf, uint64_t(kch * 128), uint64_t((a.M + 127) / 128),
+                    uint64_t(kch * 512), 256, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
+                    uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
+  const int64_t clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(2 * clusters));
+  cfg.blockDim = dim3(mxf4x2::kThreads);
+  cfg.dynamicSmemBytes = G::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>, tma, tmb, tsfa, tsfb, a.C,
+                            a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K);
+}
+
+cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st) {
+  if (variant == 256) return launch_2sm<256, 1>(a, num_sms, st);
+  return launch_2sm<128, 2>(a, num_sms, st);
+}
+
+}  // namespace adahop

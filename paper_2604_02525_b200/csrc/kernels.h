@@ -42,6 +42,9 @@ struct Mxf4GemmArgs {
   int64_t ldc, M, N, K;
 };
 cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st);
+// gemm_mxf4_2sm.cu — CTA-pair (cta_group::2) version; variant = 128 (256x128 tiles, double-
+// buffered accumulators) or 256 (256x256 tiles, single accumulator).
+cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st);
 
 // gemm_bf16.cu — D[Mb x Nb] = A[Mb x K] B[Nb x K]^T in BF16 (fp32 accumulate).
 // A/B are K-major (a_mn = 0: A[m*lda + k]) or MN-major (a_mn = 1: A[k*lda + m]).
