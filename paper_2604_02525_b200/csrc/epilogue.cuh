@@ -21,6 +21,42 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo, uint32_t hi) {
 // w[32]: this lane's 128-byte row segment. cbase: address of (row 0, first byte) of the
 // 32-row block in global memory; ldc_bytes: row pitch; rows_valid / bytes_valid clip the
 // M / N tails; elt: element size (2 or 4) for the tail path; vec_ok: 16-byte aligned rows.
+// write this lane's 128-byte row segment into the warp's stage
+__device__ __forceinline__ void epi_stage_row128(uint8_t* stg, const uint32_t (&w)[32]) {
+  const int lane = threadIdx.x & 31;
+  uint4* srow = reinterpret_cast<uint4*>(stg + lane * kEpiPitch);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) srow[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+
+// coalesced copy of a staged 32-row x 128-byte block to global memory
+__device__ __forceinline__ void epi_flush128(const uint8_t* stg, char* cbase, int64_t ldc_bytes, int rows_valid,
+                                             int bytes_valid, int elt, bool vec_ok) {
+  const int lane = threadIdx.x & 31;
+  const int c = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int row = it * 4 + (lane >> 3);
+    if (row < rows_valid) {
+      const int b0 = c * 16;
+      const uint8_t* src = stg + row * kEpiPitch + b0;
+      char* dst = cbase + int64_t(row) * ldc_bytes + b0;
+      if (vec_ok && b0 + 16 <= bytes_valid) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      } else if (b0 < bytes_valid) {
+        const int end = min(b0 + 16, bytes_valid);
+        if (elt == 4) {
+          for (int b = b0; b < end; b += 4)
+            *reinterpret_cast<uint32_t*>(dst + (b - b0)) = *reinterpret_cast<const uint32_t*>(src + (b - b0));
+        } else {
+          for (int b = b0; b < end; b += 2)
+            *reinterpret_cast<uint16_t*>(dst + (b - b0)) = *reinterpret_cast<const uint16_t*>(src + (b - b0));
+        }
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void epi_store_rows128(uint8_t* stg, const uint32_t (&w)[32], char* cbase,
                                                   int64_t ldc_bytes, int rows_valid, int bytes_valid,
                                                   int elt, bool vec_ok) {

@@ -31,10 +31,11 @@ struct Cfg {
   static constexpr int kSfb = (BN / 128) * 1024;      // all BN rows (duplicated in both CTAs)
   static constexpr int kStage = kA + kB + kSfa + kSfb;
   static constexpr int kStages = BN == 256 ? 5 : 7;
+  static constexpr int kEpiBufs = 1;
   static constexpr int kAccCols = BN;
   static constexpr int kSfaCol = 256;                 // after the accumulator buffers
   static constexpr int kSfbCol = 264;
-  static constexpr size_t kSmem = size_t(kStages) * kStage + kEpiWarps * kEpiStageBytes + 1024 + 512;
+  static constexpr size_t kSmem = size_t(kStages) * kStage + kEpiWarps * kEpiBufs * kEpiStageBytes + 1024 + 512;
   static_assert(BUFS * BN <= 256, "accumulators must fit below the scale-factor columns");
 };
 
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + size_t(G::kStages) * G::kStage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiWarps * kEpiStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiWarps * G::kEpiBufs * kEpiStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + G::kStages;
   uint64_t* tfull = bars + 2 * G::kStages;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue (8 warps per CTA)
     const uint32_t q = warp & 3;            // TMEM lane quadrant
     const uint32_t half = (warp - 4) >> 2;  // column half of the tile
-    uint8_t* stg = epi_smem + (warp - 4) * kEpiStageBytes;
+    uint8_t* stg = epi_smem + (warp - 4) * G::kEpiBufs * kEpiStageBytes;
     const int elt = out_f32 ? 4 : 2;
     const int cols_per_grp = 128 / elt;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
@@ -185,6 +186,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const int64_t m0 = mb * 256 + rank * 128 + q * 32;
       const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
+      if (BUFS == 1 && !out_f32) {
+        // bf16 single accumulator: read both column groups out of TMEM (one through the smem
+        // stage, one in registers), hand the accumulator back, then do the global stores so
+        // that they overlap the next tile's main loop
+        const uint32_t tb0 = tmem_base + ((q * 32) << 16) + buf * G::kAccCols + half * (BN / 2);
+        uint32_t w0[32], w1[32];
+        {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld_32x32b_x32(tb0, r0);
+          ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w0[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
+            w0[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
+        {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld_32x32b_x32(tb0 + 64, r0);
+          ptx::tmem_ld_32x32b_x32(tb0 + 96, r1);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w1[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
+            w1[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
+#pragma unroll 1
+        for (int g = 0; g < 2; ++g) {
+          epi_stage_row128(stg, g == 0 ? w0 : w1);
+          __syncwarp();
+          const int64_t n0 = nb * BN + half * (BN / 2) + g * 64;
+          const int64_t nrem = N - n0;
+          const int bytes_valid = int(nrem >= 64 ? 128 : (nrem > 0 ? nrem * 2 : 0));
+          if (rows_valid > 0 && bytes_valid > 0)
+            epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * 2, ldc * 2, rows_valid, bytes_valid, 2,
+                         vec_ok);
+          __syncwarp();
+        }
+        __syncwarp();
+        continue;
+      }
 #pragma unroll 1
       for (int g = 0; g < (BN / 2) / cols_per_grp; ++g) {
         const int col = half * (BN / 2) + g * cols_per_grp;
