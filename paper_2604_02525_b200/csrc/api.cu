@@ -343,6 +343,7 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   GemmPlan g;
   plan_gemm(M, N, K, s, p, dev.sms, &g);
   if (!ws || ws_bytes < g.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  if (g.kk > 0 && g.rows_oe > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
   const bool out_f32 = out_dt == ADAHOP_DT_F32;
@@ -385,7 +386,7 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   if (g.kk > 0) {
     ADAHOP_LAUNCH(launch_foid(oe_src, false, g.rows_oe, K, oe_ld, oe_ks, g.kk, p->foid_probe,
                               reinterpret_cast<double*>(w + g.keys), idx, cs));
-    launches += 2;
+    launches += foid_launches(g.rows_oe, K, p->foid_probe);
   }
   stage_mark(1, cs);
   // ---- 2. IHT + MXFP4 quantisation of both operands (P:761 stage 2); the OE rows are
@@ -507,6 +508,7 @@ adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, 
   if (ld < (k_strided ? R : K)) return ADAHOP_E_INVALID_ARG;
   if (ws_bytes < adahop_debug_workspace_bytes(R, K)) return ADAHOP_E_WORKSPACE;
   const int64_t kk = std::min<int64_t>(k, R);
+  if (R > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
   adahop_status_t st = check_device(nullptr);
   if (st != ADAHOP_OK) return st;
   Carver c;
@@ -516,8 +518,13 @@ adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, 
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys,
                             idx_sorted, cs));
-  if (keys_out)
+  if (keys_out) {
+    if (foid_keys_in_select(R, K, probe)) {
+      // keys computed inside the select kernel are not materialised; produce them explicitly
+      ADAHOP_LAUNCH(launch_foid_keys_only(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, probe, keys, cs));
+    }
     ADAHOP_LAUNCH(cudaMemcpyAsync(keys_out, keys, size_t(R) * 8, cudaMemcpyDeviceToDevice, cs));
+  }
   g_launches = 3;
   return ADAHOP_OK;
 }

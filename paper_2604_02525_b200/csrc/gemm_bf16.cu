@@ -212,8 +212,20 @@ __global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict_
     const int64_t m = m0 + mm;
     const int j = j0 + tx;
     float v = 0.f;
-    if (m < Mb && j < k)
-      for (int s = 0; s < splits; ++s) v += part[(int64_t(s) * Mb + m) * npad + j];
+    if (m < Mb && j < k) {
+      // fixed summation order s = 0, 1, 2, ... (deterministic); loads batched 8 at a time
+      const float* pp = part + m * npad + j;
+      const int64_t stride = Mb * npad;
+      int s = 0;
+      for (; s + 8 <= splits; s += 8) {
+        float t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = pp[(s + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += t[u];
+      }
+      for (; s < splits; ++s) v += pp[s * stride];
+    }
     tile[mm][tx] = v;
   }
   __syncthreads();
@@ -252,7 +264,7 @@ int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms) {
   const int64_t nks = (K + bf16g::BK - 1) / bf16g::BK;
   int64_t s = (2 * num_sms) / mt;            // one full wave of ~2 CTAs per SM
   if (s > nks) s = nks;
-  if (s > 64) s = 64;
+  if (s > 32) s = 32;
   if (s < 1) s = 1;
   return int(s);
 }

@@ -661,14 +661,21 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
   if (r < R) keys[r] = foid_key_seq(mine, p);
 }
 
-// Top-k by (key desc, index asc), written as ascending indices. One CTA: an 8-pass MSB-first
-// radix select (8-bit digits of the fp64 key bits, order-preserving for keys >= 0) finds the
-// k-th largest key T; then all keys > T plus the lowest-indexed keys == T are taken, and a
-// block scan in index order writes them sorted.
+// Top-k by (key desc, index asc), written as ascending indices, in ONE CTA:
+//  * keys (fp64 >= 0, so their bit patterns are order-preserving) are staged in smem; for
+//    small operands the probe keys are computed here too (no separate launch);
+//  * MSB-first radix select with 11-bit digits over a shrinking candidate list: after each
+//    digit only the keys sharing the selected prefix are kept (stable in-place compaction),
+//    so the passes after the exponent digits touch a handful of keys; the select stops as
+//    soon as every remaining candidate is needed;
+//  * a block scan in index order then takes all keys above the prefix plus the
+//    lowest-indexed keys at the prefix, and writes them sorted.
 constexpr int kSelThreads = 1024;
-constexpr int64_t kSelSmemKeys = 24576;   // keys staged in smem up to this many rows
+constexpr int64_t kSelSmemKeys = 16384;   // keys staged in smem up to this many rows
+constexpr int kSelPerThread = int(kSelSmemKeys / kSelThreads);
+constexpr int64_t kSelFuseKeys = 4096;    // compute the keys inside the select kernel up to here
 
-__device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[32]*/, int* total) {
+__device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[33]*/, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
@@ -696,85 +703,117 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[32]*/, int* t
   return res;
 }
 
-__global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __restrict__ keys, int64_t R,
-                                                             int k, int32_t* __restrict__ idx_sorted) {
-  extern __shared__ __align__(16) unsigned long long skeys[];
-  __shared__ unsigned int hist[256];
+template <typename T>
+__global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __restrict__ keys_g, const T* __restrict__ in,
+                                                             int64_t R, int64_t ld, int kstrided, int p, int k,
+                                                             int32_t* __restrict__ idx_sorted) {
+  extern __shared__ __align__(16) unsigned long long skeys[];   // [R] keys, then [R] candidates
+  __shared__ unsigned int hist[2048];
   __shared__ unsigned long long s_prefix;
-  __shared__ int s_kr;
+  __shared__ int s_kr, s_n;
   __shared__ int sbuf[33];
-  const bool in_smem = R <= kSelSmemKeys;
-  const unsigned long long* kb = in_smem ? skeys : reinterpret_cast<const unsigned long long*>(keys);
-  if (in_smem)
-    for (int64_t i = threadIdx.x; i < R; i += blockDim.x)
-      skeys[i] = __double_as_longlong(keys[i]);
-  const int kk = int(int64_t(k) < R ? int64_t(k) : R);
-  unsigned long long prefix = 0;
-  int kr = kk;
-  __syncthreads();
-  for (int pass = 0; pass < 8; ++pass) {
-    const int shift = 56 - 8 * pass;
-    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
-    __syncthreads();
-    // warp-aggregated histogram update: the leading digits of nearby variances coincide, so
-    // lanes with equal digits are merged before the shared-memory atomic
-    const int64_t Rup = (R + 31) & ~int64_t(31);
-    for (int64_t i = threadIdx.x; i < Rup; i += blockDim.x) {
-      int digit = -1;
-      if (i < R) {
-        const unsigned long long u = kb[i];
-        if (pass == 0 || (u >> (shift + 8)) == prefix) digit = int((u >> shift) & 255u);
+  const int tid = threadIdx.x;
+  unsigned long long* cand = skeys + R;
+  // ---- keys
+  if (in != nullptr) {  // fused: compute the probe keys of all R rows here
+    for (int64_t r = tid; r < R; r += blockDim.x) {
+      // two streaming passes (sum, then squared deviations) in the oracle's fixed order
+      double sum = 0.0;
+#pragma unroll 16
+      for (int j = 0; j < p; ++j)
+        sum = __dadd_rn(sum, double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)));
+      const double mu = sum / double(p);
+      double v = 0.0;
+#pragma unroll 16
+      for (int j = 0; j < p; ++j) {
+        const double d = __dsub_rn(double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)), mu);
+        v = __dadd_rn(v, __dmul_rn(d, d));
       }
+      const unsigned long long u = __double_as_longlong(v / double(p));
+      skeys[r] = u;
+      cand[r] = u;
+    }
+  } else {
+    for (int64_t i = tid; i < R; i += blockDim.x) {
+      const unsigned long long u = __double_as_longlong(keys_g[i]);
+      skeys[i] = u;
+      cand[i] = u;
+    }
+  }
+  const int kk = int(int64_t(k) < R ? int64_t(k) : R);
+  int n = int(R);            // live candidates (all share `prefix` above `shift`)
+  int kr = kk;               // rank of the boundary key among the candidates
+  unsigned long long prefix = 0;
+  int shift = 64;
+  bool take_all = false;     // every candidate at the final prefix is selected
+  __syncthreads();
+  for (int pass = 0; pass < 6 && !take_all; ++pass) {
+    const int bits = pass < 5 ? 11 : 9;   // 5 x 11 + 9 = 64
+    const int nshift = shift - bits;
+    for (int i = tid; i < 2048; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int nup = (n + 31) & ~31;
+    for (int i = tid; i < nup; i += blockDim.x) {
+      int digit = -1;
+      if (i < n) digit = int((cand[i] >> nshift) & ((1ull << bits) - 1));
       const unsigned grp = __match_any_sync(0xffffffffu, digit);
-      if (digit >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&hist[digit], unsigned(__popc(grp)));
+      if (digit >= 0 && (tid & 31) == __ffs(grp) - 1) atomicAdd(&hist[digit], unsigned(__popc(grp)));
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-      // lane l owns digits 255-8l .. 248-8l (descending); find the digit holding rank kr
-      const int lane = threadIdx.x;
-      int cnt[8], tot = 0;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { cnt[t] = int(hist[255 - 8 * lane - t]); tot += cnt[t]; }
-      int incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - tot;
-      if (excl < kr && kr <= incl) {
-        int c = excl;
-        for (int t = 0; t < 8; ++t) {
-          if (c + cnt[t] >= kr) {
-            s_prefix = (prefix << 8) | (unsigned long long)(255 - 8 * lane - t);
-            s_kr = kr - c;
-            break;
-          }
-          c += cnt[t];
-        }
+    // find the digit holding rank kr (counting from the largest digit): 1024 threads x 2 bins
+    {
+      const int b0 = 2047 - 2 * tid, b1 = b0 - 1;
+      const int c0 = int(hist[b0]), c1 = int(hist[b1]);
+      int tot;
+      const int before = block_excl_scan(c0 + c1, sbuf, &tot);
+      if (before < kr && kr <= before + c0 + c1) {
+        int d, above;
+        if (kr <= before + c0) { d = b0; above = before; }
+        else { d = b1; above = before + c0; }
+        s_prefix = (prefix << bits) | (unsigned long long)d;
+        s_kr = kr - above;
+        s_n = int(hist[d]);
       }
     }
     __syncthreads();
     prefix = s_prefix;
     kr = s_kr;
-    __syncthreads();
+    const int n_new = s_n;
+    shift = nshift;
+    take_all = n_new == kr;
+    if (pass < 5 && !take_all) {
+      // stable in-place compaction of the candidates carrying the selected digit
+      unsigned long long mine[kSelPerThread];
+      int cnt = 0;
+      const int seg = (n + blockDim.x - 1) / blockDim.x;
+      const int i0 = min(n, tid * seg), i1 = min(n, i0 + seg);
+      for (int i = i0; i < i1; ++i) {
+        const unsigned long long u = cand[i];
+        if ((u >> shift) == prefix) mine[cnt++] = u;
+      }
+      int tot;
+      const int pos = block_excl_scan(cnt, sbuf, &tot);   // contains the barriers we need
+      for (int i = 0; i < cnt; ++i) cand[pos + i] = mine[i];
+      n = tot;
+      __syncthreads();
+    }
   }
-  const unsigned long long T = prefix;   // the kk-th largest key; take kr of the keys == T
-  // per-thread contiguous index segment
+  // ---- selection in index order: keys above the prefix, plus (all | the kr lowest-indexed)
+  //      keys at the prefix
   const int64_t seg = (R + blockDim.x - 1) / blockDim.x;
-  const int64_t i0 = (int64_t(threadIdx.x) * seg < R ? int64_t(threadIdx.x) * seg : R);
+  const int64_t i0 = (int64_t(tid) * seg < R ? int64_t(tid) * seg : R);
   const int64_t i1 = (i0 + seg < R ? i0 + seg : R);
   int n_eq = 0;
-  for (int64_t i = i0; i < i1; ++i) n_eq += kb[i] == T;
+  for (int64_t i = i0; i < i1; ++i) n_eq += (skeys[i] >> shift) == prefix;
   int tot_eq;
-  int eq_before = block_excl_scan(n_eq, sbuf, &tot_eq);
+  const int eq_before = block_excl_scan(n_eq, sbuf, &tot_eq);
   int n_sel = 0;
   {
     int e = eq_before;
     for (int64_t i = i0; i < i1; ++i) {
-      const unsigned long long u = kb[i];
-      if (u > T) ++n_sel;
-      else if (u == T) { if (e < kr) ++n_sel; ++e; }
+      const unsigned long long t = skeys[i] >> shift;
+      if (t > prefix) ++n_sel;
+      else if (t == prefix) { if (take_all || e < kr) ++n_sel; ++e; }
     }
   }
   int tot_sel;
@@ -782,10 +821,10 @@ __global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __res
   {
     int e = eq_before;
     for (int64_t i = i0; i < i1; ++i) {
-      const unsigned long long u = kb[i];
+      const unsigned long long t = skeys[i] >> shift;
       bool take = false;
-      if (u > T) take = true;
-      else if (u == T) { take = e < kr; ++e; }
+      if (t > prefix) take = true;
+      else if (t == prefix) { take = take_all || e < kr; ++e; }
       if (take) idx_sorted[pos++] = int32_t(i);
     }
   }
@@ -794,21 +833,49 @@ __global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __res
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                         int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
                         cudaStream_t st) {
+  if (R > kSelSmemKeys) return cudaErrorInvalidValue;   // host validates first
+  const int p = int(std::min<int64_t>(probe, K));
+  const bool fuse = R <= kSelFuseKeys && p <= kProbeMax;
+  if (!fuse) {
+    const unsigned kb = unsigned((R + 127) / 128);
+    if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
+    else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
+  }
+  const size_t smem = size_t(R) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_foid_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSelSmemKeys * 16));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_foid_select<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kSelSmemKeys * 16));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (in_f32)
+    k_foid_select<float><<<1, kSelThreads, smem, st>>>(keys, fuse ? static_cast<const float*>(in) : nullptr, R, ld,
+                                                        kstrided, p, k, idx_sorted);
+  else
+    k_foid_select<__nv_bfloat16><<<1, kSelThreads, smem, st>>>(
+        keys, fuse ? static_cast<const __nv_bfloat16*>(in) : nullptr, R, ld, kstrided, p, k, idx_sorted);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_foid_keys_only(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld, int kstrided,
+                                  int probe, double* keys, cudaStream_t st) {
   const int p = int(std::min<int64_t>(probe, K));
   const unsigned kb = unsigned((R + 127) / 128);
   if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
   else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
-  const size_t smem = R <= kSelSmemKeys ? size_t(R) * 8 : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSelSmemKeys * 8));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  k_foid_select<<<1, kSelThreads, smem, st>>>(keys, R, k, idx_sorted);
   return cudaGetLastError();
 }
+
+int foid_launches(int64_t R, int64_t K, int probe) {
+  const int p = int(std::min<int64_t>(probe, K));
+  return (R <= kSelFuseKeys && p <= kProbeMax) ? 1 : 2;
+}
+
+bool foid_keys_in_select(int64_t R, int64_t K, int probe) { return foid_launches(R, K, probe) == 1; }
 
 // ================================================================== calibration stats
 // Row statistics: one warp per row, fp64 accumulation, fixed-order shuffle reduction.
