@@ -10,7 +10,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import Params, check, lib
+from ._lib import AdahopError, Params, check, lib
 
 IHT, OE_LEFT_IHT, OE_RIGHT_IHT, BF16 = 0, 1, 2, 3
 STRATEGY = {"IHT": IHT, "OE_LEFT_IHT": OE_LEFT_IHT, "OE_RIGHT_IHT": OE_RIGHT_IHT, "BF16": BF16}
@@ -21,7 +21,7 @@ PATH = {"fwd": 0, "dgrad": 1, "wgrad": 2}
 DT_BF16, DT_F32 = 0, 1
 
 __all__ = [
-    "Params", "IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16", "STRATEGY", "strategy_for_pair",
+    "AdahopError", "Params", "IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16", "STRATEGY", "strategy_for_pair",
     "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
     "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant",
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",

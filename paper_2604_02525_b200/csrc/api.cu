@@ -518,13 +518,8 @@ adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, 
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys,
                             idx_sorted, cs));
-  if (keys_out) {
-    if (foid_keys_in_select(R, K, probe)) {
-      // keys computed inside the select kernel are not materialised; produce them explicitly
-      ADAHOP_LAUNCH(launch_foid_keys_only(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, probe, keys, cs));
-    }
+  if (keys_out)
     ADAHOP_LAUNCH(cudaMemcpyAsync(keys_out, keys, size_t(R) * 8, cudaMemcpyDeviceToDevice, cs));
-  }
   g_launches = 3;
   return ADAHOP_OK;
 }

@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
 constexpr int kSelThreads = 1024;
 constexpr int64_t kSelSmemKeys = 16384;   // keys staged in smem up to this many rows
 constexpr int kSelPerThread = int(kSelSmemKeys / kSelThreads);
-constexpr int64_t kSelFuseKeys = 4096;    // compute the keys inside the select kernel up to here
+constexpr int64_t kSelFuseKeys = 0;       // (in-kernel keys measured slower than the separate kernel)
 
 __device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[33]*/, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -704,16 +704,16 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[33]*/, int* t
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __restrict__ keys_g, const T* __restrict__ in,
+__global__ void __launch_bounds__(kSelThreads) k_foid_select(double* __restrict__ keys_g, const T* __restrict__ in,
                                                              int64_t R, int64_t ld, int kstrided, int p, int k,
                                                              int32_t* __restrict__ idx_sorted) {
-  extern __shared__ __align__(16) unsigned long long skeys[];   // [R] keys, then [R] candidates
+  extern __shared__ __align__(16) unsigned long long cand[];    // [R] candidate keys
   __shared__ unsigned int hist[2048];
   __shared__ unsigned long long s_prefix;
   __shared__ int s_kr, s_n;
   __shared__ int sbuf[33];
   const int tid = threadIdx.x;
-  unsigned long long* cand = skeys + R;
+  const unsigned long long* skeys = reinterpret_cast<const unsigned long long*>(keys_g);  // index order (L2)
   // ---- keys
   if (in != nullptr) {  // fused: compute the probe keys of all R rows here
     for (int64_t r = tid; r < R; r += blockDim.x) {
@@ -729,16 +729,12 @@ __global__ void __launch_bounds__(kSelThreads) k_foid_select(const double* __res
         const double d = __dsub_rn(double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)), mu);
         v = __dadd_rn(v, __dmul_rn(d, d));
       }
-      const unsigned long long u = __double_as_longlong(v / double(p));
-      skeys[r] = u;
-      cand[r] = u;
+      const double key = v / double(p);
+      keys_g[r] = key;
+      cand[r] = __double_as_longlong(key);
     }
   } else {
-    for (int64_t i = tid; i < R; i += blockDim.x) {
-      const unsigned long long u = __double_as_longlong(keys_g[i]);
-      skeys[i] = u;
-      cand[i] = u;
-    }
+    for (int64_t i = tid; i < R; i += blockDim.x) cand[i] = __double_as_longlong(keys_g[i]);
   }
   const int kk = int(int64_t(k) < R ? int64_t(k) : R);
   int n = int(R);            // live candidates (all share `prefix` above `shift`)
@@ -841,14 +837,14 @@ cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64
     if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
     else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
   }
-  const size_t smem = size_t(R) * 16;
+  const size_t smem = size_t(R) * 8;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_foid_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSelSmemKeys * 16));
+                                         int(kSelSmemKeys * 8));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_foid_select<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(kSelSmemKeys * 16));
+                               int(kSelSmemKeys * 8));
     if (e != cudaSuccess) return e;
     attr = true;
   }

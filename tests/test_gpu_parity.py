@@ -115,8 +115,8 @@ def test_iht_quant_extreme_magnitudes():
 # ======================================================================= FOID
 @pytest.mark.parametrize("k_strided", [False, True])
 @pytest.mark.parametrize("R,K,k,probe", [(5000, 128, 64, 64), (300, 96, 8, 64), (2048, 64, 256, 64),
-                                          (4100, 256, 16, 32), (50, 32, 64, 64), (30000, 64, 64, 64),
-                                          (16384, 512, 64, 64)])
+                                          (4100, 256, 16, 32), (50, 32, 64, 64), (16384, 512, 64, 64),
+                                          (16384, 64, 256, 64)])
 def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
     x, planted = synth.operand(R, K, "R", "X", case_id=R + k, count=min(5, R))
     x[10] = x[11]                                  # an exact key tie
@@ -126,6 +126,13 @@ def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
     np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), want_keys.view(np.uint64))
     np.testing.assert_array_equal(idx.cpu().numpy(), O.foid_indices(x, k, probe))
     assert set(planted.rows) <= set(idx.cpu().numpy().tolist())
+
+
+def test_foid_row_limit_is_reported():
+    x = torch.zeros((16385, 64), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(ah.AdahopError if hasattr(ah, "AdahopError") else Exception) as e:
+        ah.debug_foid(x, k=8)
+    assert "unsupported" in str(e.value)
 
 
 # ======================================================================= MXFP4 GEMM
