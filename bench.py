@@ -265,6 +265,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2604_02525_b200 as ah
+    import paper_2604_02525_b200.dist as ahd
+
+    if world > 1 and not args.no_graph:
+        args.no_graph = True     # NCCL collectives are launched eagerly under torchrun
 
     model, pats = workload_spec(args.workload)
     T = args.tokens
@@ -306,7 +310,7 @@ def main():
             else:
                 ah.linear_wgrad(L["gy"], L["x"], g["strategy"], params, out=L["gw"], ws=ws)
                 if world > 1:
-                    dist.all_reduce(L["gw"])
+                    ahd.allreduce_wgrad(L["gw"])     # token-sharded DP: sum the wgrad partials
             if ctx is not None:
                 ctx.__exit__()
             n += ah.last_launch_count()

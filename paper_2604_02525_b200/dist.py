@@ -1,0 +1,109 @@
+"""Data-parallel plumbing of the AdaHOP hot path (token-row sharding).
+
+One process per GPU. Token rows T are split into contiguous per-rank ranges (multiples of
+the Hadamard block, so that the wgrad path's 32-blocks along T never straddle ranks).
+fwd and dgrad are independent per rank; wgrad yields a rank-local partial G_W (with
+rank-local FOID, R12) that is summed by an all-reduce over NVLink (NCCL).
+Calibration merges the per-column statistics (sum for the moments, max for |x|) and the
+per-row CV sums across ranks so every rank classifies — and freezes — the same pattern.
+
+The collective is torch.distributed (NCCL on B200, gloo in the CPU tests); the compute is
+injected (the C ABI by default) so the host logic is testable without a GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def token_shard(t_global: int, world: int, rank: int, align: int = 32) -> tuple[int, int]:
+    """[t0, t1) token rows of `rank`: contiguous, balanced, every boundary a multiple of
+    `align` (the Hadamard block along tokens)."""
+    if t_global % align:
+        raise ValueError(f"global tokens {t_global} must be a multiple of {align}")
+    blocks = t_global // align
+    base, extra = divmod(blocks, world)
+    b0 = rank * base + min(rank, extra)
+    b1 = b0 + base + (1 if rank < extra else 0)
+    return b0 * align, b1 * align
+
+
+def allreduce_wgrad(gw: torch.Tensor, group=None, async_op: bool = False):
+    """Sum the rank-local wgrad partials G_W,r = AdaHOP(G_Y,r^T, X_r) in place."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return None
+    return dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+
+
+def merge_col_stats(col_stats: torch.Tensor, group=None) -> torch.Tensor:
+    """Per-column statistics [cols, 4] = (sum x, sum x^2, sum |x|, max |x|) of the local token
+    rows -> the global ones (sum of the first three, max of the fourth), in place."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        moments = col_stats[:, :3].contiguous()
+        amax = col_stats[:, 3].contiguous()
+        dist.all_reduce(moments, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=group)
+        col_stats[:, :3] = moments
+        col_stats[:, 3] = amax
+    return col_stats
+
+
+def merge_row_cv_sum(row_cv_sum: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum over ranks of sum_i std(T_i,:)/(mean|T_i,:| + eps) of the local rows (App. A)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(row_cv_sum, op=dist.ReduceOp.SUM, group=group)
+    return row_cv_sum
+
+
+@dataclass
+class CalibrationStep:
+    pattern: str
+    cv_row: float
+    cv_col: float
+
+
+def calibrate_sharded(t_local: torch.Tensor, rows_global: int, stats_fn: Callable, classify_fn: Callable,
+                      classify_cv_fn: Callable, group=None) -> CalibrationStep:
+    """One calibration step of one token-sharded tensor (rows = tokens).
+
+    stats_fn(t) -> (row_stats [rows_local,4], col_stats [cols,4]) (adahop_stats);
+    classify_fn(row_stats, col_stats, row_len, col_count) -> (cv_sums[2], pattern) (adahop_classify);
+    classify_cv_fn(cv_row, cv_col) -> pattern (adahop_classify_cv)."""
+    rows_local, cols = t_local.shape
+    row_stats, col_stats = stats_fn(t_local)
+    merge_col_stats(col_stats, group)
+    cv, _ = classify_fn(row_stats, col_stats, cols, rows_global)
+    cv = cv.clone()
+    row_sum = cv[:1].clone()
+    merge_row_cv_sum(row_sum, group)
+    cv_row = float(row_sum.item()) / rows_global
+    cv_col = float(cv[1].item()) / cols
+    return CalibrationStep(classify_cv_fn(cv_row, cv_col), cv_row, cv_col)
+
+
+class DataParallelLinear:
+    """fwd / dgrad / wgrad of one linear on this rank's token shard, AdaHOP strategies fixed
+    per path at calibration time; wgrad partials are all-reduced."""
+
+    def __init__(self, strategies: dict, params=None, group=None, compute: Optional[dict] = None):
+        self.strategies = strategies
+        self.params = params
+        self.group = group
+        if compute is None:
+            from . import adahop as ah
+            compute = {"fwd": ah.linear_fwd, "dgrad": ah.linear_dgrad, "wgrad": ah.linear_wgrad}
+        self.compute = compute
+
+    def forward(self, x_local, w, **kw):
+        return self.compute["fwd"](x_local, w, self.strategies["fwd"], self.params, **kw)
+
+    def dgrad(self, gy_local, w, **kw):
+        return self.compute["dgrad"](gy_local, w, self.strategies["dgrad"], self.params, **kw)
+
+    def wgrad(self, gy_local, x_local, async_op: bool = False, **kw):
+        gw = self.compute["wgrad"](gy_local, x_local, self.strategies["wgrad"], self.params, **kw)
+        work = allreduce_wgrad(gw, self.group, async_op=async_op)
+        return (gw, work) if async_op else gw

@@ -1,0 +1,150 @@
+"""World-size-2 gloo tests (CPU) of the data-parallel host logic in paper_2604_02525_b200.dist:
+token sharding, the wgrad all-reduce and the calibration merge. The per-shard compute is the
+CPU oracle (injected), so the DP result must equal the sum of per-shard oracle results
+ and calibration must equal the single-process classification of the whole
+tensor."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import synth
+
+dist_mod = pytest.importorskip("paper_2604_02525_b200.dist")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def spawn(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_token_shard_covers_and_aligns():
+    for T, world in ((16384, 8), (16384, 3), (320, 4), (32, 1)):
+        ranges = [dist_mod.token_shard(T, world, r) for r in range(world)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == T
+        for (a, b), (c, d) in zip(ranges, ranges[1:]):
+            assert b == c
+        assert all(a % 32 == 0 and b % 32 == 0 for a, b in ranges)
+        sizes = [b - a for a, b in ranges]
+        assert max(sizes) - min(sizes) <= 32
+    with pytest.raises(ValueError):
+        dist_mod.token_shard(100, 2, 0)
+
+
+# -------------------------------------------------------------------------------- wgrad DP
+T, D_IN, D_OUT, K_OE = 256, 128, 96, 8
+
+
+def _inputs():
+    x, _ = synth.operand(T, D_IN, "C", "X", case_id=901)
+    gy, _ = synth.operand(T, D_OUT, "C", "GY", case_id=902)
+    return x, gy
+
+
+def _oracle_wgrad(gy, x, strategy, params, **kw):
+    g = O.linear("wgrad", strategy, x=x.numpy(), gy=gy.numpy(), k=K_OE)
+    return torch.from_numpy(g)
+
+
+def _dp_wgrad(rank, world):
+    x, gy = _inputs()
+    t0, t1 = dist_mod.token_shard(T, world, rank)
+    lin = dist_mod.DataParallelLinear({"fwd": "IHT", "dgrad": "IHT", "wgrad": O.OE_RIGHT}, params=None,
+                                      compute={"wgrad": _oracle_wgrad})
+    gw = lin.wgrad(torch.from_numpy(gy[t0:t1]), torch.from_numpy(x[t0:t1]))
+    return gw.numpy()
+
+
+def test_wgrad_allreduce_equals_sum_of_shard_oracles():
+    out = spawn(_dp_wgrad)
+    x, gy = _inputs()
+    want = sum(O.linear("wgrad", O.OE_RIGHT, x=x[a:b], gy=gy[a:b], k=K_OE)
+               for a, b in (dist_mod.token_shard(T, 2, r) for r in range(2)))
+    for r in (0, 1):
+        np.testing.assert_allclose(out[r], want, rtol=1e-12, atol=1e-15)
+    np.testing.assert_array_equal(out[0], out[1])
+    # rank-local FOID makes the DP result differ from the single-GPU one, but both stay close
+    # to the exact product (the method's approximation error)
+    exact = gy.astype(np.float64).T @ x.astype(np.float64)
+    single = O.linear("wgrad", O.OE_RIGHT, x=x, gy=gy, k=K_OE)
+    assert np.linalg.norm(out[0] - exact) / np.linalg.norm(exact) < 0.2
+    assert np.linalg.norm(single - exact) / np.linalg.norm(exact) < 0.2
+
+
+# -------------------------------------------------------------------------------- calibration
+def _np_stats(t):
+    t = t.numpy().astype(np.float64)
+    rs = np.stack([t.sum(1), (t * t).sum(1), np.abs(t).sum(1), np.abs(t).max(1)], 1)
+    cs = np.stack([t.sum(0), (t * t).sum(0), np.abs(t).sum(0), np.abs(t).max(0)], 1)
+    return torch.from_numpy(rs), torch.from_numpy(cs)
+
+
+def _np_classify(rs, cs, row_len, col_count, eps=1e-8):
+    rs = rs.numpy()
+    cs = cs.numpy()
+
+    def cv(st, n):
+        mu = st[:, 0] / n
+        var = np.maximum(st[:, 1] / n - mu * mu, 0)
+        return np.sum(np.sqrt(var) / (st[:, 2] / n + eps))
+
+    return torch.tensor([cv(rs, row_len), cv(cs, col_count)], dtype=torch.float64), None
+
+
+def _classify_cv(cv_row, cv_col):
+    if cv_col > 2.0 and (cv_row <= 2.0 or cv_col >= cv_row):
+        return "R"
+    return "C" if cv_row > 2.0 else "N"
+
+
+def _dp_calib(rank, world):
+    res = {}
+    for p in "RCN":
+        t, _ = synth.operand(512, 256, p, "GY", case_id=903)
+        a, b = dist_mod.token_shard(512, world, rank)
+        step = dist_mod.calibrate_sharded(torch.from_numpy(t[a:b]), 512, _np_stats, _np_classify, _classify_cv)
+        res[p] = (step.pattern, step.cv_row, step.cv_col)
+    return res
+
+
+def test_sharded_calibration_matches_global_oracle():
+    out = spawn(_dp_calib)
+    for p in "RCN":
+        t, _ = synth.operand(512, 256, p, "GY", case_id=903)
+        cr, cc = O.cv_row_col(t)
+        for r in (0, 1):
+            pat, cvr, cvc = out[r][p]
+            assert pat == O.classify(t) == p
+            assert abs(cvr - cr) < 1e-9 * cr and abs(cvc - cc) < 1e-9 * cc
