@@ -172,6 +172,21 @@ adahop_status_t adahop_linear_wgrad(const void* GY, const void* X, void* GW, ada
                                     const adahop_params_t* p, void* ws, size_t ws_bytes,
                                     adahop_stream_t stream);
 
+/* One linear layer's three matmuls at once (fwd Y = X W^T, dgrad G_X = G_Y W, wgrad
+ * G_W = G_Y^T X) with strategies s[0..2] = {fwd, dgrad, wgrad}. Same results as the
+ * three calls above, but every input tensor is read once: a dual-orientation quantisation
+ * pass emits both FP4 layouts of X (fwd A, wgrad B), W (fwd B, dgrad B) and G_Y (dgrad A,
+ * wgrad A) — the quantised copies the paper keeps for backward. Requires T, d_in,
+ * d_out multiples of 32 and d_in, d_out multiples of 8. Outputs Y [T x d_out],
+ * G_X [T x d_in], G_W [d_out x d_in] contiguous in out_dt. G_W is this rank's partial under
+ * token sharding (the caller all-reduces it). */
+size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                    const adahop_params_t* p);
+adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
+                                    adahop_dtype_t out_dt, int64_t T, int64_t d_in, int64_t d_out,
+                                    const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
+                                    size_t ws_bytes, adahop_stream_t stream);
+
 /* ------------------------------------------------------- debug / parity entry points */
 
 /* Fused IHT + MXFP4 quantisation of a stored operand (the production kernels), with the

@@ -51,6 +51,8 @@ SIGNATURES = {
     "adahop_linear_fwd": (I32, [P, P, P, I32, I64, I64, I64, I32, PP, P, SZ, P]),
     "adahop_linear_dgrad": (I32, [P, P, P, I32, I64, I64, I64, I32, PP, P, SZ, P]),
     "adahop_linear_wgrad": (I32, [P, P, P, I32, I64, I64, I64, I32, PP, P, SZ, P]),
+    "adahop_layer_workspace_bytes": (SZ, [I64, I64, I64, C.POINTER(I32), PP]),
+    "adahop_linear_layer": (I32, [P, P, P, P, P, P, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P]),
     "adahop_debug_iht_quant": (I32, [P, I32, I64, I64, I64, I32, P, I32, P, P, P, P, SZ, P]),
     "adahop_debug_workspace_bytes": (SZ, [I64, I64]),
     "adahop_debug_foid": (I32, [P, I32, I64, I64, I64, I32, I32, I32, P, P, P, SZ, P]),

@@ -25,7 +25,7 @@ __all__ = [
     "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
     "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant",
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
-    "Workspace", "StageEvents",
+    "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes",
 ]
 
 
@@ -300,3 +300,31 @@ class StageEvents:
     def times_ms(self):
         ev = self.events
         return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(self.NAMES)}
+
+
+def linear_layer(x, w, gy, strategies, params=None, out_dtype=torch.bfloat16, out=None, ws=None):
+    """fwd / dgrad / wgrad of one linear in one call (adahop_linear_layer): every input tensor
+    is quantised once in both orientations. strategies = (fwd, dgrad, wgrad)."""
+    p = params or Params()
+    T, d_in = x.shape
+    d_out = w.shape[0]
+    for t in (x, w, gy):
+        assert t.is_contiguous() and t.dtype == torch.bfloat16
+    s = (C.c_int32 * 3)(*[_strategy(v) for v in strategies])
+    if out is None:
+        out = (torch.empty((T, d_out), dtype=out_dtype, device=x.device),
+               torch.empty((T, d_in), dtype=out_dtype, device=x.device),
+               torch.empty((d_out, d_in), dtype=out_dtype, device=x.device))
+    y, gx, gw = out
+    n = lib.adahop_layer_workspace_bytes(T, d_in, d_out, s, C.byref(p))
+    wbuf = _ws(n, ws, x.device)
+    check("adahop_linear_layer",
+          lib.adahop_linear_layer(_ptr(x), _ptr(w), _ptr(gy), _ptr(y), _ptr(gx), _ptr(gw), _dt(y), T, d_in, d_out,
+                                  s, C.byref(p), _ptr(wbuf), wbuf.numel(), _stream()))
+    return y, gx, gw
+
+
+def layer_workspace_bytes(T, d_in, d_out, strategies, params=None) -> int:
+    p = params or Params()
+    s = (C.c_int32 * 3)(*[_strategy(v) for v in strategies])
+    return lib.adahop_layer_workspace_bytes(T, d_in, d_out, s, C.byref(p))

@@ -425,6 +425,224 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   return ADAHOP_OK;
 }
 
+// ------------------------------------------------------------------------ layer step
+// One linear layer's three matmuls with each operand tensor read ONCE by the
+// dual-orientation quantiser (X: fwd + wgrad, W: fwd + dgrad, G_Y: dgrad + wgrad).
+}  // extern "C"
+
+namespace {
+
+struct LayerPlan {
+  // per tensor (0 = X [T x d_in], 1 = W [d_out x d_in], 2 = G_Y [T x d_out])
+  int64_t R[3], C[3];
+  bool need_row[3], need_col[3];
+  size_t q_row[3], sf_row[3], q_col[3], sf_col[3];
+  // masks: which FOID feeds which (tensor, orientation)
+  int kk_row[3], kk_col[3];
+  size_t idx_row[3], idx_col[3], slice_row[3], slice_col[3];
+  size_t keys = 0, part = 0;
+  int splits[3];
+  int64_t npad[3], mbig[3];
+  size_t total = 0;
+};
+
+// path p: (A tensor, A orientation, B tensor, B orientation); orientation 0 = row, 1 = col
+constexpr int kPathA[3] = {0, 2, 2}, kPathAo[3] = {0, 0, 1};
+constexpr int kPathB[3] = {1, 1, 0}, kPathBo[3] = {0, 1, 1};
+
+void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p,
+                int sms, LayerPlan* L) {
+  *L = LayerPlan{};
+  L->R[0] = T; L->C[0] = d_in;
+  L->R[1] = d_out; L->C[1] = d_in;
+  L->R[2] = T; L->C[2] = d_out;
+  for (int t = 0; t < 3; ++t) { L->kk_row[t] = L->kk_col[t] = 0; L->need_row[t] = L->need_col[t] = false; }
+  int64_t maxR = 0;
+  for (int path = 0; path < 3; ++path) {
+    if (s[path] == ADAHOP_BF16) continue;
+    const int ta = kPathA[path], tb = kPathB[path];
+    (kPathAo[path] ? L->need_col : L->need_row)[ta] = true;
+    (kPathBo[path] ? L->need_col : L->need_row)[tb] = true;
+    if (p->oe_k > 0 && (s[path] == ADAHOP_OE_LEFT_IHT || s[path] == ADAHOP_OE_RIGHT_IHT)) {
+      const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
+      const int t = left ? ta : tb;
+      const int o = left ? kPathAo[path] : kPathBo[path];
+      const int64_t rows = o ? L->C[t] : L->R[t];        // stored rows of the OE operand
+      const int kk = int(std::min<int64_t>(p->oe_k, rows));
+      (o ? L->kk_col : L->kk_row)[t] = kk;
+      maxR = std::max(maxR, rows);
+    }
+  }
+  Carver c;
+  for (int t = 0; t < 3; ++t) {
+    const int64_t R = L->R[t], C = L->C[t];
+    if (L->need_row[t]) { L->q_row[t] = c.take(size_t(R) * size_t(C / 2)); L->sf_row[t] = c.take(size_t(sf_bytes(R, C))); }
+    if (L->need_col[t]) { L->q_col[t] = c.take(size_t(C) * size_t(R / 2)); L->sf_col[t] = c.take(size_t(sf_bytes(C, R))); }
+    if (L->kk_row[t]) { L->idx_row[t] = c.take(size_t(L->kk_row[t]) * 4); L->slice_row[t] = c.take(size_t(L->kk_row[t]) * size_t(C) * 2); }
+    if (L->kk_col[t]) { L->idx_col[t] = c.take(size_t(L->kk_col[t]) * 4); L->slice_col[t] = c.take(size_t(L->kk_col[t]) * size_t(R) * 2); }
+  }
+  L->keys = c.take(size_t(std::max<int64_t>(maxR, 1)) * 8);
+  size_t part_bytes = 0;
+  const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
+  for (int path = 0; path < 3; ++path) {
+    L->splits[path] = 1; L->npad[path] = 0; L->mbig[path] = 0;
+    if (p->oe_k <= 0 || (s[path] != ADAHOP_OE_LEFT_IHT && s[path] != ADAHOP_OE_RIGHT_IHT)) continue;
+    const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
+    const int t = left ? kPathA[path] : kPathB[path];
+    const int kk = (left ? kPathAo[path] : kPathBo[path]) ? L->kk_col[t] : L->kk_row[t];
+    L->mbig[path] = left ? MNK[path][1] : MNK[path][0];
+    L->npad[path] = bf16_gemm_npad(kk);
+    L->splits[path] = bf16_gemm_splits(L->mbig[path], MNK[path][2], sms);
+    part_bytes = std::max(part_bytes, size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4);
+  }
+  if (part_bytes) L->part = c.take(part_bytes);
+  L->total = c.take(0) + 256;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                    const adahop_params_t* p) {
+  if (!s || !p || T <= 0 || d_in <= 0 || d_out <= 0) return 0;
+  DevInfo d = dev_info();
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, d.ok ? d.sms : 148, &L);
+  return L.total;
+}
+
+adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
+                                    adahop_dtype_t out_dt, int64_t T, int64_t d_in, int64_t d_out,
+                                    const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
+                                    size_t ws_bytes, adahop_stream_t stream) {
+  if (!X || !W || !GY || !Y || !GX || !GW || !s || !p) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = validate_params(p);
+  if (st != ADAHOP_OK) return st;
+  for (int i = 0; i < 3; ++i)
+    if (s[i] < ADAHOP_IHT || s[i] > ADAHOP_BF16) return ADAHOP_E_INVALID_ARG;
+  if (out_dt != ADAHOP_DT_BF16 && out_dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
+  if (T <= 0 || d_in <= 0 || d_out <= 0) return ADAHOP_E_SHAPE;
+  if (T % 32 || d_in % 32 || d_out % 32) return ADAHOP_E_SHAPE;
+  if ((d_in % 8) || (d_out % 8)) return ADAHOP_E_INVALID_ARG;
+  for (const void* q : {X, W, GY, static_cast<const void*>(Y), static_cast<const void*>(GX), static_cast<const void*>(GW)})
+    if (!aligned16(q)) return ADAHOP_E_INVALID_ARG;
+  if (T * (std::max(d_in, d_out) / 64 + 1) >= (int64_t(1) << 31)) return ADAHOP_E_UNSUPPORTED;
+  DevInfo dev;
+  st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, dev.sms, &L);
+  if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  for (int t = 0; t < 3; ++t) {
+    if (L.kk_row[t] && L.R[t] > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
+    if (L.kk_col[t] && L.C[t] > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
+  }
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const bool out_f32 = out_dt == ADAHOP_DT_F32;
+  const __nv_bfloat16* src[3] = {static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W),
+                                 static_cast<const __nv_bfloat16*>(GY)};
+  int32_t launches = 0;
+  stage_mark(0, cs);
+  // ---- 1. FOID for every OE operand: row orientation = rows of the tensor
+  //         (K-contiguous probe), column orientation = columns (probe = first 64 rows)
+  for (int t = 0; t < 3; ++t) {
+    if (L.kk_row[t]) {
+      ADAHOP_LAUNCH(launch_foid(src[t], false, L.R[t], L.C[t], L.C[t], 0, L.kk_row[t], p->foid_probe,
+                                reinterpret_cast<double*>(w + L.keys), reinterpret_cast<int32_t*>(w + L.idx_row[t]), cs));
+      launches += foid_launches(L.R[t], L.C[t], p->foid_probe);
+    }
+    if (L.kk_col[t]) {
+      ADAHOP_LAUNCH(launch_foid(src[t], false, L.C[t], L.R[t], L.C[t], 1, L.kk_col[t], p->foid_probe,
+                                reinterpret_cast<double*>(w + L.keys), reinterpret_cast<int32_t*>(w + L.idx_col[t]), cs));
+      launches += foid_launches(L.C[t], L.R[t], p->foid_probe);
+    }
+  }
+  stage_mark(1, cs);
+  // ---- 2. one quantisation pass per tensor (both orientations when both are consumed)
+  for (int t = 0; t < 3; ++t) {
+    const int64_t R = L.R[t], C = L.C[t];
+    const int32_t* rz = L.kk_row[t] ? reinterpret_cast<const int32_t*>(w + L.idx_row[t]) : nullptr;
+    const int32_t* cz = L.kk_col[t] ? reinterpret_cast<const int32_t*>(w + L.idx_col[t]) : nullptr;
+    __nv_bfloat16* srow = L.kk_row[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_row[t]) : nullptr;
+    __nv_bfloat16* scol = L.kk_col[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_col[t]) : nullptr;
+    if (L.need_row[t] && ((R % 128) || (C % 256)))
+      ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_row[t], 0, size_t(sf_bytes(R, C)), cs));
+    if (L.need_col[t] && ((C % 128) || (R % 256)))
+      ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
+    if (L.need_row[t] && L.need_col[t]) {
+      ADAHOP_LAUNCH(launch_iht_quant_dual(src[t], R, C, C, rz, L.kk_row[t], srow, w + L.q_row[t], w + L.sf_row[t],
+                                          cz, L.kk_col[t], scol, w + L.q_col[t], w + L.sf_col[t], dev.sms, cs));
+      launches += 1;
+    } else if (L.need_row[t]) {
+      ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], w + L.q_row[t], w + L.sf_row[t],
+                                     nullptr, srow, false, dev.sms, cs));
+      launches += 1;
+    } else if (L.need_col[t]) {
+      ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], w + L.q_col[t], w + L.sf_col[t],
+                                     nullptr, scol, false, dev.sms, cs));
+      launches += 1;
+    }
+  }
+  stage_mark(2, cs);
+  // ---- 3. the three MXFP4 GEMMs (or BF16 for Lv2 CC)
+  void* out[3] = {Y, GX, GW};
+  const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
+  const int64_t ldc[3] = {d_out, d_in, d_in};
+  // raw operand views per path: A_store / B_store as (ptr, kstrided, ld)
+  const void* rawA[3] = {X, GY, GY};
+  const int rawAks[3] = {0, 0, 1};
+  const int64_t rawAld[3] = {d_in, d_out, d_out};
+  const void* rawB[3] = {W, W, X};
+  const int rawBks[3] = {0, 1, 1};
+  const int64_t rawBld[3] = {d_in, d_in, d_in};
+  for (int path = 0; path < 3; ++path) {
+    const int64_t M = MNK[path][0], N = MNK[path][1], K = MNK[path][2];
+    if (s[path] == ADAHOP_BF16) {
+      Bf16GemmArgs ga{};
+      ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path];
+      ga.B = static_cast<const __nv_bfloat16*>(rawB[path]); ga.b_mn = rawBks[path]; ga.ldb = rawBld[path];
+      ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = out[path]; ga.out_f32 = out_f32; ga.ldc = ldc[path];
+      ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+      launches += 1;
+      continue;
+    }
+    const int ta = kPathA[path], tb = kPathB[path];
+    const uint8_t* qa = w + (kPathAo[path] ? L.q_col[ta] : L.q_row[ta]);
+    const uint8_t* qa_sf = w + (kPathAo[path] ? L.sf_col[ta] : L.sf_row[ta]);
+    const uint8_t* qb = w + (kPathBo[path] ? L.q_col[tb] : L.q_row[tb]);
+    const uint8_t* qb_sf = w + (kPathBo[path] ? L.sf_col[tb] : L.sf_row[tb]);
+    Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], out_f32, ldc[path], M, N, K};
+    ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
+    launches += 1;
+  }
+  stage_mark(3, cs);
+  // ---- 4. BF16 outlier GEMMs + scatter into the outputs (disjoint support)
+  for (int path = 0; path < 3; ++path) {
+    if (L.mbig[path] == 0) continue;
+    const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
+    const int t = left ? kPathA[path] : kPathB[path];
+    const bool col = left ? kPathAo[path] : kPathBo[path];
+    const int kk = col ? L.kk_col[t] : L.kk_row[t];
+    const int32_t* idx = reinterpret_cast<const int32_t*>(w + (col ? L.idx_col[t] : L.idx_row[t]));
+    const __nv_bfloat16* slice = reinterpret_cast<const __nv_bfloat16*>(w + (col ? L.slice_col[t] : L.slice_row[t]));
+    Bf16GemmArgs ga{};
+    if (!left) { ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path]; }
+    else { ga.A = static_cast<const __nv_bfloat16*>(rawB[path]); ga.a_mn = rawBks[path]; ga.lda = rawBld[path]; }
+    ga.B = slice; ga.b_mn = 0; ga.ldb = MNK[path][2];
+    ga.Mb = L.mbig[path]; ga.Nb = kk; ga.K = MNK[path][2]; ga.mode = 1;
+    ga.part = reinterpret_cast<float*>(w + L.part); ga.splits = L.splits[path]; ga.npad = L.npad[path];
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    ADAHOP_LAUNCH(launch_outlier_reduce(ga.part, ga.splits, ga.Mb, ga.npad, kk, idx, !left, out[path], out_f32,
+                                        ldc[path], cs));
+    launches += 2;
+  }
+  stage_mark(4, cs);
+  g_launches = launches;
+  return ADAHOP_OK;
+}
+
 size_t adahop_workspace_bytes(adahop_path_t path, int64_t T, int64_t d_in, int64_t d_out,
                               adahop_strategy_t s, const adahop_params_t* p) {
   switch (path) {

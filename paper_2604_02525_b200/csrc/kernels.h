@@ -14,6 +14,13 @@ cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, 
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
                              uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
                              int num_sms, cudaStream_t st);
+// One pass over bf16 T [R x C] (pitch ld): row quantisation (rows, K = C) and column
+// quantisation (columns, K = R), each with its own OE mask / slice (nullable).
+cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld,
+                                  const int32_t* row_zero, int nrow_zero, __nv_bfloat16* slice_row,
+                                  uint8_t* q_row, uint8_t* sf_row, const int32_t* col_zero, int ncol_zero,
+                                  __nv_bfloat16* slice_col, uint8_t* q_col, uint8_t* sf_col, int num_sms,
+                                  cudaStream_t st);
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
 // FOID: probe keys (keys[R], fp64) + single-CTA radix top-k -> idx_sorted[min(k,R)].

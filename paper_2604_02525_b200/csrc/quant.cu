@@ -409,6 +409,194 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Dual-orientation IHT + MXFP4 quantisation: ONE pass over a bf16 tensor T [R x C] emits
+//   the row quantisation   (stored rows = the R rows,    K = C) -> q_row, sf_row
+//   the column quantisation (stored rows = the C columns, K = R) -> q_col, sf_col
+// with independent OE masks for each orientation (row_zero: rows of T extracted from the
+// row quantisation, gathered raw into slice_row [k x C]; col_zero: columns of T extracted
+// from the column quantisation, gathered into slice_col [k x R]). This is how X, W and G_Y
+// feed both of their matmuls (X: fwd + wgrad, W: fwd + dgrad, G_Y: dgrad + wgrad) from a
+// single HBM read — the quantised copies are what the paper saves for backward.
+// Tiles: 128 rows x 128 cols, loaded by TMA as two 128B-swizzled 64-column boxes into a
+// 3-stage ring; thread t quantises one row pair-of-blocks and one column pair per tile.
+// ------------------------------------------------------------------------------------
+struct DualOut {
+  uint8_t* q_row; uint8_t* sf_row; const int32_t* row_zero; int nrow_zero; __nv_bfloat16* slice_row;
+  uint8_t* q_col; uint8_t* sf_col; const int32_t* col_zero; int ncol_zero; __nv_bfloat16* slice_col;
+};
+
+template <bool kSwCvt>
+__global__ void __launch_bounds__(256, 2) k_iht_quant_dual(const __grid_constant__ CUtensorMap tm, int64_t R,
+                                                           int64_t C, const DualOut o) {
+  constexpr int TR = 128, TC = 128, kBox = 16384;
+  extern __shared__ __align__(1024) uint8_t smem_dual[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dual) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQStages * kQTileBytes);
+  const int64_t rtiles = (R + TR - 1) / TR, ctiles = (C + TC - 1) / TC;
+  const int64_t ntiles = rtiles * ctiles;
+  const int64_t kch_row = sf_kchunks(C), kch_col = sf_kchunks(R);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tm);
+    for (int i = 0; i < kQStages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  auto issue = [&](int64_t tile, int st) {
+    // row-tile fastest: consecutive CTAs share the same column strip of the output
+    const int64_t rt = tile % rtiles, ct = tile / rtiles;
+    ptx::mbar_arrive_expect_tx(&full[st], 2 * kBox);
+    uint8_t* dst = ring + st * kQTileBytes;
+    ptx::tma_load_2d(dst, &tm, &full[st], int32_t(ct * TC), int32_t(rt * TR));
+    ptx::tma_load_2d(dst + kBox, &tm, &full[st], int32_t(ct * TC + 64), int32_t(rt * TR));
+  };
+  if (tid == 0)
+    for (int i = 0; i < kQStages; ++i)
+      if (first + i * stride < ntiles) issue(first + i * stride, i);
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += stride, ++it) {
+    const int st = it % kQStages;
+    ptx::mbar_wait(&full[st], uint32_t((it / kQStages) & 1));
+    const int64_t rt = tile % rtiles, ct = tile / rtiles;
+    const uint8_t* tb = ring + st * kQTileBytes;
+    // row part: row rr, the 64 columns of box bx; column part: columns 2cp, 2cp+1, rows
+    // rb*32 .. +32 (both read straight from the swizzled stage, one after the other to keep
+    // the register footprint at one 64-value pair)
+    const int rr = tid & 127, bx = tid >> 7;
+    const int cp = tid & 63, rb = tid >> 6;
+    uint64_t P[32];
+    {
+      const uint8_t* row = tb + bx * kBox + rr * 128;
+      const int sw = rr & 7;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 ua = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
+        const uint4 ub = *reinterpret_cast<const uint4*>(row + (((j + 4) ^ sw) << 4));
+        const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w};
+        const uint32_t wb[4] = {ub.x, ub.y, ub.z, ub.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          P[8 * j + 2 * t] = f2_pack(bf16lo(wa[t]), bf16lo(wb[t]));
+          P[8 * j + 2 * t + 1] = f2_pack(bf16hi(wa[t]), bf16hi(wb[t]));
+        }
+      }
+    }
+    // ---- row quantisation: stored row r0 + rr, K-blocks kb0, kb0 + 1 along C
+    {
+      const int64_t r = rt * TR + rr;
+      const int64_t kb0 = (ct * TC + bx * 64) / kBlk;
+      const bool va = r < R && kb0 * kBlk < C, vb = r < R && (kb0 + 1) * kBlk < C;
+      if (o.nrow_zero > 0 && va) {
+        const int s = find_sorted(o.row_zero, o.nrow_zero, r);
+        if (s >= 0) {
+          float x[32];
+          if (o.slice_row) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
+            store_slice32(o.slice_row + int64_t(s) * C + kb0 * kBlk, x);
+            if (vb) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
+              store_slice32(o.slice_row + int64_t(s) * C + (kb0 + 1) * kBlk, x);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) P[i] = 0ull;
+        }
+      }
+      uint4 c0, c1;
+      uint32_t s0, s1;
+      float ydummy[1];
+      iht_quant_pair<false, kSwCvt>(P, c0, c1, s0, s1, ydummy, ydummy);
+      if (va) {
+        *reinterpret_cast<uint4*>(o.q_row + r * (C / 2) + kb0 * 16) = c0;
+        o.sf_row[sf_offset(r, kb0, kch_row)] = uint8_t(s0);
+      }
+      if (vb) {
+        *reinterpret_cast<uint4*>(o.q_row + r * (C / 2) + (kb0 + 1) * 16) = c1;
+        o.sf_row[sf_offset(r, kb0 + 1, kch_row)] = uint8_t(s1);
+      }
+    }
+    {
+      const int cb = (2 * cp) >> 6, cc = (2 * cp) & 63;   // box, column within box
+      const uint8_t* box = tb + cb * kBox;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int r = rb * 32 + i;
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(
+            box + r * 128 + ((((cc * 2) >> 4) ^ (r & 7)) << 4) + ((cc * 2) & 15));
+        P[i] = f2_pack(bf16lo(w), bf16hi(w));
+      }
+    }
+    __syncthreads();                                   // stage consumed by every thread
+    if (tid == 0 && tile + kQStages * stride < ntiles) issue(tile + kQStages * stride, st);
+    // ---- column quantisation: stored rows c0 + 2cp, +1; K-block along R
+    {
+      const int64_t ca = ct * TC + 2 * cp, cb2 = ca + 1;
+      const int64_t kb = (rt * TR) / kBlk + rb;
+      const bool va = ca < C && kb * kBlk < R, vb = cb2 < C && kb * kBlk < R;
+      if (o.ncol_zero > 0) {
+        const int sa = va ? find_sorted(o.col_zero, o.ncol_zero, ca) : -1;
+        const int sb = vb ? find_sorted(o.col_zero, o.ncol_zero, cb2) : -1;
+        if (sa >= 0 || sb >= 0) {
+          float x[32];
+          if (sa >= 0 && o.slice_col) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
+            store_slice32(o.slice_col + int64_t(sa) * R + kb * kBlk, x);
+          }
+          if (sb >= 0 && o.slice_col) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
+            store_slice32(o.slice_col + int64_t(sb) * R + kb * kBlk, x);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) P[i] = f2_pack(sa >= 0 ? 0.f : f2_lo(P[i]), sb >= 0 ? 0.f : f2_hi(P[i]));
+        }
+      }
+      uint4 c0, c1;
+      uint32_t s0, s1;
+      float ydummy[1];
+      iht_quant_pair<false, kSwCvt>(P, c0, c1, s0, s1, ydummy, ydummy);
+      if (va) {
+        *reinterpret_cast<uint4*>(o.q_col + ca * (R / 2) + kb * 16) = c0;
+        o.sf_col[sf_offset(ca, kb, kch_col)] = uint8_t(s0);
+      }
+      if (vb) {
+        *reinterpret_cast<uint4*>(o.q_col + cb2 * (R / 2) + kb * 16) = c1;
+        o.sf_col[sf_offset(cb2, kb, kch_col)] = uint8_t(s1);
+      }
+    }
+  }
+}
+
+cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld,
+                                  const int32_t* row_zero, int nrow_zero, __nv_bfloat16* slice_row,
+                                  uint8_t* q_row, uint8_t* sf_row, const int32_t* col_zero, int ncol_zero,
+                                  __nv_bfloat16* slice_col, uint8_t* q_col, uint8_t* sf_col, int num_sms,
+                                  cudaStream_t st) {
+  if ((ld * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0) return cudaErrorInvalidValue;
+  CUtensorMap tm;
+  if (!make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(C), uint64_t(R), uint64_t(ld) * 2, 64,
+                    128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  DualOut o{q_row, sf_row, row_zero, nrow_zero, slice_row, q_col, sf_col, col_zero, ncol_zero, slice_col};
+  const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ntiles = ((R + 127) / 128) * ((C + 127) / 128);
+  const int64_t cap = int64_t(num_sms) * 2;
+  k_iht_quant_dual<false><<<unsigned(ntiles < cap ? ntiles : cap), 256, smem, st>>>(tm, R, C, o);
+  return cudaGetLastError();
+}
+
 // Generic transposing variant for sources whose row pitch is not 16-byte aligned (TMA
 // cannot address them): one 64(k) x 256(r) tile per CTA through dynamic shared memory.
 template <typename T, bool kHad, bool kSwCvt>

@@ -295,3 +295,31 @@ def test_full_size_llama1b_sampled(path, strategy, pats):
             rows, cols = np.concatenate([rows, extra]), np.concatenate([cols, idx])
     ref = O.sampled_entries(np.ascontiguousarray(a_store), np.ascontiguousarray(b_store), strategy, rows, cols)
     assert rel_fro(got[rows, cols], ref) <= TOL_OUT
+
+
+# ======================================================================= layer step (dual quant)
+LAYER_STRATS = [("IHT", "IHT", "OE_RIGHT_IHT"), ("IHT", "OE_LEFT_IHT", "OE_LEFT_IHT"),
+                ("OE_LEFT_IHT", "OE_RIGHT_IHT", "OE_RIGHT_IHT"), ("OE_RIGHT_IHT", "IHT", "BF16"),
+                ("BF16", "BF16", "IHT")]
+
+
+@pytest.mark.parametrize("shape", [(640, 384, 256), (544, 352, 224)])
+@pytest.mark.parametrize("strats", LAYER_STRATS)
+def test_linear_layer_matches_paths_and_oracle(strats, shape):
+    T, d_in, d_out = shape
+    x, _ = synth.operand(T, d_in, "C", "X", case_id=401)
+    w, _ = synth.operand(d_out, d_in, "N", "W", case_id=402)
+    gy, _ = synth.operand(T, d_out, "R", "GY", case_id=403)
+    p = ah.Params(oe_k=16)
+    xd, wd, gd = dev_bf16(x), dev_bf16(w), dev_bf16(gy)
+    y, gx, gw = ah.linear_layer(xd, wd, gd, strats, p, out_dtype=torch.float32)
+    # identical (bitwise) to the three per-path calls: same quantiser arithmetic, one read
+    y1 = ah.linear_fwd(xd, wd, strats[0], p, out_dtype=torch.float32)
+    gx1 = ah.linear_dgrad(gd, wd, strats[1], p, out_dtype=torch.float32)
+    gw1 = ah.linear_wgrad(gd, xd, strats[2], p, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    for a, b in ((y, y1), (gx, gx1), (gw, gw1)):
+        np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+    for path, got, s in (("fwd", y, strats[0]), ("dgrad", gx, strats[1]), ("wgrad", gw, strats[2])):
+        ref = O.linear(path, s, x=x, w=w, gy=gy, k=16)
+        assert rel_fro(got.cpu().numpy(), ref) <= TOL_OUT, (path, s)
