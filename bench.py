@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64, help="oracle sample rows/cols per GEMM")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
+    ap.add_argument("--per-path", action="store_true",
+                    help="three adahop_linear_* calls per linear instead of one adahop_linear_layer call")
     return ap.parse_args()
 
 
@@ -237,6 +239,7 @@ def make_host_inputs(model, pats, tokens):
 
 def config_dict(args, world):
     return {"workload": f"{args.workload}_layer_21gemm (7 linears x fwd/dgrad/wgrad)",
+            "api": "adahop_linear_* per path" if args.per_path else "adahop_linear_layer (dual-orientation quant)",
             "tokens_per_gpu": args.tokens, "global_tokens": args.tokens * world,
             "pairs": "CN NN RN RC NC CC (Table-1 census classes)", "oe_k": args.oe_k,
             "level": args.level, "hadamard_block": 32, "out_dtype": "bf16",
@@ -290,20 +293,31 @@ def main():
                          y=torch.empty(T, d_out, dtype=torch.bfloat16, device=dev),
                          gx=torch.empty(T, d_in, dtype=torch.bfloat16, device=dev),
                          gw=torch.empty(d_out, d_in, dtype=torch.bfloat16, device=dev))
-    ws_bytes = max(ah.workspace_bytes(g["path"], T, g["d_in"], g["d_out"], g["strategy"], params) for g in gemms)
+    strat3 = {name: tuple(g["strategy"] for g in gemms if g["linear"] == name) for name, _, _ in model["linears"]}
+    if args.per_path:
+        ws_bytes = max(ah.workspace_bytes(g["path"], T, g["d_in"], g["d_out"], g["strategy"], params) for g in gemms)
+    else:
+        ws_bytes = max(ah.layer_workspace_bytes(T, d_in, d_out, strat3[name], params)
+                       for name, d_in, d_out in model["linears"])
     ws = ah.Workspace(ws_bytes, dev)
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     launches = [0]
+    units = gemms if args.per_path else [dict(linear=name) for name, _, _ in model["linears"]]
 
     def step_adahop(stage_events=None):
         n = 0
-        for gi, g in enumerate(gemms):
+        for gi, g in enumerate(units):
             L = lin[g["linear"]]
             ctx = stage_events[gi] if stage_events is not None else None
             if ctx is not None:
                 ctx.__enter__()
-            if g["path"] == "fwd":
+            if not args.per_path:
+                ah.linear_layer(L["x"], L["w"], L["gy"], strat3[g["linear"]], params, out=(L["y"], L["gx"], L["gw"]),
+                                ws=ws)
+                if world > 1:
+                    ahd.allreduce_wgrad(L["gw"])     # token-sharded DP: sum the wgrad partials
+            elif g["path"] == "fwd":
                 ah.linear_fwd(L["x"], L["w"], g["strategy"], params, out=L["y"], ws=ws)
             elif g["path"] == "dgrad":
                 ah.linear_dgrad(L["gy"], L["w"], g["strategy"], params, out=L["gx"], ws=ws)
@@ -381,17 +395,17 @@ def main():
     flops_step = sum(g["flops"] for g in gemms)
 
     # ---- AdaHOP, device-resident inputs; per-stage events recorded by the library
-    stage_ev = [ah.StageEvents() for _ in gemms]
+    stage_ev = [ah.StageEvents() for _ in units]
     step_adahop(stage_ev)                                  # first call: kernel attributes
     torch.cuda.synchronize()
     launches[0] = 0
     step_adahop(stage_ev)
     launches_per_step = launches[0]
     run_ada = as_graph(lambda: step_adahop(stage_ev))
-    acc = [{n: 0.0 for n in ah.StageEvents.NAMES} for _ in gemms]
+    acc = [{n: 0.0 for n in ah.StageEvents.NAMES} for _ in units]
 
     def collect():
-        for gi in range(len(gemms)):
+        for gi in range(len(units)):
             for n, v in stage_ev[gi].times_ms().items():
                 acc[gi][n] += v / args.steps
 
@@ -401,12 +415,11 @@ def main():
 
     # per-stage breakdown (tab:latency analogue), summed over the step
     stage_tot = {n: 0.0 for n in ah.StageEvents.NAMES}
-    per_gemm = []
-    for gi, g in enumerate(gemms):
+    per_unit = []
+    for gi, g in enumerate(units):
         for n in acc[gi]:
             stage_tot[n] += acc[gi][n]
-        per_gemm.append(dict(linear=g["linear"], path=g["path"], pair=g["pair"], strategy=g["strategy"],
-                             M=g["M"], N=g["N"], K=g["K"], **{k: round(v, 4) for k, v in acc[gi].items()}))
+        per_unit.append(dict(g, **{k: round(v, 4) for k, v in acc[gi].items()}))
 
     # ---- cuBLAS BF16 baseline (same GEMMs, same flush protocol)
     ms_cub = None
@@ -438,7 +451,7 @@ def main():
     # ---- roofline of the dominant kernel
     peaks = load_peaks()
     dom = max(stage_tot, key=stage_tot.get)
-    roof = roofline(dom, gemms, stage_tot, peaks, T)
+    roof = roofline(dom, gemms, stage_tot, peaks, T, model, per_path=args.per_path)
 
     # ---- CPU oracle baseline (rank 0, bounded sample)
     cpu = None
@@ -468,12 +481,12 @@ def main():
         print(json.dumps(line), flush=True)
         with open(os.path.join(ROOT, "gpurun_out", "bench_per_gemm.json") if os.path.isdir(
                 os.path.join(ROOT, "gpurun_out")) else os.devnull, "w") as f:
-            json.dump(per_gemm, f, indent=1)
+            json.dump(per_unit, f, indent=1)
     if world > 1:
         dist.destroy_process_group()
 
 
-def roofline(dom, gemms, stage_tot, peaks, T):
+def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False):
     """Achieved = algorithmic work of the dominant stage per step / its measured time."""
     fp4_peak = peaks["bf16_sustained"] * 4.0            # nominal fp4/bf16 dense ratio 9/2.25
     if dom == "gemm_mxf4":
@@ -483,8 +496,15 @@ def roofline(dom, gemms, stage_tot, peaks, T):
                 "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak, "traffic": None,
                 "peak_src": f"{peaks['src']} bf16 sustained x 4 (nominal fp4/bf16)"}
     if dom == "quant":
-        # 2 B in + 0.5 B codes + 1/32 B scale per element of both operands
-        by = sum((g["M"] + g["N"]) * g["K"] * (2 + 0.5 + 1 / 32) for g in gemms if g["strategy"] != "BF16")
+        if per_path:
+            # 2 B in + 0.5 B codes + 1/32 B scale per element of both operands of every GEMM
+            by = sum((g["M"] + g["N"]) * g["K"] * (2 + 0.5 + 1 / 32) for g in gemms if g["strategy"] != "BF16")
+        else:
+            # layer step: every tensor read once (2 B) and written in both FP4 layouts
+            by = 0.0
+            for _, d_in, d_out in model["linears"]:
+                for n_el in (T * d_in, d_out * d_in, T * d_out):
+                    by += n_el * (2 + 2 * (0.5 + 1 / 32))
         ach = by / (stage_tot[dom] * 1e-3) / 1e9
         return {"kernel": "k_iht_quant_row/col", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_src": peaks["src"]}
