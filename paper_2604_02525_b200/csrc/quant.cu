@@ -8,6 +8,7 @@
 #include "kernels.h"
 #include "ptx.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace adahop {
 
@@ -108,12 +109,22 @@ __device__ __forceinline__ void iht_quant_pair(uint64_t (&P)[32], uint4& codes0,
       }
     }
   }
-  float m0 = 0.f, m1 = 0.f;
+  // block amax as a depth-5 tree (a serial max chain would stall the warp ~128 cycles)
+  float t0[16], t1[16];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    m0 = fmaxf(m0, fabsf(f2_lo(P[i])));
-    m1 = fmaxf(m1, fabsf(f2_hi(P[i])));
+  for (int i = 0; i < 16; ++i) {
+    t0[i] = fmaxf(fabsf(f2_lo(P[i])), fabsf(f2_lo(P[i + 16])));
+    t1[i] = fmaxf(fabsf(f2_hi(P[i])), fabsf(f2_hi(P[i + 16])));
   }
+#pragma unroll
+  for (int wdt = 8; wdt >= 1; wdt >>= 1) {
+#pragma unroll
+    for (int i = 0; i < wdt; ++i) {
+      t0[i] = fmaxf(t0[i], t0[i + wdt]);
+      t1[i] = fmaxf(t1[i], t1[i + wdt]);
+    }
+  }
+  const float m0 = t0[0], m1 = t1[0];
   const int e0 = mx_exponent(m0), e1 = mx_exponent(m1);
   s0 = uint32_t(e0 + 127);
   s1 = uint32_t(e1 + 127);
@@ -426,8 +437,8 @@ struct DualOut {
   uint8_t* q_col; uint8_t* sf_col; const int32_t* col_zero; int ncol_zero; __nv_bfloat16* slice_col;
 };
 
-template <bool kSwCvt>
-__global__ void __launch_bounds__(256, 2) k_iht_quant_dual(const __grid_constant__ CUtensorMap tm, int64_t R,
+template <bool kSwCvt, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid_constant__ CUtensorMap tm, int64_t R,
                                                            int64_t C, const DualOut o) {
   constexpr int TR = 128, TC = 128, kBox = 16384;
   extern __shared__ __align__(1024) uint8_t smem_dual[];
@@ -584,16 +595,21 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
     return cudaErrorInvalidValue;
   DualOut o{q_row, sf_row, row_zero, nrow_zero, slice_row, q_col, sf_col, col_zero, ncol_zero, slice_col};
   const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64;
+  static const int occ = [] { const char* e = getenv("ADAHOP_DUAL_OCC"); return e ? atoi(e) : 2; }();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_iht_quant_dual<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int64_t ntiles = ((R + 127) / 128) * ((C + 127) / 128);
-  const int64_t cap = int64_t(num_sms) * 2;
-  k_iht_quant_dual<false><<<unsigned(ntiles < cap ? ntiles : cap), 256, smem, st>>>(tm, R, C, o);
+  const int64_t cap = int64_t(num_sms) * occ;
+  const unsigned grid = unsigned(ntiles < cap ? ntiles : cap);
+  if (occ == 1) k_iht_quant_dual<false, 1><<<grid, 256, smem, st>>>(tm, R, C, o);
+  else k_iht_quant_dual<false, 2><<<grid, 256, smem, st>>>(tm, R, C, o);
   return cudaGetLastError();
 }
 
