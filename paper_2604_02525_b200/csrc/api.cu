@@ -571,18 +571,21 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
       ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_row[t], 0, size_t(sf_bytes(R, C)), cs));
     if (L.need_col[t] && ((C % 128) || (R % 256)))
       ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
-    if (L.need_row[t] && L.need_col[t]) {
+    if (L.need_row[t] && L.need_col[t] && dual_quant_supported(R, C, rz != nullptr, cz != nullptr)) {
       ADAHOP_LAUNCH(launch_iht_quant_dual(src[t], R, C, C, rz, L.kk_row[t], srow, w + L.q_row[t], w + L.sf_row[t],
                                           cz, L.kk_col[t], scol, w + L.q_col[t], w + L.sf_col[t], dev.sms, cs));
       launches += 1;
-    } else if (L.need_row[t]) {
-      ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], w + L.q_row[t], w + L.sf_row[t],
-                                     nullptr, srow, false, dev.sms, cs));
-      launches += 1;
-    } else if (L.need_col[t]) {
-      ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], w + L.q_col[t], w + L.sf_col[t],
-                                     nullptr, scol, false, dev.sms, cs));
-      launches += 1;
+    } else {
+      if (L.need_row[t]) {
+        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], w + L.q_row[t], w + L.sf_row[t],
+                                       nullptr, srow, false, dev.sms, cs));
+        launches += 1;
+      }
+      if (L.need_col[t]) {
+        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], w + L.q_col[t], w + L.sf_col[t],
+                                       nullptr, scol, false, dev.sms, cs));
+        launches += 1;
+      }
     }
   }
   stage_mark(2, cs);

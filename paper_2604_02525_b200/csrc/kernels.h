@@ -21,6 +21,7 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
                                   uint8_t* q_row, uint8_t* sf_row, const int32_t* col_zero, int ncol_zero,
                                   __nv_bfloat16* slice_col, uint8_t* q_col, uint8_t* sf_col, int num_sms,
                                   cudaStream_t st);
+bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask);
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
 // FOID: probe keys (keys[R], fp64) + single-CTA radix top-k -> idx_sorted[min(k,R)].

@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQStages * kQTileBytes);
+  SmemMask* mask = reinterpret_cast<SmemMask*>(full + kQStages);
   const int64_t rtiles = (R + TR - 1) / TR, ktiles = (K + TK - 1) / TK;
   const int64_t ntiles = rtiles * ktiles;
   const int tid = threadIdx.x;
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
     for (int i = 0; i < kQStages; ++i) ptx::mbar_init(&full[i], 1);
     ptx::fence_barrier_init();
   }
+  if (nzero > 0) mask_build(mask, zero_rows, nzero, R);
   __syncthreads();
   const int64_t first = blockIdx.x, stride = gridDim.x;
   auto issue = [&](int64_t tile, int st) {
@@ -383,8 +385,8 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
     const bool va = ra < R && kba * kBlk < K;
     const bool vb = rb < R && kbb * kBlk < K;
     if (nzero > 0) {
-      const int sa = va ? find_sorted(zero_rows, nzero, ra) : -1;
-      const int sb = vb ? (kCol ? find_sorted(zero_rows, nzero, rb) : sa) : -1;
+      const int sa = va ? mask_slot(mask, nzero, ra) : -1;
+      const int sb = vb ? (kCol ? mask_slot(mask, nzero, rb) : sa) : -1;
       if (sa >= 0 || sb >= 0) {
         float x[32];
         if (sa >= 0 && slice) {
@@ -420,6 +422,44 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
   }
 }
 
+
+// ------------------------------------------------------------------------------------
+// OE masks in shared memory: a bitmap over the stored rows for the O(1) "is this row
+// extracted" test every thread makes per tile, plus a copy of the sorted index list for
+// the (rare) slot lookup of an extracted row. Built once per CTA.
+// ------------------------------------------------------------------------------------
+constexpr int kMaskMaxRows = 32768;                 // bitmap capacity per mask
+constexpr int kMaskWords = kMaskMaxRows / 32;
+constexpr int kMaskMaxK = 256;
+
+struct SmemMask {
+  uint32_t bits[kMaskWords];
+  int32_t idx[kMaskMaxK];
+};
+
+__device__ __forceinline__ void mask_build(SmemMask* m, const int32_t* __restrict__ idx, int n, int64_t rows) {
+  const int words = int((rows + 31) / 32);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) m->bits[i] = 0u;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = idx[i];
+    atomicOr(&m->bits[r >> 5], 1u << (r & 31));
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ int mask_slot(const SmemMask* m, int n, int64_t r) {
+  if (!((m->bits[r >> 5] >> (r & 31)) & 1u)) return -1;
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int x = m->idx[mid];
+    if (x == r) return mid;
+    if (x < r) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
 // ------------------------------------------------------------------------------------
 // Dual-orientation IHT + MXFP4 quantisation: ONE pass over a bf16 tensor T [R x C] emits
 //   the row quantisation   (stored rows = the R rows,    K = C) -> q_row, sf_row
@@ -447,12 +487,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
   const int64_t rtiles = (R + TR - 1) / TR, ctiles = (C + TC - 1) / TC;
   const int64_t ntiles = rtiles * ctiles;
   const int64_t kch_row = sf_kchunks(C), kch_col = sf_kchunks(R);
+  SmemMask* mrow = reinterpret_cast<SmemMask*>(full + kQStages);
+  SmemMask* mcol = mrow + 1;
   const int tid = threadIdx.x;
   if (tid == 0) {
     ptx::prefetch_tmap(&tm);
     for (int i = 0; i < kQStages; ++i) ptx::mbar_init(&full[i], 1);
     ptx::fence_barrier_init();
   }
+  if (o.nrow_zero > 0) mask_build(mrow, o.row_zero, o.nrow_zero, R);
+  if (o.ncol_zero > 0) mask_build(mcol, o.col_zero, o.ncol_zero, C);
   __syncthreads();
   const int64_t first = blockIdx.x, stride = gridDim.x;
   auto issue = [&](int64_t tile, int st) {
@@ -500,7 +544,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
       const int64_t kb0 = (ct * TC + bx * 64) / kBlk;
       const bool va = r < R && kb0 * kBlk < C, vb = r < R && (kb0 + 1) * kBlk < C;
       if (o.nrow_zero > 0 && va) {
-        const int s = find_sorted(o.row_zero, o.nrow_zero, r);
+        const int s = mask_slot(mrow, o.nrow_zero, r);
         if (s >= 0) {
           float x[32];
           if (o.slice_row) {
@@ -549,8 +593,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
       const int64_t kb = (rt * TR) / kBlk + rb;
       const bool va = ca < C && kb * kBlk < R, vb = cb2 < C && kb * kBlk < R;
       if (o.ncol_zero > 0) {
-        const int sa = va ? find_sorted(o.col_zero, o.ncol_zero, ca) : -1;
-        const int sb = vb ? find_sorted(o.col_zero, o.ncol_zero, cb2) : -1;
+        const int sa = va ? mask_slot(mcol, o.ncol_zero, ca) : -1;
+        const int sb = vb ? mask_slot(mcol, o.ncol_zero, cb2) : -1;
         if (sa >= 0 || sb >= 0) {
           float x[32];
           if (sa >= 0 && o.slice_col) {
@@ -594,14 +638,16 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
                     128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   DualOut o{q_row, sf_row, row_zero, nrow_zero, slice_row, q_col, sf_col, col_zero, ncol_zero, slice_col};
-  const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64;
+  const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64 +
+                      ((nrow_zero > 0 || ncol_zero > 0) ? 2 * sizeof(SmemMask) : 0);
+  if ((nrow_zero > 0 && R > kMaskMaxRows) || (ncol_zero > 0 && C > kMaskMaxRows)) return cudaErrorInvalidValue;
   static const int occ = [] { const char* e = getenv("ADAHOP_DUAL_OCC"); return e ? atoi(e) : 2; }();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+    const int mx = int(size_t(kQStages) * kQTileBytes + 1024 + 64 + 2 * sizeof(SmemMask));
+    cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_iht_quant_dual<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      e = cudaFuncSetAttribute(k_iht_quant_dual<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -684,7 +730,8 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
                                   const int32_t* zero_rows, int nzero, uint8_t* codes, uint8_t* sf,
                                   float* had_out, __nv_bfloat16* slice, int num_sms, cudaStream_t st) {
   const int64_t kch = sf_kchunks(K);
-  const bool tma_ok = sizeof(T) == 2 && (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const bool tma_ok = sizeof(T) == 2 && (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                      (nzero == 0 || R <= kMaskMaxRows);
   if (tma_ok) {
     CUtensorMap tm;
     bool ok;
@@ -698,13 +745,14 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
                         64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
       ntiles = ((R + 255) / 256) * ((K + 63) / 64);
     }
-    if (!ok) return cudaErrorInvalidValue;
-    const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64;
+    if (!ok || R > kMaskMaxRows) return cudaErrorInvalidValue;
+    const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64 + (nzero > 0 ? sizeof(SmemMask) : 0);
     static bool attr[2] = {false, false};
     if (!attr[kstrided]) {
+      const int mx = int(size_t(kQStages) * kQTileBytes + 1024 + 64 + sizeof(SmemMask));
       cudaError_t e = kstrided
-          ? cudaFuncSetAttribute(k_iht_quant_tma<true, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))
-          : cudaFuncSetAttribute(k_iht_quant_tma<false, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+          ? cudaFuncSetAttribute(k_iht_quant_tma<true, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)
+          : cudaFuncSetAttribute(k_iht_quant_tma<false, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
       if (e != cudaSuccess) return e;
       attr[kstrided] = true;
     }
@@ -1068,6 +1116,10 @@ cudaError_t launch_foid_keys_only(const void* in, bool in_f32, int64_t R, int64_
   if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
   else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
   return cudaGetLastError();
+}
+
+bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask) {
+  return (!row_mask || R <= kMaskMaxRows) && (!col_mask || C <= kMaskMaxRows);
 }
 
 int foid_launches(int64_t R, int64_t K, int probe) {
