@@ -299,6 +299,44 @@ __global__ void __launch_bounds__(256) k_iht_quant_row(const T* __restrict__ in,
   }
 }
 
+// ------------------------------------------------------------------------------------
+// OE masks in shared memory: a bitmap over the stored rows for the O(1) "is this row
+// extracted" test every thread makes per tile, plus a copy of the sorted index list for
+// the (rare) slot lookup of an extracted row. Built once per CTA.
+// ------------------------------------------------------------------------------------
+constexpr int kMaskMaxRows = 32768;                 // bitmap capacity per mask
+constexpr int kMaskWords = kMaskMaxRows / 32;
+constexpr int kMaskMaxK = 256;
+
+struct SmemMask {
+  uint32_t bits[kMaskWords];
+  int32_t idx[kMaskMaxK];
+};
+
+__device__ __forceinline__ void mask_build(SmemMask* m, const int32_t* __restrict__ idx, int n, int64_t rows) {
+  const int words = int((rows + 31) / 32);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) m->bits[i] = 0u;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = idx[i];
+    atomicOr(&m->bits[r >> 5], 1u << (r & 31));
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ int mask_slot(const SmemMask* m, int n, int64_t r) {
+  if (!((m->bits[r >> 5] >> (r & 31)) & 1u)) return -1;
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int x = m->idx[mid];
+    if (x == r) return mid;
+    if (x < r) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+
 // TMA-ring variant for bf16 sources with 16-byte aligned pitch (the production path).
 // Persistent CTAs (one per SM, 256 threads) walk 32-KB tiles that a kStages-deep TMA ring
 // keeps in flight; each thread quantises two 32-blocks per tile with fp32x2 arithmetic.
@@ -422,43 +460,6 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
   }
 }
 
-
-// ------------------------------------------------------------------------------------
-// OE masks in shared memory: a bitmap over the stored rows for the O(1) "is this row
-// extracted" test every thread makes per tile, plus a copy of the sorted index list for
-// the (rare) slot lookup of an extracted row. Built once per CTA.
-// ------------------------------------------------------------------------------------
-constexpr int kMaskMaxRows = 32768;                 // bitmap capacity per mask
-constexpr int kMaskWords = kMaskMaxRows / 32;
-constexpr int kMaskMaxK = 256;
-
-struct SmemMask {
-  uint32_t bits[kMaskWords];
-  int32_t idx[kMaskMaxK];
-};
-
-__device__ __forceinline__ void mask_build(SmemMask* m, const int32_t* __restrict__ idx, int n, int64_t rows) {
-  const int words = int((rows + 31) / 32);
-  for (int i = threadIdx.x; i < words; i += blockDim.x) m->bits[i] = 0u;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = idx[i];
-    atomicOr(&m->bits[r >> 5], 1u << (r & 31));
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ int mask_slot(const SmemMask* m, int n, int64_t r) {
-  if (!((m->bits[r >> 5] >> (r & 31)) & 1u)) return -1;
-  int lo = 0, hi = n - 1;
-  while (lo <= hi) {
-    const int mid = (lo + hi) >> 1;
-    const int x = m->idx[mid];
-    if (x == r) return mid;
-    if (x < r) lo = mid + 1; else hi = mid - 1;
-  }
-  return -1;
-}
 
 // ------------------------------------------------------------------------------------
 // Dual-orientation IHT + MXFP4 quantisation: ONE pass over a bf16 tensor T [R x C] emits
