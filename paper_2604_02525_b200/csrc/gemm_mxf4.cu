@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint8_t* __restrict__ sfa, const uint8_t* __restrict__ sfb, void* C,
                 int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* epi_smem = smem + size_t(kStages) * kStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* full = bars;

@@ -67,9 +67,8 @@ __device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
   return d;
 }
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
-  uint64_t d;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
-  return d;
+  // plain integer composition: the register allocator places lo/hi in the pair directly
+  return (uint64_t(__float_as_uint(hi)) << 32) | uint64_t(__float_as_uint(lo));
 }
 __device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(uint32_t(v)); }
 __device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
@@ -357,7 +356,7 @@ __global__ void __launch_bounds__(256, 2) k_iht_quant_tma(const __grid_constant_
   // row: TR = 256 rows, TK = 64; col: TR = 128 rows, TK = 128
   constexpr int TR = kCol ? 128 : 256, TK = kCol ? 128 : 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQStages * kQTileBytes);
   SmemMask* mask = reinterpret_cast<SmemMask*>(full + kQStages);
   const int64_t rtiles = (R + TR - 1) / TR, ktiles = (K + TK - 1) / TK;
@@ -483,7 +482,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
                                                            int64_t C, const DualOut o) {
   constexpr int TR = 128, TC = 128, kBox = 16384;
   extern __shared__ __align__(1024) uint8_t smem_dual[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dual) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem_dual + ((1024u - (ptx::smem_u32(smem_dual) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kQStages * kQTileBytes);
   const int64_t rtiles = (R + TR - 1) / TR, ctiles = (C + TC - 1) / TC;
   const int64_t ntiles = rtiles * ctiles;
@@ -518,48 +517,44 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
     const int64_t rt = tile % rtiles, ct = tile / rtiles;
     const uint8_t* tb = ring + st * kQTileBytes;
     // row part: row rr, the 64 columns of box bx; column part: columns 2cp, 2cp+1, rows
-    // rb*32 .. +32 (both read straight from the swizzled stage, one after the other to keep
-    // the register footprint at one 64-value pair)
+    // rb*32 .. +32. Values are read straight from the swizzled stage into the fp32x2 pairs;
+    // the (rare) OE rows/columns copy their raw values to the slice from the stage as well,
+    // so no raw copy stays live in registers.
     const int rr = tid & 127, bx = tid >> 7;
     const int cp = tid & 63, rb = tid >> 6;
+    const uint8_t* rowp = tb + bx * kBox + rr * 128;
+    const int sw = rr & 7;
     uint64_t P[32];
-    {
-      const uint8_t* row = tb + bx * kBox + rr * 128;
-      const int sw = rr & 7;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 ua = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
-        const uint4 ub = *reinterpret_cast<const uint4*>(row + (((j + 4) ^ sw) << 4));
-        const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w};
-        const uint32_t wb[4] = {ub.x, ub.y, ub.z, ub.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          P[8 * j + 2 * t] = f2_pack(bf16lo(wa[t]), bf16lo(wb[t]));
-          P[8 * j + 2 * t + 1] = f2_pack(bf16hi(wa[t]), bf16hi(wb[t]));
-        }
-      }
-    }
     // ---- row quantisation: stored row r0 + rr, K-blocks kb0, kb0 + 1 along C
     {
       const int64_t r = rt * TR + rr;
       const int64_t kb0 = (ct * TC + bx * 64) / kBlk;
       const bool va = r < R && kb0 * kBlk < C, vb = r < R && (kb0 + 1) * kBlk < C;
-      if (o.nrow_zero > 0 && va) {
-        const int s = mask_slot(mrow, o.nrow_zero, r);
-        if (s >= 0) {
-          float x[32];
-          if (o.slice_row) {
+      const int s = (o.nrow_zero > 0 && va) ? mask_slot(mrow, o.nrow_zero, r) : -1;
+      if (s >= 0) {
+        if (o.slice_row) {
+          // raw bf16 row segment -> slice (two 64-byte halves, un-swizzled)
+          __nv_bfloat16* dst = o.slice_row + int64_t(s) * C + kb0 * kBlk;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
-            store_slice32(o.slice_row + int64_t(s) * C + kb0 * kBlk, x);
-            if (vb) {
+          for (int j = 0; j < 8; ++j)
+            if (j < 4 || vb)
+              reinterpret_cast<uint4*>(dst)[j] = *reinterpret_cast<const uint4*>(rowp + ((j ^ sw) << 4));
+        }
 #pragma unroll
-              for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
-              store_slice32(o.slice_row + int64_t(s) * C + (kb0 + 1) * kBlk, x);
-            }
-          }
+        for (int i = 0; i < 32; ++i) P[i] = 0ull;
+      } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) P[i] = 0ull;
+        for (int j = 0; j < 4; ++j) {
+          const uint4 ua = *reinterpret_cast<const uint4*>(rowp + ((j ^ sw) << 4));
+          const uint4 ub = *reinterpret_cast<const uint4*>(rowp + (((j + 4) ^ sw) << 4));
+          P[8 * j + 0] = f2_pack(bf16lo(ua.x), bf16lo(ub.x));
+          P[8 * j + 1] = f2_pack(bf16hi(ua.x), bf16hi(ub.x));
+          P[8 * j + 2] = f2_pack(bf16lo(ua.y), bf16lo(ub.y));
+          P[8 * j + 3] = f2_pack(bf16hi(ua.y), bf16hi(ub.y));
+          P[8 * j + 4] = f2_pack(bf16lo(ua.z), bf16lo(ub.z));
+          P[8 * j + 5] = f2_pack(bf16hi(ua.z), bf16hi(ub.z));
+          P[8 * j + 6] = f2_pack(bf16lo(ua.w), bf16lo(ub.w));
+          P[8 * j + 7] = f2_pack(bf16hi(ua.w), bf16hi(ub.w));
         }
       }
       uint4 c0, c1;
@@ -575,54 +570,51 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
         o.sf_row[sf_offset(r, kb0 + 1, kch_row)] = uint8_t(s1);
       }
     }
+    // ---- column quantisation: stored rows c0 + 2cp, +1; K-block rb along R
+    const int64_t ca = ct * TC + 2 * cp, cb2 = ca + 1;
+    const int64_t kbc = (rt * TR) / kBlk + rb;
+    const bool cva = ca < C && kbc * kBlk < R, cvb = cb2 < C && kbc * kBlk < R;
     {
-      const int cb = (2 * cp) >> 6, cc = (2 * cp) & 63;   // box, column within box
-      const uint8_t* box = tb + cb * kBox;
+      const int ccol = (2 * cp) & 63;
+      const uint8_t* box = tb + ((2 * cp) >> 6) * kBox + rb * 32 * 128 + ((ccol * 2) & 15);
+      const int chunk = (ccol * 2) >> 4;
+      const int sa = (o.ncol_zero > 0 && cva) ? mask_slot(mcol, o.ncol_zero, ca) : -1;
+      const int sb = (o.ncol_zero > 0 && cvb) ? mask_slot(mcol, o.ncol_zero, cb2) : -1;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int r = rb * 32 + i;
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(
-            box + r * 128 + ((((cc * 2) >> 4) ^ (r & 7)) << 4) + ((cc * 2) & 15));
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(box + i * 128 + ((chunk ^ (i & 7)) << 4));
         P[i] = f2_pack(bf16lo(w), bf16hi(w));
+      }
+      if (sa >= 0 || sb >= 0) {
+        float x[32];
+        if (sa >= 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
+          if (o.slice_col) store_slice32(o.slice_col + int64_t(sa) * R + kbc * kBlk, x);
+        }
+        if (sb >= 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
+          if (o.slice_col) store_slice32(o.slice_col + int64_t(sb) * R + kbc * kBlk, x);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) P[i] = f2_pack(sa >= 0 ? 0.f : f2_lo(P[i]), sb >= 0 ? 0.f : f2_hi(P[i]));
       }
     }
     __syncthreads();                                   // stage consumed by every thread
     if (tid == 0 && tile + kQStages * stride < ntiles) issue(tile + kQStages * stride, st);
-    // ---- column quantisation: stored rows c0 + 2cp, +1; K-block along R
     {
-      const int64_t ca = ct * TC + 2 * cp, cb2 = ca + 1;
-      const int64_t kb = (rt * TR) / kBlk + rb;
-      const bool va = ca < C && kb * kBlk < R, vb = cb2 < C && kb * kBlk < R;
-      if (o.ncol_zero > 0) {
-        const int sa = va ? mask_slot(mcol, o.ncol_zero, ca) : -1;
-        const int sb = vb ? mask_slot(mcol, o.ncol_zero, cb2) : -1;
-        if (sa >= 0 || sb >= 0) {
-          float x[32];
-          if (sa >= 0 && o.slice_col) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = f2_lo(P[i]);
-            store_slice32(o.slice_col + int64_t(sa) * R + kb * kBlk, x);
-          }
-          if (sb >= 0 && o.slice_col) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = f2_hi(P[i]);
-            store_slice32(o.slice_col + int64_t(sb) * R + kb * kBlk, x);
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) P[i] = f2_pack(sa >= 0 ? 0.f : f2_lo(P[i]), sb >= 0 ? 0.f : f2_hi(P[i]));
-        }
-      }
       uint4 c0, c1;
       uint32_t s0, s1;
       float ydummy[1];
       iht_quant_pair<false, kSwCvt>(P, c0, c1, s0, s1, ydummy, ydummy);
-      if (va) {
-        *reinterpret_cast<uint4*>(o.q_col + ca * (R / 2) + kb * 16) = c0;
-        o.sf_col[sf_offset(ca, kb, kch_col)] = uint8_t(s0);
+      if (cva) {
+        *reinterpret_cast<uint4*>(o.q_col + ca * (R / 2) + kbc * 16) = c0;
+        o.sf_col[sf_offset(ca, kbc, kch_col)] = uint8_t(s0);
       }
-      if (vb) {
-        *reinterpret_cast<uint4*>(o.q_col + cb2 * (R / 2) + kb * 16) = c1;
-        o.sf_col[sf_offset(cb2, kb, kch_col)] = uint8_t(s1);
+      if (cvb) {
+        *reinterpret_cast<uint4*>(o.q_col + cb2 * (R / 2) + kbc * 16) = c1;
+        o.sf_col[sf_offset(cb2, kbc, kch_col)] = uint8_t(s1);
       }
     }
   }
