@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads)
 
 // Deterministic split-K fold + scatter into C, through a 32 x 32 smem tile so that both
 // the partial reads (along j) and the OE-Left row writes (along m) are coalesced.
-__global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict__ part, int splits,
+__global__ void __launch_bounds__(1024) k_outlier_reduce(const float* __restrict__ part, int splits,
                                                         int64_t Mb, int64_t npad, int k,
                                                         const int32_t* __restrict__ idx,
                                                         int scatter_cols, void* C, int out_f32,
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict_
   const int64_t m0 = int64_t(blockIdx.x) * 32;
   const int j0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int mm = ty; mm < 32; mm += 8) {
+  for (int mm = ty; mm < 32; mm += blockDim.y) {
     const int64_t m = m0 + mm;
     const int j = j0 + tx;
     float v = 0.f;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict_
   }
   __syncthreads();
   if (scatter_cols) {  // OE-Right: C[m][idx[j]]
-    for (int mm = ty; mm < 32; mm += 8) {
+    for (int mm = ty; mm < 32; mm += blockDim.y) {
       const int64_t m = m0 + mm;
       const int j = j0 + tx;
       if (m >= Mb || j >= k) continue;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) k_outlier_reduce(const float* __restrict_
       else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(tile[mm][tx]);
     }
   } else {             // OE-Left (transposed product): C[idx[j]][m]
-    for (int jj = ty; jj < 32; jj += 8) {
+    for (int jj = ty; jj < 32; jj += blockDim.y) {
       const int j = j0 + jj;
       const int64_t m = m0 + tx;
       if (m >= Mb || j >= k) continue;
@@ -324,7 +324,7 @@ cudaError_t launch_outlier_reduce(const float* part, int splits, int64_t Mb, int
                                   const int32_t* idx, bool scatter_cols, void* C, bool out_f32,
                                   int64_t ldc, cudaStream_t st) {
   dim3 grid(unsigned((Mb + 31) / 32), unsigned((k + 31) / 32));
-  bf16g::k_outlier_reduce<<<grid, dim3(32, 8), 0, st>>>(part, splits, Mb, npad, k, idx, scatter_cols ? 1 : 0,
+  bf16g::k_outlier_reduce<<<grid, dim3(32, 32), 0, st>>>(part, splits, Mb, npad, k, idx, scatter_cols ? 1 : 0,
                                                 C, out_f32 ? 1 : 0, ldc);
   return cudaGetLastError();
 }
