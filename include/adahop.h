@@ -203,6 +203,20 @@ adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_
                                        adahop_stream_t stream);
 size_t adahop_debug_workspace_bytes(int64_t R, int64_t K);
 
+/* One-pass dual-orientation IHT + quantisation of a bf16 tensor T [R x C] (pitch ld elements):
+ * the row operand (stored rows = R, K = C: q_row [R x C/2], scales_row [R x C/32]) and the
+ * column operand (stored rows = C, K = R: q_col [C x R/2], scales_col [C x R/32]) — the two
+ * layouts the three GEMMs of one linear need (eq:iht_fwd/dgrad/wgrad). row_zero /
+ * col_zero (sorted int32, device, <= 256 each) are the OE rows / columns: masked to zero blocks
+ * and copied raw to slice_row [nrow_zero x C] / slice_col [ncol_zero x R] bf16 (nullable).
+ * Canonical code / scale layouts as adahop_debug_iht_quant. R, C multiples of 32.
+ * ws >= adahop_debug_workspace_bytes(R, C) + adahop_debug_workspace_bytes(C, R). */
+adahop_status_t adahop_debug_quant_dual(const void* in, adahop_dtype_t dt, int64_t R, int64_t C, int64_t ld,
+                                       const int32_t* row_zero, int32_t nrow_zero, const int32_t* col_zero,
+                                       int32_t ncol_zero, uint8_t* q_row, uint8_t* scales_row, uint8_t* q_col,
+                                       uint8_t* scales_col, void* slice_row, void* slice_col, void* ws,
+                                       size_t ws_bytes, adahop_stream_t stream);
+
 /* FOID: idx_sorted[0..min(k,R)) = ascending indices of the top-k stored rows by
  * the fp64 probe variance (ties -> lower index); keys_out (nullable) = the R keys. */
 adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libadahop.so")
+# ADAHOP_LIB selects another in-tree build of the same ABI (kernel experiments)
+LIB_PATH = os.environ.get("ADAHOP_LIB") or os.path.join(_HERE, "libadahop.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -54,6 +55,7 @@ SIGNATURES = {
     "adahop_layer_workspace_bytes": (SZ, [I64, I64, I64, C.POINTER(I32), PP]),
     "adahop_linear_layer": (I32, [P, P, P, P, P, P, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P]),
     "adahop_debug_iht_quant": (I32, [P, I32, I64, I64, I64, I32, P, I32, P, P, P, P, SZ, P]),
+    "adahop_debug_quant_dual": (I32, [P, I32, I64, I64, I64, P, I32, P, I32, P, P, P, P, P, P, P, SZ, P]),
     "adahop_debug_workspace_bytes": (SZ, [I64, I64]),
     "adahop_debug_foid": (I32, [P, I32, I64, I64, I64, I32, I32, I32, P, P, P, SZ, P]),
     "adahop_debug_gemm_mxf4": (I32, [P, P, P, P, P, I32, I64, I64, I64, I64, P, SZ, P]),

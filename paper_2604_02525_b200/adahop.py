@@ -23,7 +23,7 @@ DT_BF16, DT_F32 = 0, 1
 __all__ = [
     "AdahopError", "Params", "IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT", "BF16", "STRATEGY", "strategy_for_pair",
     "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
-    "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant",
+    "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant", "debug_quant_dual",
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes",
 ]
@@ -227,6 +227,36 @@ def debug_iht_quant(x: torch.Tensor, k_strided: bool = False, zero_rows=None, wa
           lib.adahop_debug_iht_quant(_ptr(x), _dt(x), R, K, x.stride(0), int(k_strided), _ptr(zr), nz,
                                      _ptr(had), _ptr(codes), _ptr(scales), _ptr(w), n, _stream()))
     return codes, scales, had
+
+
+def debug_quant_dual(x: torch.Tensor, row_zero=None, col_zero=None, want_slices: bool = False):
+    """Dual-orientation IHT+quant of a bf16 [R x C] tensor in one pass: (row codes, row scales,
+    col codes, col scales[, row slice, col slice]), canonical layouts."""
+    R, C = x.shape
+    dev = x.device
+    qr = torch.empty((R, C // 2), dtype=torch.uint8, device=dev)
+    sr = torch.empty((R, C // 32), dtype=torch.uint8, device=dev)
+    qc = torch.empty((C, R // 2), dtype=torch.uint8, device=dev)
+    sc = torch.empty((C, R // 32), dtype=torch.uint8, device=dev)
+
+    def idx(z):
+        if z is None or len(z) == 0:
+            return None, 0
+        t = torch.as_tensor(z, dtype=torch.int32, device=dev).contiguous()
+        return t, t.numel()
+
+    rz, nr = idx(row_zero)
+    cz, nc = idx(col_zero)
+    slr = torch.zeros((nr, C), dtype=torch.bfloat16, device=dev) if want_slices and nr else None
+    slc = torch.zeros((nc, R), dtype=torch.bfloat16, device=dev) if want_slices and nc else None
+    n = lib.adahop_debug_workspace_bytes(R, C) + lib.adahop_debug_workspace_bytes(C, R)
+    w = torch.empty(n, dtype=torch.uint8, device=dev)
+    check("adahop_debug_quant_dual",
+          lib.adahop_debug_quant_dual(_ptr(x), _dt(x), R, C, x.stride(0), _ptr(rz), nr, _ptr(cz), nc, _ptr(qr),
+                                      _ptr(sr), _ptr(qc), _ptr(sc), _ptr(slr), _ptr(slc), _ptr(w), n, _stream()))
+    if want_slices:
+        return qr, sr, qc, sc, slr, slc
+    return qr, sr, qc, sc
 
 
 def debug_foid(x: torch.Tensor, k: int, probe: int = 64, k_strided: bool = False):

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libadahop.so")
-SOURCES = ["api.cu", "quant.cu", "gemm_mxf4.cu", "gemm_mxf4_2sm.cu", "gemm_bf16.cu"]
+SOURCES = ["api.cu", "quant.cu", "quant_tc.cu", "gemm_mxf4.cu", "gemm_mxf4_2sm.cu", "gemm_bf16.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,38 +34,43 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = LIB) -> str:
     if not force and not needs_build():
         return LIB
     objs = []
-    os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
+    bdir = os.path.join(PKG, "build" if out == LIB else "build_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in SOURCES:
-        obj = os.path.join(PKG, "build", src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-dc" if False else "-c",
+        obj = os.path.join(bdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-Xptxas", "-v" if verbose else "-O3", "-dc" if False else "-c",
                os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = False
     for src, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if verbose or p.returncode != 0:
-            sys.stderr.write(f"--- {src}\n{out}")
+            sys.stderr.write(f"--- {src}\n{log}")
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
     # the exported C ABI symbols are marked default-visible in api.cu via a version script
-    ver = os.path.join(PKG, "build", "exports.map")
+    ver = os.path.join(bdir, "exports.map")
     with open(ver, "w") as f:
         f.write("{ global: adahop_*; local: *; };\n")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-           *objs, "-o", LIB, "-Xlinker", f"--version-script={ver}", "-lpthread", "-ldl", "-lrt"]
+           *objs, "-o", out, "-Xlinker", f"--version-script={ver}", "-lpthread", "-ldl", "-lrt"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout)
         raise RuntimeError("link failed")
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force=True))
+    # --define NAME=VAL (repeatable) and --out PATH build an experiment variant of the library
+    args = sys.argv[1:]
+    defs = [args[i + 1] for i, a in enumerate(args) if a == "--define"]
+    out = next((args[i + 1] for i, a in enumerate(args) if a == "--out"), LIB)
+    print(build(verbose="--verbose" in args, force=True, defines=defs, out=os.path.abspath(out)))

@@ -719,6 +719,35 @@ adahop_status_t adahop_debug_iht_quant(const void* in, adahop_dtype_t dt, int64_
   return ADAHOP_OK;
 }
 
+adahop_status_t adahop_debug_quant_dual(const void* in, adahop_dtype_t dt, int64_t R, int64_t C, int64_t ld,
+                                       const int32_t* row_zero, int32_t nrow_zero, const int32_t* col_zero,
+                                       int32_t ncol_zero, uint8_t* q_row, uint8_t* scales_row, uint8_t* q_col,
+                                       uint8_t* scales_col, void* slice_row, void* slice_col, void* ws,
+                                       size_t ws_bytes, adahop_stream_t stream) {
+  if (!in || !q_row || !scales_row || !q_col || !scales_col || !ws) return ADAHOP_E_INVALID_ARG;
+  if (dt != ADAHOP_DT_BF16) return ADAHOP_E_UNSUPPORTED;
+  if (nrow_zero < 0 || ncol_zero < 0 || (nrow_zero > 0 && !row_zero) || (ncol_zero > 0 && !col_zero))
+    return ADAHOP_E_INVALID_ARG;
+  if (nrow_zero > 256 || ncol_zero > 256) return ADAHOP_E_UNSUPPORTED;
+  if (R <= 0 || C <= 0 || R % 32 || C % 32) return ADAHOP_E_SHAPE;
+  if (ld < C || (ld * 2) % 16 || !aligned16(in)) return ADAHOP_E_INVALID_ARG;
+  if (ws_bytes < adahop_debug_workspace_bytes(R, C) + adahop_debug_workspace_bytes(C, R)) return ADAHOP_E_WORKSPACE;
+  if (!dual_quant_supported(R, C, nrow_zero > 0, ncol_zero > 0)) return ADAHOP_E_UNSUPPORTED;
+  DevInfo dev;
+  adahop_status_t st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* sf_r = static_cast<uint8_t*>(ws);
+  uint8_t* sf_c = sf_r + adahop_debug_workspace_bytes(R, C);
+  ADAHOP_LAUNCH(launch_iht_quant_dual(static_cast<const __nv_bfloat16*>(in), R, C, ld, row_zero, nrow_zero,
+                                      static_cast<__nv_bfloat16*>(slice_row), q_row, sf_r, col_zero, ncol_zero,
+                                      static_cast<__nv_bfloat16*>(slice_col), q_col, sf_c, dev.sms, cs));
+  ADAHOP_LAUNCH(launch_sf_convert(sf_r, R, C, scales_row, true, cs));
+  ADAHOP_LAUNCH(launch_sf_convert(sf_c, C, R, scales_col, true, cs));
+  g_launches = 3;
+  return ADAHOP_OK;
+}
+
 adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, int64_t K,
                                   int64_t ld, int32_t k_strided, int32_t k, int32_t probe,
                                   int32_t* idx_sorted, double* keys_out, void* ws, size_t ws_bytes,

@@ -1,0 +1,509 @@
+// quant_tc.cu — IHT + MXFP4 quantisation with the Hadamard contraction on the tensor cores.
+//
+// The inner Hadamard transform is the dense contraction A·H_k of eq:inner_hadamard,
+// blockwise with H_32. The scalar butterfly version spends ~12 instructions per
+// element and is issue-bound well below HBM bandwidth; here each 32-block is multiplied by
+// the +-1 Sylvester matrix with tcgen05.mma.kind::f16 (bf16 inputs are exact, the +-x
+// products are exact, the 32-term sums accumulate in fp32), and the epilogue warps only
+// scale by RN32(1/sqrt 32), take the block amax, and convert to E2M1/E8M0.
+// Bit-exactness contract: codes and scales equal the OCP quantiser applied to the fp32
+// Hadamard output this kernel produces (SURVEY c19 protocol (a)); that output is within
+// 1e-6 relative of the exact transform (R2).
+//
+// One pass over a bf16 tensor T [R x C] can emit
+//   the row quantisation    (stored rows = the R rows,    K = C)  — kRow,
+//   the column quantisation (stored rows = the C columns, K = R)  — kCol,
+// each with its own OE mask (extracted rows / columns become zero blocks: codes 0, scale
+// 0x7F) and raw bf16 slice. Tiles of 128 x 128 arrive by TMA (two 128B-swizzled 64-column
+// boxes) in a 4-stage ring. Per tile the MMA warp issues, per 32-block, M=128 x N=32 x K=32:
+//   row blocks: A = the tile's 32-column slice, K-major;
+//   column blocks: A = the transposed 32-row slice, MN-major (the same smem bytes);
+// B = H_32 (K-major, in smem). Accumulators (double-buffered, 2 x 256 TMEM columns) are
+// drained by 8 epilogue warps: 4 for row blocks (TMEM lane = tile row), 4 for column blocks
+// (TMEM lane = tile column).
+#include "common.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+// Experiment knob (never set in the product build): bit 0 skips the MMAs, bit 1 the
+// epilogue TMEM loads + quantisation, bit 2 the code TMA stores, bit 3 the scale stores.
+#ifndef QTC_ABLATE
+#define QTC_ABLATE 0
+#endif
+
+// Experiment knob: QTC_TRACE=1 records per-tile timestamps of CTA 0 and prints them.
+#ifndef QTC_TRACE
+#define QTC_TRACE 0
+#endif
+#if QTC_TRACE
+#include <cstdio>
+__device__ long long g_qtc_trace[5][64];
+#define QTC_T(k, lt) do { if (blockIdx.x == 0 && (lt) < 64) g_qtc_trace[k][lt] = clock64(); } while (0)
+#else
+#define QTC_T(k, lt) do { } while (0)
+#endif
+
+namespace adahop {
+namespace qtc {
+
+constexpr int kStages = 4;
+constexpr int kBox = 16384;           // 128 rows x 128 bytes (64 bf16 columns)
+constexpr int kTile = 2 * kBox;       // 128 x 128 bf16
+constexpr int kEpiGroups = 4;         // epilogue groups of 4 warps (one warp per TMEM lane quarter)
+constexpr int kThreads = 128 + kEpiGroups * 128;   // warps 0..3 control, 4..19 epilogue
+constexpr int kHBytes = 32 * 32 * 2;  // H_32 in the canonical no-swizzle K-major layout
+constexpr int kStg = 128 * 64;        // one tile's codes of one orientation: 128 stored rows x 64 bytes
+
+constexpr int kMaskMaxRows = 32768;
+struct Mask {
+  uint32_t bits[kMaskMaxRows / 32];
+  int32_t idx[256];
+};
+__device__ __forceinline__ void mask_build(Mask* m, const int32_t* __restrict__ idx, int n, int64_t rows) {
+  const int words = int((rows + 31) / 32);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) m->bits[i] = 0u;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicOr(&m->bits[idx[i] >> 5], 1u << (idx[i] & 31));
+  __syncthreads();
+}
+__device__ __forceinline__ bool mask_hit(const Mask* m, int64_t r) { return (m->bits[r >> 5] >> (r & 31)) & 1u; }
+__device__ __forceinline__ int mask_slot(const Mask* m, int n, int64_t r) {
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int x = m->idx[mid];
+    if (x == r) return mid;
+    if (x < r) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+struct Out {
+  uint8_t* q; uint8_t* sf; const int32_t* zero; int nzero; __nv_bfloat16* slice; float* had;
+};
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, M = 128, N = 32, A major selectable.
+__host__ __device__ constexpr uint32_t idesc_h(int a_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(32 >> 3) << 17) |
+         (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ float inv_sqrt32() { return __uint_as_float(0x3E3504F3u); }
+
+__device__ __forceinline__ uint32_t e2m1x8(const float* v) {
+  uint32_t out;
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t}"
+      : "=r"(out)
+      : "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
+  return out;
+}
+
+// Quantise one 32-block from its unnormalised Hadamard sums d[32] (fp32 accumulator).
+// y = RN(d c); e = floor(log2 max|y|) - 2 (clamped, 0 for a zero block); codes = E2M1(y 2^-e).
+template <bool kHad>
+__device__ __forceinline__ void quant_block(const uint32_t (&d)[32], uint4& codes, uint32_t& sbyte, float* y_out) {
+  const float c = inv_sqrt32();
+  // max |d| as a depth-4 tree of 3-input maxima (FMNMX3) instead of a 32-long chain
+  float m[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    m[i] = fmaxf(fmaxf(fabsf(__uint_as_float(d[3 * i])), fabsf(__uint_as_float(d[3 * i + 1]))),
+                 fabsf(__uint_as_float(d[3 * i + 2])));
+  m[10] = fmaxf(fabsf(__uint_as_float(d[30])), fabsf(__uint_as_float(d[31])));
+  const float amax = fmaxf(fmaxf(fmaxf(fmaxf(m[0], m[1]), m[2]), fmaxf(fmaxf(m[3], m[4]), m[5])),
+                           fmaxf(fmaxf(fmaxf(m[6], m[7]), m[8]), fmaxf(m[9], m[10])));
+  const float amax_y = __fmul_rn(amax, c);
+  const uint32_t bits = __float_as_uint(amax_y);
+  int e;
+  if (amax_y == 0.f) e = 0;
+  else if ((bits >> 23) != 0) e = int(bits >> 23) - 127 - 2;
+  else e = (31 - __clz(int(bits))) - 149 - 2;
+  e = max(-127, min(127, e));
+  sbyte = uint32_t(e + 127);
+  float v[32];
+  if (kHad || e > 120 || e < -100) {
+    const float s = __uint_as_float(uint32_t(127 - e) << 23);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float y = __fmul_rn(__uint_as_float(d[i]), c);
+      if (kHad) y_out[i] = y;
+      v[i] = __fmul_rn(y, s);
+    }
+  } else {
+    // fused c * 2^-e (exact: no subnormal / overflow in this exponent range), packed FMUL2
+    const uint32_t cs = __float_as_uint(__fmul_rn(c, __uint_as_float(uint32_t(127 - e) << 23)));
+    const uint64_t cs2 = (uint64_t(cs) << 32) | cs;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      uint64_t p;
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"((uint64_t(d[i + 1]) << 32) | d[i]), "l"(cs2));
+      v[i] = __uint_as_float(uint32_t(p));
+      v[i + 1] = __uint_as_float(uint32_t(p >> 32));
+    }
+  }
+  codes = make_uint4(e2m1x8(v), e2m1x8(v + 8), e2m1x8(v + 16), e2m1x8(v + 24));
+}
+
+template <bool kRow, bool kCol, bool kHad>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_quant_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_qrow,
+               const __grid_constant__ CUtensorMap tm_qcol, int64_t R, int64_t C, const Out orow, const Out ocol) {
+  extern __shared__ __align__(1024) uint8_t smem_q[];
+  uint8_t* ring = smem_q + ((1024u - (ptx::smem_u32(smem_q) & 1023u)) & 1023u);
+  uint8_t* stg = ring + kStages * kTile;   // codes [orientation][buffer][128 rows x 64 B], 64B-swizzled
+  uint8_t* sfstg = stg + 4 * kStg;         // scales [orientation][buffer][512 B] = one SF chunk each
+  uint8_t* hmat = sfstg + 4 * 512;
+  uint64_t* full = reinterpret_cast<uint64_t*>(hmat + kHBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint64_t* staged = tempty + 2;       // [2] epilogue warps -> store warp
+  uint64_t* stgfree = staged + 2;      // [2] store warp -> epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stgfree + 2);
+  Mask* mrow = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+  Mask* mcol = mrow + 1;
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int rtiles = int((R + 127) / 128), ctiles = int((C + 127) / 128);
+  const int ntiles = rtiles * ctiles;
+  const int64_t kch_row = sf_kchunks(C), kch_col = sf_kchunks(R);
+  constexpr int kEpiWarps = kEpiGroups * 4;
+
+  // ---- setup: barriers, H_32, TMEM, OE masks
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm);
+    if (kRow) ptx::prefetch_tmap(&tm_qrow);
+    if (kCol) ptx::prefetch_tmap(&tm_qcol);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 2);   // MMA commit + slice-copy warp
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], kEpiWarps);
+      ptx::mbar_init(&staged[b], kEpiWarps);
+      ptx::mbar_init(&stgfree[b], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  // H (n = j rows, k = i): core matrices of 8 rows x 16 bytes, (n/8, k/8) -> ((n/8)*4 + k/8)*128
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int n = e >> 5, k = e & 31;
+    const bool neg = __popc(n & k) & 1;
+    *reinterpret_cast<__nv_bfloat16*>(hmat + ((n >> 3) * 4 + (k >> 3)) * 128 + (n & 7) * 16 + (k & 7) * 2) =
+        __float2bfloat16_rn(neg ? -1.f : 1.f);
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  if (kRow && orow.nzero > 0) mask_build(mrow, orow.zero, orow.nzero, R);
+  if (kCol && ocol.nzero > 0) mask_build(mcol, ocol.zero, ocol.nzero, C);
+  ptx::fence_proxy_async();  // H written by threads, read by the tensor core
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int first = blockIdx.x, stride = gridDim.x;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = first; tile < ntiles; tile += stride) {
+      const int rt = tile % rtiles, ct = tile / rtiles;
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      QTC_T(0, (tile - first) / stride);
+      uint8_t* dst = ring + stage * kTile;
+      ptx::mbar_arrive_expect_tx(&full[stage], kTile);
+      ptx::tma_load_2d(dst, &tm, &full[stage], int32_t(ct * 128), int32_t(rt * 128));
+      ptx::tma_load_2d(dst + kBox, &tm, &full[stage], int32_t(ct * 128 + 64), int32_t(rt * 128));
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane
+    // issues; descriptors stay warp-uniform so they live in uniform registers)
+    const uint64_t bdesc = ptx::make_sdesc(ptx::smem_u32(hmat), 128, 512, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int lt = 0;
+    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
+      const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
+      ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      QTC_T(1, lt);
+      ptx::mbar_wait(&full[stage], phase);
+      QTC_T(2, lt);
+      ptx::tc_fence_after();
+      const uint32_t base = ptx::smem_u32(ring + stage * kTile);
+      const uint32_t d0 = tmem_base + buf * 256;
+      // start-address field = bits [0,14) of the descriptor in 16-byte units: offsets add directly
+      const uint64_t arow = ptx::make_sdesc(base, 16, 1024, 2);     // K-major (row blocks)
+      const uint64_t acol = ptx::make_sdesc(base, kBox, 1024, 2);   // MN-major (column blocks)
+      if (ptx::elect_one()) {
+        if (!(QTC_ABLATE & 1)) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {   // K = 32 as two K = 16 steps
+              // row blocks: rows of the tile x columns [32 b + 16 s, +16): box b/2, byte 64 (b%2) + 32 s
+              if (kRow)
+                ptx::mma_bf16(d0 + b * 32, arow + uint64_t(((b >> 1) * kBox + (b & 1) * 64 + s * 32) >> 4),
+                              bdesc + uint64_t(s * 16), idesc_h(0), s);
+              // column blocks: columns of the tile x rows [32 b + 16 s, +16): MN-major, two 64-column atoms
+              if (kCol)
+                ptx::mma_bf16(d0 + 128 + b * 32, acol + uint64_t(((b * 32 + s * 16) * 128) >> 4),
+                              bdesc + uint64_t(s * 16), idesc_h(1), s);
+            }
+          }
+        }
+        ptx::tc_commit(&empty[stage]);
+        ptx::tc_commit(&tfull[buf]);
+      }
+      __syncwarp();
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ store warp
+    // One TMA store of the 128 x 64-byte code box and one 512-byte bulk copy of the scale chunk
+    // per orientation and tile, so the epilogue warps never stall on global-store issue.
+    int lt = 0;
+    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
+      const int rt = tile % rtiles, ct = tile / rtiles;
+      const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
+      ptx::mbar_wait(&staged[buf], use & 1);
+      if (ptx::elect_one()) {
+        ptx::fence_proxy_async();
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if ((o == 0 && !kRow) || (o == 1 && !kCol)) continue;
+          const bool cs = o == 1;
+          const int oi = kRow ? o : 0;   // staging slot of this orientation
+          const int64_t srow0 = cs ? int64_t(ct) * 128 : int64_t(rt) * 128;
+          const int kt = cs ? rt : ct;   // K-tile index: K-blocks [4 kt, 4 kt + 4)
+          if (!(QTC_ABLATE & 4))
+            ptx::tma_store_2d(cs ? &tm_qcol : &tm_qrow, stg + (oi * 2 + buf) * kStg, kt * 64, int32_t(srow0));
+          if (!(QTC_ABLATE & 8)) {
+            uint8_t* gsf = (cs ? ocol.sf : orow.sf) + ((srow0 >> 7) * (cs ? kch_col : kch_row) + kt) * 512;
+            ptx::bulk_store(gsf, sfstg + (oi * 2 + buf) * 512, 512);
+          }
+        }
+        ptx::bulk_commit_group();
+        ptx::bulk_wait_group_read<0>();
+        ptx::mbar_arrive(&stgfree[buf]);
+      }
+      __syncwarp();
+    }
+    if (ptx::elect_one()) ptx::bulk_wait_group<0>();
+    __syncwarp();
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ OE slice copies
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = first; tile < ntiles; tile += stride) {
+      const int rt = tile % rtiles, ct = tile / rtiles;
+      ptx::mbar_wait(&full[stage], phase);
+      const uint8_t* tb = ring + stage * kTile;
+      if (kRow && orow.nzero > 0 && orow.slice) {
+        // extracted rows of this tile: 128 raw values each -> slice_row[slot][c0 ..]
+        for (int r0 = 0; r0 < 128; r0 += 32) {
+          uint32_t hits = __ballot_sync(~0u, rt * 128 + r0 + lane < R && mask_hit(mrow, rt * 128 + r0 + lane));
+          while (hits) {
+          const int rr = r0 + __ffs(hits) - 1;
+          hits &= hits - 1;
+          const int64_t r = rt * 128 + rr;
+          const int slot = mask_slot(mrow, orow.nzero, r);
+          // lane l copies 16-byte chunk (l & 7) of box (l >> 3) [16 chunks per row]
+          if (lane < 16) {
+            const int bx = lane >> 3, j = lane & 7;
+            const int64_t col = ct * 128 + bx * 64 + j * 8;
+            if (col < C) {
+              const uint4 v = *reinterpret_cast<const uint4*>(tb + bx * kBox + rr * 128 + ((j ^ (rr & 7)) << 4));
+              *reinterpret_cast<uint4*>(orow.slice + int64_t(slot) * C + col) = v;
+            }
+          }
+          }
+        }
+      }
+      if (kCol && ocol.nzero > 0 && ocol.slice) {
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t hits = __ballot_sync(~0u, ct * 128 + c0 + lane < C && mask_hit(mcol, ct * 128 + c0 + lane));
+          while (hits) {
+          const int cc = c0 + __ffs(hits) - 1;
+          hits &= hits - 1;
+          const int64_t c = ct * 128 + cc;
+          const int slot = mask_slot(mcol, ocol.nzero, c);
+          const int bx = cc >> 6, cb = (cc & 63) * 2;
+          for (int rr = lane; rr < 128; rr += 32) {
+            const int64_t r = rt * 128 + rr;
+            if (r < R)
+              ocol.slice[int64_t(slot) * R + r] = *reinterpret_cast<const __nv_bfloat16*>(
+                  tb + bx * kBox + rr * 128 + ((((cb >> 4) ^ (rr & 7)) << 4) | (cb & 15)));
+          }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    // Dual launch: groups 0,1 -> row blocks {0,1},{2,3}; groups 2,3 -> column blocks {0,1},{2,3}.
+    // Single orientation: group g -> block g. Four warps per SM sub-partition hide the
+    // TMEM-load -> amax -> convert latency chain of each block.
+    constexpr int kOrients = (kRow ? 1 : 0) + (kCol ? 1 : 0);
+    constexpr int kBlocksPerGroup = 4 * kOrients / kEpiGroups;
+    constexpr int kGroupsPerOrient = kEpiGroups / kOrients;
+    const uint32_t group = (warp - 4) >> 2;
+    const uint32_t orient = group / kGroupsPerOrient;          // 0: first enabled orientation
+    const uint32_t sub = group % kGroupsPerOrient;
+    const bool col_side = kRow ? (orient == 1) : true;
+    const uint32_t q = warp & 3;
+    const Out& o = col_side ? ocol : orow;
+    const Mask* m = col_side ? mcol : mrow;
+    const CUtensorMap* tq = col_side ? &tm_qcol : &tm_qrow;
+    const int64_t K = col_side ? R : C;
+    const int64_t kch = col_side ? kch_col : kch_row;
+    const int64_t rows_total = col_side ? C : R;
+    const uint32_t row = q * 32 + lane;        // stored row within the tile = TMEM lane
+    const uint32_t blk0 = sub * kBlocksPerGroup;
+    const uint32_t oi = kRow ? orient : 0;     // staging slot of this orientation
+    const uint32_t sw = (row >> 1) & 3;        // 64B swizzle of the staging row
+    int lt = 0;
+    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
+      const int rt = tile % rtiles, ct = tile / rtiles;
+      const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
+      uint8_t* st = stg + (oi * 2 + buf) * kStg;
+      uint8_t* sst = sfstg + (oi * 2 + buf) * 512;
+      const int64_t srow = (col_side ? int64_t(ct) * 128 : int64_t(rt) * 128) + row;
+      const int64_t kb0 = (col_side ? int64_t(rt) * 4 : int64_t(ct) * 4) + blk0;   // first K-block of this group
+      const bool extracted = srow < rows_total && o.nzero > 0 && mask_hit(m, srow);
+      ptx::mbar_wait(&stgfree[buf], (use & 1) ^ 1);   // the store warp has read this staging buffer
+      ptx::mbar_wait(&tfull[buf], use & 1);
+      if (warp == 4 && lane == 0) QTC_T(3, lt);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int b = 0; b < kBlocksPerGroup; ++b) {
+        uint32_t d[32];
+        if (QTC_ABLATE & 2) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) d[i] = 0;
+        } else {
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + buf * 256 + (col_side ? 128 : 0) + (blk0 + b) * 32, d);
+          ptx::tmem_ld_wait();
+        }
+        if (b == kBlocksPerGroup - 1) {   // accumulators drained: the MMA warp may reuse this buffer
+          if (warp == 4 && lane == 0) QTC_T(4, lt);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+        }
+        float ysink[kHad ? 32 : 1];
+        uint4 c;
+        uint32_t sbyte;
+        if (QTC_ABLATE & 2) { c = make_uint4(d[0], d[1], d[2], d[3]); sbyte = 127; }
+        else quant_block<kHad>(d, c, sbyte, ysink);
+        if (extracted) { c = make_uint4(0, 0, 0, 0); sbyte = 127u; }
+        *reinterpret_cast<uint4*>(st + row * 64 + (((blk0 + b) ^ sw) << 4)) = c;
+        // SF chunk byte of (row, K-block) = (row % 32) * 16 + (row / 32) * 4 + kb % 4
+        sst[lane * 16 + q * 4 + blk0 + b] = uint8_t(sbyte);
+        if (kHad && srow < rows_total && (kb0 + b) * kBlk < K) {
+          float* dst = o.had + srow * K + (kb0 + b) * kBlk;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dst[i] = extracted ? 0.f : ysink[i];
+        }
+      }
+      ptx::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&staged[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem_base);
+  }
+#if QTC_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_qtc_trace[0][0];
+    for (int i = 0; i < 64 && first + i * stride < ntiles; ++i)
+      printf("qtc tile %2d: tma %7lld tempty %7lld full %7lld epi %7lld drained %7lld\n", i,
+             g_qtc_trace[0][i] - t0, g_qtc_trace[1][i] - t0, g_qtc_trace[2][i] - t0, g_qtc_trace[3][i] - t0,
+             g_qtc_trace[4][i] - t0);
+  }
+#endif
+}
+
+}  // namespace qtc
+
+size_t quant_tc_smem(bool masks) {
+  return size_t(qtc::kStages) * qtc::kTile + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
+         (masks ? 2 * sizeof(qtc::Mask) : 0);
+}
+
+bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask) {
+  return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+         (!row_mask || R <= qtc::kMaskMaxRows) && (!col_mask || C <= qtc::kMaskMaxRows);
+}
+
+template <bool kRow, bool kCol, bool kHad>
+static cudaError_t launch_tc(const CUtensorMap& tm, const CUtensorMap& tqr, const CUtensorMap& tqc, int64_t R, int64_t C, const qtc::Out& orow, const qtc::Out& ocol,
+                             bool masks, int num_sms, cudaStream_t st) {
+  const size_t smem = quant_tc_smem(masks);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(quant_tc_smem(true)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ntiles = ((R + 127) / 128) * ((C + 127) / 128);
+  const unsigned grid = unsigned(ntiles < num_sms ? ntiles : num_sms);
+  qtc::k_quant_tc<kRow, kCol, kHad><<<grid, qtc::kThreads, smem, st>>>(tm, tqr, tqc, R, C, orow, ocol);
+  return cudaGetLastError();
+}
+
+// T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) when q_row != nullptr; column
+// outputs (stored rows = C, K = R) when q_col != nullptr. had_* (debug, nullable) receive the
+// fp32 Hadamard output of the respective orientation.
+cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld, const int32_t* row_zero,
+                            int nrow_zero, __nv_bfloat16* slice_row, uint8_t* q_row, uint8_t* sf_row, float* had_row,
+                            const int32_t* col_zero, int ncol_zero, __nv_bfloat16* slice_col, uint8_t* q_col,
+                            uint8_t* sf_col, float* had_col, int num_sms, cudaStream_t st) {
+  CUtensorMap tm;
+  if (!make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(C), uint64_t(R), uint64_t(ld) * 2, 64, 128,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const bool row = q_row != nullptr, col = q_col != nullptr;
+  // code outputs, stored by TMA: [stored rows][K/2] bytes, 128 x 64-byte boxes, 64B swizzle
+  CUtensorMap tqr = tm, tqc = tm;
+  if (row && !make_tmap_2d(&tqr, CU_TENSOR_MAP_DATA_TYPE_UINT8, q_row, uint64_t(C / 2), uint64_t(R), uint64_t(C / 2),
+                           64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  if (col && !make_tmap_2d(&tqc, CU_TENSOR_MAP_DATA_TYPE_UINT8, q_col, uint64_t(R / 2), uint64_t(C), uint64_t(R / 2),
+                           64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  qtc::Out orow{q_row, sf_row, row_zero, row ? nrow_zero : 0, slice_row, had_row};
+  qtc::Out ocol{q_col, sf_col, col_zero, col ? ncol_zero : 0, slice_col, had_col};
+  const bool masks = (row && nrow_zero > 0) || (col && ncol_zero > 0);
+  const bool had = had_row != nullptr || had_col != nullptr;
+  if (row && col) {
+    if (had) return launch_tc<true, true, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+    return launch_tc<true, true, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+  }
+  if (row) {
+    if (had) return launch_tc<true, false, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+    return launch_tc<true, false, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+  }
+  if (col) {
+    if (had) return launch_tc<false, true, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+    return launch_tc<false, true, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
+  }
+  return cudaSuccess;
+}
+
+}  // namespace adahop
