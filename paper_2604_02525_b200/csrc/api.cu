@@ -140,7 +140,7 @@ bool plan_gemm(int64_t M, int64_t N, int64_t K, adahop_strategy_t s, const adaho
     g->rows_oe = s == ADAHOP_OE_LEFT_IHT ? M : N;
     g->mbig = s == ADAHOP_OE_LEFT_IHT ? N : M;
     g->kk = int(std::min<int64_t>(p->oe_k, g->rows_oe));
-    g->keys = c.take(size_t(g->rows_oe) * 8);
+    g->keys = c.take(foid_ws_bytes(g->rows_oe));
     g->idx = c.take(size_t(g->kk) * 4);
     g->slice = c.take(size_t(g->kk) * size_t(K) * 2);
     g->npad = bf16_gemm_npad(g->kk);
@@ -481,7 +481,7 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     if (L->kk_row[t]) { L->idx_row[t] = c.take(size_t(L->kk_row[t]) * 4); L->slice_row[t] = c.take(size_t(L->kk_row[t]) * size_t(C) * 2); }
     if (L->kk_col[t]) { L->idx_col[t] = c.take(size_t(L->kk_col[t]) * 4); L->slice_col[t] = c.take(size_t(L->kk_col[t]) * size_t(R) * 2); }
   }
-  L->keys = c.take(size_t(std::max<int64_t>(maxR, 1)) * 8);
+  L->keys = c.take(foid_ws_bytes(std::max<int64_t>(maxR, 1)));
   size_t part_bytes = 0;
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   for (int path = 0; path < 3; ++path) {
@@ -689,7 +689,7 @@ size_t adahop_debug_workspace_bytes(int64_t R, int64_t K) {
   if (R <= 0 || K <= 0) return 0;
   Carver c;
   c.take(size_t(sf_bytes(R, K)));
-  c.take(size_t(R) * 8);                                   // FOID keys
+  c.take(foid_ws_bytes(R));                                // FOID keys + candidates
   return c.take(0) + 256;
 }
 
@@ -764,7 +764,7 @@ adahop_status_t adahop_debug_foid(const void* in, adahop_dtype_t dt, int64_t R, 
   Carver c;
   uint8_t* w = static_cast<uint8_t*>(ws);
   c.take(size_t(sf_bytes(R, K)));
-  double* keys = reinterpret_cast<double*>(w + c.take(size_t(R) * 8));
+  double* keys = reinterpret_cast<double*>(w + c.take(foid_ws_bytes(R)));
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   ADAHOP_LAUNCH(launch_foid(in, dt == ADAHOP_DT_F32, R, K, ld, k_strided, int(kk), probe, keys,
                             idx_sorted, cs));

@@ -31,17 +31,16 @@ cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64
                             uint8_t* sf_col, float* had_col, int num_sms, cudaStream_t st);
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
-// FOID: probe keys (keys[R], fp64) + single-CTA radix top-k -> idx_sorted[min(k,R)].
-// R <= kFoidMaxRows. For R <= 4096 the keys are computed inside the select kernel (keys[]
-// is then not written).
+// FOID: probe keys + top-k -> idx_sorted[min(k,R)] (ascending). `keys` points to a scratch
+// buffer of foid_ws_bytes(R) bytes whose first R doubles receive the keys. R <= kFoidMaxRows.
 constexpr int64_t kFoidMaxRows = 16384;
+size_t foid_ws_bytes(int64_t R);
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                         int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
                         cudaStream_t st);
 cudaError_t launch_foid_keys_only(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld, int kstrided,
                                   int probe, double* keys, cudaStream_t st);
 int foid_launches(int64_t R, int64_t K, int probe);
-bool foid_keys_in_select(int64_t R, int64_t K, int probe);
 int64_t stats_chunks(int64_t R);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);

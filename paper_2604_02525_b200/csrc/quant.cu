@@ -863,9 +863,11 @@ constexpr int kProbeMax = 64;  // probe lengths above this take the generic path
 // 16-byte loads, then each lane folds its own row.
 template <typename T>
 __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int64_t R, int64_t ld,
-                                                   int kstrided, int p, double* __restrict__ keys) {
+                                                   int kstrided, int p, double* __restrict__ keys,
+                                                   unsigned* __restrict__ counter = nullptr) {
   __shared__ __align__(16) float stage[4][32][kProbeMax + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter = 0u;   // for k_foid_select
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p > kProbeMax) {  // generic (slow) path
     if (r >= R) return;
@@ -923,199 +925,176 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
   if (r < R) keys[r] = foid_key_seq(mine, p);
 }
 
-// Top-k by (key desc, index asc), written as ascending indices, in ONE CTA:
-//  * keys (fp64 >= 0, so their bit patterns are order-preserving) are staged in smem; for
-//    small operands the probe keys are computed here too (no separate launch);
-//  * MSB-first radix select with 11-bit digits over a shrinking candidate list: after each
-//    digit only the keys sharing the selected prefix are kept (stable in-place compaction),
-//    so the passes after the exponent digits touch a handful of keys; the select stops as
-//    soon as every remaining candidate is needed;
-//  * a block scan in index order then takes all keys above the prefix plus the
-//    lowest-indexed keys at the prefix, and writes them sorted.
-constexpr int kSelThreads = 1024;
-constexpr int64_t kSelSmemKeys = 16384;   // keys staged in smem up to this many rows
-constexpr int kSelPerThread = int(kSelSmemKeys / kSelThreads);
-constexpr int64_t kSelFuseKeys = 0;       // (in-kernel keys measured slower than the separate kernel)
+// Top-k by (key desc, index asc), written as ascending indices. Keys come from k_foid_keys.
+// The selection never sorts all R keys. topk_core selects the kk best of n <= 4096 pairs in
+// one CTA of 1024 threads:
+//  1. thread t holds entries t, t + 1024, ... (E <= 4); the 8 threads 8g..8g+7 form group g
+//     (128 groups) and find the group maximum in the total order (key desc, index asc);
+//  2. L = the kk-th largest group maximum (each maximum ranked by its 8 threads against all
+//     maxima). At least kk entries (those maxima) are >= L, so every top-kk entry is >= L; an
+//     entry >= L lies in a group whose maximum is >= L, so at most kk * 8E entries are >= L;
+//  3. the entries >= L are compacted into shared memory and ranked exactly among themselves.
+// k_foid_select runs it per 1024-row block (rows -> the block's kk best), and the last block
+// to finish runs it again over the blocks' nb * kk survivors. Keys are fp64 >= 0, so their
+// bit patterns order like the values; the index breaks ties, so the selected set is unique.
+constexpr int kTopkThreads = 1024;
+constexpr int kTopkGroupLanes = 8;
+constexpr int kTopkGroups = kTopkThreads / kTopkGroupLanes;
+constexpr int kTopkMaxPer = 4;                                   // n <= 4096
+constexpr int kTopkMaxCand = 256 * kTopkGroupLanes * kTopkMaxPer; // kk * 8E bound
 
-__device__ __forceinline__ int block_excl_scan(int v, int* sbuf /*[33]*/, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sbuf[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < (blockDim.x >> 5) ? sbuf[lane] : 0;
-    int ws = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, ws, o);
-      if (lane >= o) ws += y;
-    }
-    sbuf[lane] = ws - w;               // exclusive warp offsets
-    if (lane == 31) sbuf[32] = ws;     // total
-  }
-  __syncthreads();
-  const int res = sbuf[warp] + x - v;
-  *total = sbuf[32];
-  __syncthreads();
-  return res;
+__device__ __forceinline__ bool foid_before(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kSelThreads) k_foid_select(double* __restrict__ keys_g, const T* __restrict__ in,
-                                                             int64_t R, int64_t ld, int kstrided, int p, int k,
-                                                             int32_t* __restrict__ idx_sorted) {
-  extern __shared__ __align__(16) unsigned long long cand[];    // [R] candidate keys
-  __shared__ unsigned int hist[2048];
-  __shared__ unsigned long long s_prefix;
-  __shared__ int s_kr, s_n;
-  __shared__ int sbuf[33];
+struct TopkSmem {
+  unsigned long long gmk[kTopkGroups];
+  int gmi[kTopkGroups];
+  unsigned long long lk;
+  int li, nc, last;
+};
+
+// Entries come from (src_key[e], src_idx ? src_idx[e] : idx0 + e), e < n. Writes the kk best
+// in rank order to sel_key / sel_idx (shared or global) — rank r at position r.
+__device__ void topk_core(const unsigned long long* __restrict__ src_key, const int* __restrict__ src_idx, int idx0,
+                          int n, int kk, TopkSmem& sm, unsigned long long* ckey, int* cidx,
+                          unsigned long long* sel_key, int* sel_idx) {
   const int tid = threadIdx.x;
-  const unsigned long long* skeys = reinterpret_cast<const unsigned long long*>(keys_g);  // index order (L2)
-  // ---- keys
-  if (in != nullptr) {  // fused: compute the probe keys of all R rows here
-    for (int64_t r = tid; r < R; r += blockDim.x) {
-      // two streaming passes (sum, then squared deviations) in the oracle's fixed order
-      double sum = 0.0;
-#pragma unroll 16
-      for (int j = 0; j < p; ++j)
-        sum = __dadd_rn(sum, double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)));
-      const double mu = sum / double(p);
-      double v = 0.0;
-#pragma unroll 16
-      for (int j = 0; j < p; ++j) {
-        const double d = __dsub_rn(double(load_as_float(in, kstrided ? int64_t(j) * ld + r : r * ld + j)), mu);
-        v = __dadd_rn(v, __dmul_rn(d, d));
-      }
-      const double key = v / double(p);
-      keys_g[r] = key;
-      cand[r] = __double_as_longlong(key);
-    }
-  } else {
-    for (int64_t i = tid; i < R; i += blockDim.x) cand[i] = __double_as_longlong(keys_g[i]);
+  const int E = (n + kTopkThreads - 1) / kTopkThreads;
+  const int NG = min(kTopkGroups, (n + kTopkGroupLanes - 1) / kTopkGroupLanes);   // groups with entries
+  const int g = tid / kTopkGroupLanes, qq = tid % kTopkGroupLanes;
+  unsigned long long k[kTopkMaxPer];
+  int x[kTopkMaxPer];
+#pragma unroll
+  for (int j = 0; j < kTopkMaxPer; ++j) {
+    const int e = j * kTopkThreads + tid;
+    const bool ok = j < E && e < n;
+    k[j] = ok ? src_key[e] : 0ull;
+    x[j] = ok ? (src_idx ? src_idx[e] : idx0 + e) : 0x7FFFFFFF;
   }
-  const int kk = int(int64_t(k) < R ? int64_t(k) : R);
-  int n = int(R);            // live candidates (all share `prefix` above `shift`)
-  int kr = kk;               // rank of the boundary key among the candidates
-  unsigned long long prefix = 0;
-  int shift = 64;
-  bool take_all = false;     // every candidate at the final prefix is selected
+  unsigned long long mk = 0;
+  int mi = 0x7FFFFFFF;
+#pragma unroll
+  for (int j = 0; j < kTopkMaxPer; ++j)
+    if (foid_before(k[j], x[j], mk, mi)) { mk = k[j]; mi = x[j]; }
+#pragma unroll
+  for (int o = 1; o < kTopkGroupLanes; o <<= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, mk, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+    if (foid_before(ok, oi, mk, mi)) { mk = ok; mi = oi; }
+  }
+  if (qq == 0) { sm.gmk[g] = mk; sm.gmi[g] = mi; }
+  if (tid == 0) sm.nc = 0;
   __syncthreads();
-  for (int pass = 0; pass < 6 && !take_all; ++pass) {
-    const int bits = pass < 5 ? 11 : 9;   // 5 x 11 + 9 = 64
-    const int nshift = shift - bits;
-    for (int i = tid; i < 2048; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const int nup = (n + 31) & ~31;
-    for (int i = tid; i < nup; i += blockDim.x) {
-      int digit = -1;
-      if (i < n) digit = int((cand[i] >> nshift) & ((1ull << bits) - 1));
-      const unsigned grp = __match_any_sync(0xffffffffu, digit);
-      if (digit >= 0 && (tid & 31) == __ffs(grp) - 1) atomicAdd(&hist[digit], unsigned(__popc(grp)));
-    }
-    __syncthreads();
-    // find the digit holding rank kr (counting from the largest digit): 1024 threads x 2 bins
-    {
-      const int b0 = 2047 - 2 * tid, b1 = b0 - 1;
-      const int c0 = int(hist[b0]), c1 = int(hist[b1]);
-      int tot;
-      const int before = block_excl_scan(c0 + c1, sbuf, &tot);
-      if (before < kr && kr <= before + c0 + c1) {
-        int d, above;
-        if (kr <= before + c0) { d = b0; above = before; }
-        else { d = b1; above = before + c0; }
-        s_prefix = (prefix << bits) | (unsigned long long)d;
-        s_kr = kr - above;
-        s_n = int(hist[d]);
+  if (kk <= NG) {
+    int rank = 0;
+    if (g < NG)
+      for (int u = qq; u < NG; u += kTopkGroupLanes) rank += foid_before(sm.gmk[u], sm.gmi[u], mk, mi);
+#pragma unroll
+    for (int o = 1; o < kTopkGroupLanes; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (qq == 0 && g < NG && rank == kk - 1) { sm.lk = mk; sm.li = mi; }
+  } else if (tid == 0) {
+    sm.lk = 0; sm.li = 0x7FFFFFFF;   // fewer groups than kk: every entry is a candidate
+  }
+  __syncthreads();
+  const unsigned long long lk = sm.lk;
+  const int li = sm.li;
+#pragma unroll
+  for (int j = 0; j < kTopkMaxPer; ++j) {
+    if (j >= E) break;
+    const bool c = j * kTopkThreads + tid < n && !foid_before(lk, li, k[j], x[j]);   // >= L
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if (m) {
+      int wbase = 0;
+      if ((tid & 31) == 0) wbase = atomicAdd(&sm.nc, __popc(m));
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (c) {
+        const int pos = wbase + __popc(m & ((1u << (tid & 31)) - 1u));
+        ckey[pos] = k[j];
+        cidx[pos] = x[j];
       }
     }
+  }
+  __syncthreads();
+  const int nc = sm.nc;
+  for (int c = tid; c < nc; c += kTopkThreads) {
+    const unsigned long long a = ckey[c];
+    const int ai = cidx[c];
+    int rank = 0;
+    for (int u = 0; u < nc; ++u) rank += foid_before(ckey[u], cidx[u], a, ai);
+    if (rank < kk) { sel_key[rank] = a; sel_idx[rank] = ai; }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_foid_select(const double* __restrict__ keys_g, int R, int kk,
+                                                              unsigned long long* __restrict__ part_key,
+                                                              int* __restrict__ part_idx, unsigned* __restrict__ counter,
+                                                              int32_t* __restrict__ idx_sorted) {
+  extern __shared__ __align__(16) unsigned long long ckey[];   // [kTopkMaxCand] keys, then indices
+  int* cidx = reinterpret_cast<int*>(ckey + kTopkMaxCand);
+  __shared__ TopkSmem sm;
+  __shared__ unsigned long long fkey[256];
+  __shared__ int fidx[256];
+  const int nb = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int n_b = min(kTopkThreads, R - b * kTopkThreads);
+  const int kb = min(kk, n_b);
+  const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(keys_g);
+  // this block's kb best rows (padding up to kk with entries that rank after every row)
+  topk_core(keys + int64_t(b) * kTopkThreads, nullptr, b * kTopkThreads, n_b, kb, sm, ckey, cidx,
+            part_key + int64_t(b) * kk, part_idx + int64_t(b) * kk);
+  for (int t = kb + tid; t < kk; t += kTopkThreads) { part_key[int64_t(b) * kk + t] = 0ull; part_idx[int64_t(b) * kk + t] = 0x7FFFFFFF; }
+  if (nb == 1) {
+    if (tid < kk) { fkey[tid] = part_key[tid]; fidx[tid] = part_idx[tid]; }
+  } else {
+    __threadfence();
     __syncthreads();
-    prefix = s_prefix;
-    kr = s_kr;
-    const int n_new = s_n;
-    shift = nshift;
-    take_all = n_new == kr;
-    if (pass < 5 && !take_all) {
-      // stable in-place compaction of the candidates carrying the selected digit
-      unsigned long long mine[kSelPerThread];
-      int cnt = 0;
-      const int seg = (n + blockDim.x - 1) / blockDim.x;
-      const int i0 = min(n, tid * seg), i1 = min(n, i0 + seg);
-      for (int i = i0; i < i1; ++i) {
-        const unsigned long long u = cand[i];
-        if ((u >> shift) == prefix) mine[cnt++] = u;
-      }
-      int tot;
-      const int pos = block_excl_scan(cnt, sbuf, &tot);   // contains the barriers we need
-      for (int i = 0; i < cnt; ++i) cand[pos + i] = mine[i];
-      n = tot;
-      __syncthreads();
-    }
+    if (tid == 0) sm.last = atomicAdd(counter, 1u) == unsigned(nb - 1);
+    __syncthreads();
+    if (!sm.last) return;
+    __threadfence();
+    topk_core(part_key, part_idx, 0, nb * kk, kk, sm, ckey, cidx, fkey, fidx);
   }
-  // ---- selection in index order: keys above the prefix, plus (all | the kr lowest-indexed)
-  //      keys at the prefix
-  const int64_t seg = (R + blockDim.x - 1) / blockDim.x;
-  const int64_t i0 = (int64_t(tid) * seg < R ? int64_t(tid) * seg : R);
-  const int64_t i1 = (i0 + seg < R ? i0 + seg : R);
-  int n_eq = 0;
-  for (int64_t i = i0; i < i1; ++i) n_eq += (skeys[i] >> shift) == prefix;
-  int tot_eq;
-  const int eq_before = block_excl_scan(n_eq, sbuf, &tot_eq);
-  int n_sel = 0;
-  {
-    int e = eq_before;
-    for (int64_t i = i0; i < i1; ++i) {
-      const unsigned long long t = skeys[i] >> shift;
-      if (t > prefix) ++n_sel;
-      else if (t == prefix) { if (take_all || e < kr) ++n_sel; ++e; }
-    }
+  __syncthreads();
+  const int kkr = min(kk, R);
+  if (tid < kkr) {   // ascending index order
+    const int v = fidx[tid];
+    int pos = 0;
+    for (int u = 0; u < kkr; ++u) pos += fidx[u] < v;
+    idx_sorted[pos] = v;
   }
-  int tot_sel;
-  int pos = block_excl_scan(n_sel, sbuf, &tot_sel);
-  {
-    int e = eq_before;
-    for (int64_t i = i0; i < i1; ++i) {
-      const unsigned long long t = skeys[i] >> shift;
-      bool take = false;
-      if (t > prefix) take = true;
-      else if (t == prefix) { take = take_all || e < kr; ++e; }
-      if (take) idx_sorted[pos++] = int32_t(i);
-    }
-  }
+}
+
+// scratch: keys [R] f64 | survivors [nb * 256] (u64 key, i32 index) | counter
+size_t foid_ws_bytes(int64_t R) {
+  const int64_t nb = (R + kTopkThreads - 1) / kTopkThreads;
+  return size_t(R) * 8 + size_t(nb) * 256 * 12 + 64;
 }
 
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                         int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
                         cudaStream_t st) {
-  if (R > kSelSmemKeys) return cudaErrorInvalidValue;   // host validates first
+  if (R > kFoidMaxRows || R <= 0 || k <= 0 || k > 256) return cudaErrorInvalidValue;   // host validates first
   const int p = int(std::min<int64_t>(probe, K));
-  const bool fuse = R <= kSelFuseKeys && p <= kProbeMax;
-  if (!fuse) {
-    const unsigned kb = unsigned((R + 127) / 128);
-    if (in_f32) k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys);
-    else k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys);
-  }
-  const size_t smem = size_t(R) * 8;
+  const int nb = int((R + kTopkThreads - 1) / kTopkThreads);
+  unsigned long long* part_key = reinterpret_cast<unsigned long long*>(keys + R);
+  int* part_idx = reinterpret_cast<int*>(part_key + size_t(nb) * 256);
+  unsigned* counter = reinterpret_cast<unsigned*>(part_idx + size_t(nb) * 256);
+  const unsigned kb = unsigned((R + 127) / 128);
+  if (in_f32)
+    k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys, counter);
+  else
+    k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys,
+                                                   counter);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_foid_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSelSmemKeys * 8));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_foid_select<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(kSelSmemKeys * 8));
+    cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kTopkMaxCand * 12));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (in_f32)
-    k_foid_select<float><<<1, kSelThreads, smem, st>>>(keys, fuse ? static_cast<const float*>(in) : nullptr, R, ld,
-                                                        kstrided, p, k, idx_sorted);
-  else
-    k_foid_select<__nv_bfloat16><<<1, kSelThreads, smem, st>>>(
-        keys, fuse ? static_cast<const __nv_bfloat16*>(in) : nullptr, R, ld, kstrided, p, k, idx_sorted);
+  k_foid_select<<<nb, kTopkThreads, kTopkMaxCand * 12, st>>>(keys, int(R), k, part_key, part_idx, counter,
+                                                             idx_sorted);
   return cudaGetLastError();
 }
 
@@ -1132,12 +1111,7 @@ bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask) {
   return (!row_mask || R <= kMaskMaxRows) && (!col_mask || C <= kMaskMaxRows);
 }
 
-int foid_launches(int64_t R, int64_t K, int probe) {
-  const int p = int(std::min<int64_t>(probe, K));
-  return (R <= kSelFuseKeys && p <= kProbeMax) ? 1 : 2;
-}
-
-bool foid_keys_in_select(int64_t R, int64_t K, int probe) { return foid_launches(R, K, probe) == 1; }
+int foid_launches(int64_t, int64_t, int) { return 2; }
 
 // ================================================================== calibration stats
 // Row statistics: one warp per row, fp64 accumulation, fixed-order shuffle reduction.

@@ -364,9 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3;
     const Out& o = col_side ? ocol : orow;
     const Mask* m = col_side ? mcol : mrow;
-    const CUtensorMap* tq = col_side ? &tm_qcol : &tm_qrow;
     const int64_t K = col_side ? R : C;
-    const int64_t kch = col_side ? kch_col : kch_row;
     const int64_t rows_total = col_side ? C : R;
     const uint32_t row = q * 32 + lane;        // stored row within the tile = TMEM lane
     const uint32_t blk0 = sub * kBlocksPerGroup;
