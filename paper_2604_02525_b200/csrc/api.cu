@@ -440,7 +440,7 @@ struct LayerPlan {
   // masks: which FOID feeds which (tensor, orientation)
   int kk_row[3], kk_col[3];
   size_t idx_row[3], idx_col[3], slice_row[3], slice_col[3];
-  size_t keys = 0, part = 0;
+  size_t keys_row[3], keys_col[3], part = 0;   // per-FOID scratch
   int splits[3];
   int64_t npad[3], mbig[3];
   size_t total = 0;
@@ -457,7 +457,6 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
   L->R[1] = d_out; L->C[1] = d_in;
   L->R[2] = T; L->C[2] = d_out;
   for (int t = 0; t < 3; ++t) { L->kk_row[t] = L->kk_col[t] = 0; L->need_row[t] = L->need_col[t] = false; }
-  int64_t maxR = 0;
   for (int path = 0; path < 3; ++path) {
     if (s[path] == ADAHOP_BF16) continue;
     const int ta = kPathA[path], tb = kPathB[path];
@@ -470,7 +469,6 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
       const int64_t rows = o ? L->C[t] : L->R[t];        // stored rows of the OE operand
       const int kk = int(std::min<int64_t>(p->oe_k, rows));
       (o ? L->kk_col : L->kk_row)[t] = kk;
-      maxR = std::max(maxR, rows);
     }
   }
   Carver c;
@@ -478,10 +476,17 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     const int64_t R = L->R[t], C = L->C[t];
     if (L->need_row[t]) { L->q_row[t] = c.take(size_t(R) * size_t(C / 2)); L->sf_row[t] = c.take(size_t(sf_bytes(R, C))); }
     if (L->need_col[t]) { L->q_col[t] = c.take(size_t(C) * size_t(R / 2)); L->sf_col[t] = c.take(size_t(sf_bytes(C, R))); }
-    if (L->kk_row[t]) { L->idx_row[t] = c.take(size_t(L->kk_row[t]) * 4); L->slice_row[t] = c.take(size_t(L->kk_row[t]) * size_t(C) * 2); }
-    if (L->kk_col[t]) { L->idx_col[t] = c.take(size_t(L->kk_col[t]) * 4); L->slice_col[t] = c.take(size_t(L->kk_col[t]) * size_t(R) * 2); }
+    if (L->kk_row[t]) {
+      L->idx_row[t] = c.take(size_t(L->kk_row[t]) * 4);
+      L->slice_row[t] = c.take(size_t(L->kk_row[t]) * size_t(C) * 2);
+      L->keys_row[t] = c.take(foid_ws_bytes(R));
+    }
+    if (L->kk_col[t]) {
+      L->idx_col[t] = c.take(size_t(L->kk_col[t]) * 4);
+      L->slice_col[t] = c.take(size_t(L->kk_col[t]) * size_t(R) * 2);
+      L->keys_col[t] = c.take(foid_ws_bytes(C));
+    }
   }
-  L->keys = c.take(foid_ws_bytes(std::max<int64_t>(maxR, 1)));
   size_t part_bytes = 0;
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   for (int path = 0; path < 3; ++path) {
@@ -547,16 +552,20 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
   stage_mark(0, cs);
   // ---- 1. FOID for every OE operand: row orientation = rows of the tensor
   //         (K-contiguous probe), column orientation = columns (probe = first 64 rows)
-  for (int t = 0; t < 3; ++t) {
-    if (L.kk_row[t]) {
-      ADAHOP_LAUNCH(launch_foid(src[t], false, L.R[t], L.C[t], L.C[t], 0, L.kk_row[t], p->foid_probe,
-                                reinterpret_cast<double*>(w + L.keys), reinterpret_cast<int32_t*>(w + L.idx_row[t]), cs));
-      launches += foid_launches(L.R[t], L.C[t], p->foid_probe);
+  {
+    FoidJob jobs[kFoidMaxJobs];
+    int nj = 0;
+    for (int t = 0; t < 3; ++t) {
+      if (L.kk_row[t])
+        jobs[nj++] = FoidJob{src[t], L.R[t], L.C[t], L.C[t], 0, L.kk_row[t], p->foid_probe,
+                             reinterpret_cast<double*>(w + L.keys_row[t]), reinterpret_cast<int32_t*>(w + L.idx_row[t])};
+      if (L.kk_col[t])
+        jobs[nj++] = FoidJob{src[t], L.C[t], L.R[t], L.C[t], 1, L.kk_col[t], p->foid_probe,
+                             reinterpret_cast<double*>(w + L.keys_col[t]), reinterpret_cast<int32_t*>(w + L.idx_col[t])};
     }
-    if (L.kk_col[t]) {
-      ADAHOP_LAUNCH(launch_foid(src[t], false, L.C[t], L.R[t], L.C[t], 1, L.kk_col[t], p->foid_probe,
-                                reinterpret_cast<double*>(w + L.keys), reinterpret_cast<int32_t*>(w + L.idx_col[t]), cs));
-      launches += foid_launches(L.C[t], L.R[t], p->foid_probe);
+    if (nj) {
+      ADAHOP_LAUNCH(launch_foid_batch(jobs, nj, false, cs));
+      launches += 2;
     }
   }
   stage_mark(1, cs);

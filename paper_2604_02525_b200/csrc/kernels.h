@@ -41,6 +41,12 @@ cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64
 cudaError_t launch_foid_keys_only(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld, int kstrided,
                                   int probe, double* keys, cudaStream_t st);
 int foid_launches(int64_t R, int64_t K, int probe);
+// Several FOIDs in two launches (keys, select); each job has its own foid_ws_bytes(R) scratch.
+constexpr int kFoidMaxJobs = 6;
+struct FoidJob {
+  const void* in; int64_t R, K, ld; int kstrided, k, probe; double* scratch; int32_t* idx;
+};
+cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStream_t st);
 int64_t stats_chunks(int64_t R);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);

@@ -4,6 +4,7 @@
 //   * FOID: fp64 probe variance, deterministic top-k, outlier-slice gather  [P:760]
 //   * pattern statistics for calibration (per-row / per-column moments)    [P:523-541]
 //   * layout converters used only by the debug / parity entry points
+#include <cstdio>
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -862,13 +863,11 @@ constexpr int kProbeMax = 64;  // probe lengths above this take the generic path
 // K-contiguous operand: a warp stages the probes of its 32 rows into shared memory with
 // 16-byte loads, then each lane folds its own row.
 template <typename T>
-__global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int64_t R, int64_t ld,
-                                                   int kstrided, int p, double* __restrict__ keys,
-                                                   unsigned* __restrict__ counter = nullptr) {
+__device__ __forceinline__ void foid_keys_block(const T* __restrict__ in, int64_t R, int64_t ld, int kstrided, int p,
+                                                double* __restrict__ keys, int bid) {
   __shared__ __align__(16) float stage[4][32][kProbeMax + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter = 0u;   // for k_foid_select
-  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = int64_t(bid) * blockDim.x + threadIdx.x;
   if (p > kProbeMax) {  // generic (slow) path
     if (r >= R) return;
     double s = 0.0;
@@ -897,7 +896,7 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
       for (int j = 0; j < p; ++j) mine[j] = load_as_float(in, int64_t(j) * ld + r);
     }
   } else {
-    const int64_t rw = int64_t(blockIdx.x) * blockDim.x + warp * 32;  // first row of this warp
+    const int64_t rw = int64_t(bid) * blockDim.x + warp * 32;  // first row of this warp
     if (sizeof(T) == 2 && p == 64 && ((ld * 2) % 16) == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
       // 32 rows x 128 B: 256 16-byte chunks, 8 per lane, 8 lanes per row -> full lines
 #pragma unroll
@@ -923,6 +922,42 @@ __global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int
     __syncwarp();
   }
   if (r < R) keys[r] = foid_key_seq(mine, p);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_foid_keys(const T* __restrict__ in, int64_t R, int64_t ld, int kstrided,
+                                                   int p, double* __restrict__ keys) {
+  foid_keys_block(in, R, ld, kstrided, p, keys, blockIdx.x);
+}
+
+// A batch of FOID jobs (the OE operands of one linear): one keys launch and one select launch
+// for all of them. Job j owns key blocks [kb_off[j], kb_off[j+1]) and select blocks
+// [sb_off[j], sb_off[j+1]).
+struct FoidJobDev {
+  const void* in; int64_t R, ld; int kstrided, p, k; double* scratch; int32_t* idx;
+};
+struct FoidBatchDev {
+  FoidJobDev j[kFoidMaxJobs];
+  int n;
+  int kb_off[kFoidMaxJobs + 1], sb_off[kFoidMaxJobs + 1];
+};
+__device__ __forceinline__ int foid_job_of(const int* off, int n, int b) {
+  int j = 0;
+  while (j + 1 < n && b >= off[j + 1]) ++j;
+  return j;
+}
+__device__ __forceinline__ unsigned* foid_counter(const FoidJobDev& J) {
+  const int64_t nb = (J.R + 1023) / 1024;
+  return reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(J.scratch) + J.R * 8 + nb * 256 * 12);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_foid_keys_batch(const __grid_constant__ FoidBatchDev B) {
+  const int jb = foid_job_of(B.kb_off, B.n, blockIdx.x);
+  const FoidJobDev& J = B.j[jb];
+  const int bid = blockIdx.x - B.kb_off[jb];
+  if (bid == 0 && threadIdx.x == 0) *foid_counter(J) = 0u;   // for k_foid_select
+  foid_keys_block(static_cast<const T*>(J.in), J.R, J.ld, J.kstrided, J.p, J.scratch, bid);
 }
 
 // Top-k by (key desc, index asc), written as ascending indices. Keys come from k_foid_keys.
@@ -1017,33 +1052,55 @@ __device__ void topk_core(const unsigned long long* __restrict__ src_key, const 
   }
   __syncthreads();
   const int nc = sm.nc;
-  for (int c = tid; c < nc; c += kTopkThreads) {
-    const unsigned long long a = ckey[c];
-    const int ai = cidx[c];
+  // rank of candidate c: a team of 8 lanes (the group lanes) splits the comparisons
+  const int ncr = (nc + kTopkGroups - 1) / kTopkGroups * kTopkGroups;   // uniform trip count per warp
+  for (int c = g; c < ncr; c += kTopkGroups) {
+    const bool live = c < nc;
+    const unsigned long long a = live ? ckey[c] : 0ull;
+    const int ai = live ? cidx[c] : 0;
     int rank = 0;
-    for (int u = 0; u < nc; ++u) rank += foid_before(ckey[u], cidx[u], a, ai);
-    if (rank < kk) { sel_key[rank] = a; sel_idx[rank] = ai; }
+    if (live)
+      for (int u = qq; u < nc; u += kTopkGroupLanes) rank += foid_before(ckey[u], cidx[u], a, ai);
+#pragma unroll
+    for (int o = 1; o < kTopkGroupLanes; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (live && qq == 0 && rank < kk) { sel_key[rank] = a; sel_idx[rank] = ai; }
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kTopkThreads) k_foid_select(const double* __restrict__ keys_g, int R, int kk,
-                                                              unsigned long long* __restrict__ part_key,
-                                                              int* __restrict__ part_idx, unsigned* __restrict__ counter,
-                                                              int32_t* __restrict__ idx_sorted) {
+#ifndef FOID_TRACE
+#define FOID_TRACE 0
+#endif
+#if FOID_TRACE
+__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#endif
+__global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_constant__ FoidBatchDev B) {
+#if FOID_TRACE
+  const long long t0 = gtime();
+#endif
   extern __shared__ __align__(16) unsigned long long ckey[];   // [kTopkMaxCand] keys, then indices
   int* cidx = reinterpret_cast<int*>(ckey + kTopkMaxCand);
   __shared__ TopkSmem sm;
   __shared__ unsigned long long fkey[256];
   __shared__ int fidx[256];
-  const int nb = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int jb = foid_job_of(B.sb_off, B.n, blockIdx.x);
+  const FoidJobDev& J = B.j[jb];
+  const int R = int(J.R), kk = J.k;
+  const int nb = B.sb_off[jb + 1] - B.sb_off[jb], b = blockIdx.x - B.sb_off[jb], tid = threadIdx.x;
+  unsigned long long* part_key = reinterpret_cast<unsigned long long*>(J.scratch + R);
+  int* part_idx = reinterpret_cast<int*>(part_key + size_t(nb) * 256);
+  unsigned* counter = foid_counter(J);
   const int n_b = min(kTopkThreads, R - b * kTopkThreads);
   const int kb = min(kk, n_b);
-  const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(keys_g);
+  const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(J.scratch);
   // this block's kb best rows (padding up to kk with entries that rank after every row)
   topk_core(keys + int64_t(b) * kTopkThreads, nullptr, b * kTopkThreads, n_b, kb, sm, ckey, cidx,
             part_key + int64_t(b) * kk, part_idx + int64_t(b) * kk);
   for (int t = kb + tid; t < kk; t += kTopkThreads) { part_key[int64_t(b) * kk + t] = 0ull; part_idx[int64_t(b) * kk + t] = 0x7FFFFFFF; }
+#if FOID_TRACE
+  const long long t1 = gtime();
+  const int nc1 = sm.nc;
+#endif
   if (nb == 1) {
     if (tid < kk) { fkey[tid] = part_key[tid]; fidx[tid] = part_idx[tid]; }
   } else {
@@ -1053,7 +1110,45 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const double* __re
     __syncthreads();
     if (!sm.last) return;
     __threadfence();
-    topk_core(part_key, part_idx, 0, nb * kk, kk, sm, ckey, cidx, fkey, fidx);
+#if FOID_TRACE
+    const long long t2 = gtime();
+#endif
+    // merge: the nb lists are each sorted; merge them pairwise (log2 nb levels), keeping the
+    // first kk of every merge. An entry at position p of one list lands at p + (entries of the
+    // partner list before it), found by binary search.
+    unsigned long long* ka = ckey;
+    int* xa = cidx;
+    unsigned long long* kb2 = ckey + 4096;
+    int* xb = cidx + 4096;
+    for (int e = tid; e < nb * kk; e += kTopkThreads) { ka[e] = __ldcg(part_key + e); xa[e] = __ldcg(part_idx + e); }
+    __syncthreads();
+    for (int m = nb; m > 1; m = (m + 1) >> 1) {
+      for (int e = tid; e < m * kk; e += kTopkThreads) {
+        const int l = e / kk, pe = e - l * kk;
+        const int q = l >> 1;
+        if (l == m - 1 && (m & 1)) {   // odd list out: carried over unchanged
+          kb2[q * kk + pe] = ka[e]; xb[q * kk + pe] = xa[e];
+          continue;
+        }
+        const int other = (l ^ 1) * kk;
+        const unsigned long long a = ka[e];
+        const int ai = xa[e];
+        int lo = 0, hi = kk;   // entries of the partner list before (a, ai)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (foid_before(ka[other + mid], xa[other + mid], a, ai)) lo = mid + 1; else hi = mid;
+        }
+        const int pos = pe + lo;
+        if (pos < kk) { kb2[q * kk + pos] = a; xb[q * kk + pos] = ai; }
+      }
+      __syncthreads();
+      unsigned long long* tk = ka; ka = kb2; kb2 = tk;
+      int* tx = xa; xa = xb; xb = tx;
+    }
+    for (int t = tid; t < kk; t += kTopkThreads) { fkey[t] = ka[t]; fidx[t] = xa[t]; }
+#if FOID_TRACE
+    if (tid == 0) printf("select b=%d: start %lld phaseL %lld (nc %d) merge-start %lld end %lld\n", b, t0 % 100000000, t1 - t0, nc1, t2 - t0, gtime() - t0);
+#endif
   }
   __syncthreads();
   const int kkr = min(kk, R);
@@ -1061,7 +1156,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const double* __re
     const int v = fidx[tid];
     int pos = 0;
     for (int u = 0; u < kkr; ++u) pos += fidx[u] < v;
-    idx_sorted[pos] = v;
+    J.idx[pos] = v;
   }
 }
 
@@ -1071,21 +1166,21 @@ size_t foid_ws_bytes(int64_t R) {
   return size_t(R) * 8 + size_t(nb) * 256 * 12 + 64;
 }
 
-cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
-                        int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
-                        cudaStream_t st) {
-  if (R > kFoidMaxRows || R <= 0 || k <= 0 || k > 256) return cudaErrorInvalidValue;   // host validates first
-  const int p = int(std::min<int64_t>(probe, K));
-  const int nb = int((R + kTopkThreads - 1) / kTopkThreads);
-  unsigned long long* part_key = reinterpret_cast<unsigned long long*>(keys + R);
-  int* part_idx = reinterpret_cast<int*>(part_key + size_t(nb) * 256);
-  unsigned* counter = reinterpret_cast<unsigned*>(part_idx + size_t(nb) * 256);
-  const unsigned kb = unsigned((R + 127) / 128);
-  if (in_f32)
-    k_foid_keys<float><<<kb, 128, 0, st>>>(static_cast<const float*>(in), R, ld, kstrided, p, keys, counter);
-  else
-    k_foid_keys<__nv_bfloat16><<<kb, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, ld, kstrided, p, keys,
-                                                   counter);
+cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kFoidMaxJobs) return cudaErrorInvalidValue;
+  FoidBatchDev B{};
+  B.n = n;
+  B.kb_off[0] = B.sb_off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    const FoidJob& J = jobs[i];
+    if (J.R > kFoidMaxRows || J.R <= 0 || J.k <= 0 || J.k > 256) return cudaErrorInvalidValue;
+    B.j[i] = FoidJobDev{J.in, J.R, J.ld, J.kstrided, int(std::min<int64_t>(J.probe, J.K)), J.k, J.scratch, J.idx};
+    B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
+    B.sb_off[i + 1] = B.sb_off[i] + int((J.R + kTopkThreads - 1) / kTopkThreads);
+  }
+  if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
+  else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1093,9 +1188,15 @@ cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_foid_select<<<nb, kTopkThreads, kTopkMaxCand * 12, st>>>(keys, int(R), k, part_key, part_idx, counter,
-                                                             idx_sorted);
+  k_foid_select<<<B.sb_off[n], kTopkThreads, kTopkMaxCand * 12, st>>>(B);
   return cudaGetLastError();
+}
+
+cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
+                        int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,
+                        cudaStream_t st) {
+  const FoidJob J{in, R, K, ld, kstrided, k, probe, keys, idx_sorted};
+  return launch_foid_batch(&J, 1, in_f32, st);
 }
 
 cudaError_t launch_foid_keys_only(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld, int kstrided,
