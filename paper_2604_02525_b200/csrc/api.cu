@@ -569,8 +569,34 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     }
   }
   stage_mark(1, cs);
-  // ---- 2. one quantisation pass per tensor (both orientations when both are consumed)
+  // ---- 2. one quantisation pass per tensor (both orientations when both are consumed); the
+  //         tensors that need both orientations share ONE persistent tensor-core launch
+  QuantTcJob tc_jobs[3];
+  int n_tc = 0;
+  bool in_tc[3] = {false, false, false};
   for (int t = 0; t < 3; ++t) {
+    const int64_t R = L.R[t], C = L.C[t];
+    if (!(L.need_row[t] && L.need_col[t]) || !quant_use_tc() ||
+        !quant_tc_supported(R, C, C, src[t], L.kk_row[t] > 0, L.kk_col[t] > 0))
+      continue;
+    in_tc[t] = true;
+    tc_jobs[n_tc++] = QuantTcJob{
+        src[t], R, C, C,
+        L.kk_row[t] ? reinterpret_cast<const int32_t*>(w + L.idx_row[t]) : nullptr, L.kk_row[t],
+        L.kk_row[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_row[t]) : nullptr, w + L.q_row[t], w + L.sf_row[t],
+        nullptr,
+        L.kk_col[t] ? reinterpret_cast<const int32_t*>(w + L.idx_col[t]) : nullptr, L.kk_col[t],
+        L.kk_col[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_col[t]) : nullptr, w + L.q_col[t], w + L.sf_col[t],
+        nullptr};
+    if ((R % 128) || (C % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_row[t], 0, size_t(sf_bytes(R, C)), cs));
+    if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
+  }
+  if (n_tc) {
+    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, dev.sms, cs));
+    launches += 1;
+  }
+  for (int t = 0; t < 3; ++t) {
+    if (in_tc[t]) continue;
     const int64_t R = L.R[t], C = L.C[t];
     const int32_t* rz = L.kk_row[t] ? reinterpret_cast<const int32_t*>(w + L.idx_row[t]) : nullptr;
     const int32_t* cz = L.kk_col[t] ? reinterpret_cast<const int32_t*>(w + L.idx_col[t]) : nullptr;

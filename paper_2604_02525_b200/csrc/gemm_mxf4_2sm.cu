@@ -16,6 +16,17 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+#ifndef GEMM_TRACE
+#define GEMM_TRACE 0
+#endif
+#if GEMM_TRACE
+#include <cstdio>
+__device__ long long g_gt[6][64];
+#define GT(k, lt) do { if (blockIdx.x == 0 && (lt) < 64) g_gt[k][lt] = clock64(); } while (0)
+#else
+#define GT(k, lt) do { } while (0)
+#endif
+
 namespace adahop {
 namespace mxf4x2 {
 
@@ -133,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t buf = uint32_t(lt % BUFS);
       const uint32_t use = uint32_t(lt / BUFS);
       ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      GT(0, lt);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * G::kAccCols;
       for (int ks = 0; ks < nks; ++ks) {
@@ -166,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
       }
       ptx::tc_commit_2sm(&tfull[buf]);
+      GT(1, lt);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (8 warps per CTA)
@@ -183,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t buf = uint32_t(lt % BUFS);
       const uint32_t use = uint32_t(lt / BUFS);
       ptx::mbar_wait(&tfull[buf], use & 1);
+      if (warp == 4 && lane == 0) GT(2, lt);
       ptx::tc_fence_after();
       const int64_t m0 = mb * 256 + rank * 128 + q * 32;
       const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
@@ -193,30 +207,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tb0 = tmem_base + ((q * 32) << 16) + buf * G::kAccCols + half * (BN / 2);
         uint32_t w0[32], w1[32];
         {
-          uint32_t r0[32], r1[32];
+          // all four loads in flight before the single wait: the drain time gates the next tile
+          uint32_t r0[32], r1[32], r2[32], r3[32];
           ptx::tmem_ld_32x32b_x32(tb0, r0);
           ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
+          ptx::tmem_ld_32x32b_x32(tb0 + 64, r2);
+          ptx::tmem_ld_32x32b_x32(tb0 + 96, r3);
           ptx::tmem_ld_wait();
+          // accumulator is in registers: hand it back to the MMA warp before packing
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
+          if (warp == 4 && lane == 0) GT(3, lt);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             w0[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
             w0[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
+            w1[i] = pack_bf16x2(r2[2 * i], r2[2 * i + 1]);
+            w1[16 + i] = pack_bf16x2(r3[2 * i], r3[2 * i + 1]);
           }
         }
-        {
-          uint32_t r0[32], r1[32];
-          ptx::tmem_ld_32x32b_x32(tb0 + 64, r0);
-          ptx::tmem_ld_32x32b_x32(tb0 + 96, r1);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            w1[i] = pack_bf16x2(r0[2 * i], r0[2 * i + 1]);
-            w1[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
 #pragma unroll 1
         for (int g = 0; g < 2; ++g) {
           epi_stage_row128(stg, g == 0 ? w0 : w1);
@@ -230,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
         __syncwarp();
+        if (warp == 4 && lane == 0) GT(4, lt);
         continue;
       }
 #pragma unroll 1
@@ -272,6 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<512>(tmem_base);
   }
+#if GEMM_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_gt[0][0];
+    for (int i = 0; i < 64 && cluster + i * nclusters < ntiles; ++i)
+      printf("gemm tile %2d: mma-start %7lld mma-issued %7lld epi-wake %7lld drained %7lld stored %7lld\n", i,
+             g_gt[0][i] - t0, g_gt[1][i] - t0, g_gt[2][i] - t0, g_gt[3][i] - t0, g_gt[4][i] - t0);
+  }
+#endif
 }
 
 }  // namespace mxf4x2

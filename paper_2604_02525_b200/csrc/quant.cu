@@ -1081,7 +1081,6 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_const
   extern __shared__ __align__(16) unsigned long long ckey[];   // [kTopkMaxCand] keys, then indices
   int* cidx = reinterpret_cast<int*>(ckey + kTopkMaxCand);
   __shared__ TopkSmem sm;
-  __shared__ unsigned long long fkey[256];
   __shared__ int fidx[256];
   const int jb = foid_job_of(B.sb_off, B.n, blockIdx.x);
   const FoidJobDev& J = B.j[jb];
@@ -1102,7 +1101,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_const
   const int nc1 = sm.nc;
 #endif
   if (nb == 1) {
-    if (tid < kk) { fkey[tid] = part_key[tid]; fidx[tid] = part_idx[tid]; }
+    if (tid < kk) fidx[tid] = part_idx[tid];
   } else {
     __threadfence();
     __syncthreads();
@@ -1145,7 +1144,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_const
       unsigned long long* tk = ka; ka = kb2; kb2 = tk;
       int* tx = xa; xa = xb; xb = tx;
     }
-    for (int t = tid; t < kk; t += kTopkThreads) { fkey[t] = ka[t]; fidx[t] = xa[t]; }
+    for (int t = tid; t < kk; t += kTopkThreads) fidx[t] = xa[t];
 #if FOID_TRACE
     if (tid == 0) printf("select b=%d: start %lld phaseL %lld (nc %d) merge-start %lld end %lld\n", b, t0 % 100000000, t1 - t0, nc1, t2 - t0, gtime() - t0);
 #endif

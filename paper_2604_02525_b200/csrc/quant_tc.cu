@@ -150,10 +150,28 @@ __device__ __forceinline__ void quant_block(const uint32_t (&d)[32], uint4& code
   codes = make_uint4(e2m1x8(v), e2m1x8(v + 8), e2m1x8(v + 16), e2m1x8(v + 24));
 }
 
+// Several tensors in one persistent launch: the global tile index runs over the tiles of job 0,
+// then job 1, ...; every role finds its tile's job by the prefix offsets.
+constexpr int kMaxJobs = 3;
+struct Job {
+  int64_t R, C;
+  int rtiles, tile0;
+  int64_t kch_row, kch_col;
+  Out orow, ocol;
+};
+struct Jobs {
+  CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs];
+  Job j[kMaxJobs];
+  int n, ntiles;
+};
+__device__ __forceinline__ int job_of(const Jobs& J, int tile) {
+  int jb = 0;
+  while (jb + 1 < J.n && tile >= J.j[jb + 1].tile0) ++jb;
+  return jb;
+}
+
 template <bool kRow, bool kCol, bool kHad>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_quant_tc(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_qrow,
-               const __grid_constant__ CUtensorMap tm_qcol, int64_t R, int64_t C, const Out orow, const Out ocol) {
+__global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant__ Jobs J) {
   extern __shared__ __align__(1024) uint8_t smem_q[];
   uint8_t* ring = smem_q + ((1024u - (ptx::smem_u32(smem_q) & 1023u)) & 1023u);
   uint8_t* stg = ring + kStages * kTile;   // codes [orientation][buffer][128 rows x 64 B], 64B-swizzled
@@ -166,20 +184,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* staged = tempty + 2;       // [2] epilogue warps -> store warp
   uint64_t* stgfree = staged + 2;      // [2] store warp -> epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stgfree + 2);
-  Mask* mrow = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
-  Mask* mcol = mrow + 1;
-
+  Mask* masks = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [job][row, col]
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int rtiles = int((R + 127) / 128), ctiles = int((C + 127) / 128);
-  const int ntiles = rtiles * ctiles;
-  const int64_t kch_row = sf_kchunks(C), kch_col = sf_kchunks(R);
+  const int ntiles = J.ntiles;
   constexpr int kEpiWarps = kEpiGroups * 4;
 
   // ---- setup: barriers, H_32, TMEM, OE masks
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tm);
-    if (kRow) ptx::prefetch_tmap(&tm_qrow);
-    if (kCol) ptx::prefetch_tmap(&tm_qcol);
+    for (int jb = 0; jb < J.n; ++jb) {
+      ptx::prefetch_tmap(&J.tm[jb]);
+      if (kRow) ptx::prefetch_tmap(&J.tqr[jb]);
+      if (kCol) ptx::prefetch_tmap(&J.tqc[jb]);
+    }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 2);   // MMA commit + slice-copy warp
@@ -200,8 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __float2bfloat16_rn(neg ? -1.f : 1.f);
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
-  if (kRow && orow.nzero > 0) mask_build(mrow, orow.zero, orow.nzero, R);
-  if (kCol && ocol.nzero > 0) mask_build(mcol, ocol.zero, ocol.nzero, C);
+  for (int jb = 0; jb < J.n; ++jb) {
+    if (kRow && J.j[jb].orow.nzero > 0) mask_build(&masks[2 * jb], J.j[jb].orow.zero, J.j[jb].orow.nzero, J.j[jb].R);
+    if (kCol && J.j[jb].ocol.nzero > 0) mask_build(&masks[2 * jb + 1], J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
+  }
   ptx::fence_proxy_async();  // H written by threads, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
@@ -214,13 +232,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = first; tile < ntiles; tile += stride) {
-      const int rt = tile % rtiles, ct = tile / rtiles;
+      const int jb = job_of(J, tile);
+      const int lt0 = tile - J.j[jb].tile0, rtiles = J.j[jb].rtiles;
+      const int rt = lt0 % rtiles, ct = lt0 / rtiles;
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       QTC_T(0, (tile - first) / stride);
       uint8_t* dst = ring + stage * kTile;
       ptx::mbar_arrive_expect_tx(&full[stage], kTile);
-      ptx::tma_load_2d(dst, &tm, &full[stage], int32_t(ct * 128), int32_t(rt * 128));
-      ptx::tma_load_2d(dst + kBox, &tm, &full[stage], int32_t(ct * 128 + 64), int32_t(rt * 128));
+      ptx::tma_load_2d(dst, &J.tm[jb], &full[stage], int32_t(ct * 128), int32_t(rt * 128));
+      ptx::tma_load_2d(dst + kBox, &J.tm[jb], &full[stage], int32_t(ct * 128 + 64), int32_t(rt * 128));
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 1) {
@@ -271,7 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per orientation and tile, so the epilogue warps never stall on global-store issue.
     int lt = 0;
     for (int tile = first; tile < ntiles; tile += stride, ++lt) {
-      const int rt = tile % rtiles, ct = tile / rtiles;
+      const int jb = job_of(J, tile);
+      const Job& jj = J.j[jb];
+      const int lt0 = tile - jj.tile0;
+      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
       const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
       ptx::mbar_wait(&staged[buf], use & 1);
       if (ptx::elect_one()) {
@@ -284,9 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t srow0 = cs ? int64_t(ct) * 128 : int64_t(rt) * 128;
           const int kt = cs ? rt : ct;   // K-tile index: K-blocks [4 kt, 4 kt + 4)
           if (!(QTC_ABLATE & 4))
-            ptx::tma_store_2d(cs ? &tm_qcol : &tm_qrow, stg + (oi * 2 + buf) * kStg, kt * 64, int32_t(srow0));
+            ptx::tma_store_2d(cs ? &J.tqc[jb] : &J.tqr[jb], stg + (oi * 2 + buf) * kStg, kt * 64, int32_t(srow0));
           if (!(QTC_ABLATE & 8)) {
-            uint8_t* gsf = (cs ? ocol.sf : orow.sf) + ((srow0 >> 7) * (cs ? kch_col : kch_row) + kt) * 512;
+            uint8_t* gsf = (cs ? jj.ocol.sf : jj.orow.sf) + ((srow0 >> 7) * (cs ? jj.kch_col : jj.kch_row) + kt) * 512;
             ptx::bulk_store(gsf, sfstg + (oi * 2 + buf) * 512, 512);
           }
         }
@@ -303,7 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = first; tile < ntiles; tile += stride) {
-      const int rt = tile % rtiles, ct = tile / rtiles;
+      const int jb = job_of(J, tile);
+      const Job& jj = J.j[jb];
+      const int lt0 = tile - jj.tile0;
+      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
+      const int64_t R = jj.R, C = jj.C;
+      const Out& orow = jj.orow;
+      const Out& ocol = jj.ocol;
+      const Mask* mrow = &masks[2 * jb];
+      const Mask* mcol = &masks[2 * jb + 1];
       ptx::mbar_wait(&full[stage], phase);
       const uint8_t* tb = ring + stage * kTile;
       if (kRow && orow.nzero > 0 && orow.slice) {
@@ -362,17 +393,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sub = group % kGroupsPerOrient;
     const bool col_side = kRow ? (orient == 1) : true;
     const uint32_t q = warp & 3;
-    const Out& o = col_side ? ocol : orow;
-    const Mask* m = col_side ? mcol : mrow;
-    const int64_t K = col_side ? R : C;
-    const int64_t rows_total = col_side ? C : R;
     const uint32_t row = q * 32 + lane;        // stored row within the tile = TMEM lane
     const uint32_t blk0 = sub * kBlocksPerGroup;
     const uint32_t oi = kRow ? orient : 0;     // staging slot of this orientation
     const uint32_t sw = (row >> 1) & 3;        // 64B swizzle of the staging row
     int lt = 0;
     for (int tile = first; tile < ntiles; tile += stride, ++lt) {
-      const int rt = tile % rtiles, ct = tile / rtiles;
+      const int jb = job_of(J, tile);
+      const Job& jj = J.j[jb];
+      const int lt0 = tile - jj.tile0;
+      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
+      const Out& o = col_side ? jj.ocol : jj.orow;
+      const Mask* m = &masks[2 * jb + (col_side ? 1 : 0)];
+      const int64_t K = col_side ? jj.R : jj.C;
+      const int64_t rows_total = col_side ? jj.C : jj.R;
       const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
       uint8_t* st = stg + (oi * 2 + buf) * kStg;
       uint8_t* sst = sfstg + (oi * 2 + buf) * 512;
@@ -440,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t quant_tc_smem(bool masks) {
   return size_t(qtc::kStages) * qtc::kTile + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
-         (masks ? 2 * sizeof(qtc::Mask) : 0);
+         (masks ? 2 * qtc::kMaxJobs * sizeof(qtc::Mask) : 0);
 }
 
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask) {
@@ -449,8 +483,7 @@ bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool r
 }
 
 template <bool kRow, bool kCol, bool kHad>
-static cudaError_t launch_tc(const CUtensorMap& tm, const CUtensorMap& tqr, const CUtensorMap& tqc, int64_t R, int64_t C, const qtc::Out& orow, const qtc::Out& ocol,
-                             bool masks, int num_sms, cudaStream_t st) {
+static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaStream_t st) {
   const size_t smem = quant_tc_smem(masks);
   static bool attr = false;
   if (!attr) {
@@ -459,49 +492,74 @@ static cudaError_t launch_tc(const CUtensorMap& tm, const CUtensorMap& tqr, cons
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int64_t ntiles = ((R + 127) / 128) * ((C + 127) / 128);
-  const unsigned grid = unsigned(ntiles < num_sms ? ntiles : num_sms);
-  qtc::k_quant_tc<kRow, kCol, kHad><<<grid, qtc::kThreads, smem, st>>>(tm, tqr, tqc, R, C, orow, ocol);
+  const unsigned grid = unsigned(J.ntiles < num_sms ? J.ntiles : num_sms);
+  qtc::k_quant_tc<kRow, kCol, kHad><<<grid, qtc::kThreads, smem, st>>>(J);
   return cudaGetLastError();
 }
 
-// T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) when q_row != nullptr; column
-// outputs (stored rows = C, K = R) when q_col != nullptr. had_* (debug, nullable) receive the
-// fp32 Hadamard output of the respective orientation.
+// Each job: T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) and / or column
+// outputs (stored rows = C, K = R); all jobs of one launch produce the same orientations.
+// had_* (debug, nullable) receive the fp32 Hadamard output of the respective orientation.
+cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > qtc::kMaxJobs) return cudaErrorInvalidValue;
+  qtc::Jobs J;
+  memset(&J, 0, sizeof(J));
+  J.n = n;
+  const bool row = jobs[0].q_row != nullptr, col = jobs[0].q_col != nullptr;
+  const bool had = jobs[0].had_row != nullptr || jobs[0].had_col != nullptr;
+  bool masks = false;
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const QuantTcJob& q = jobs[i];
+    if ((q.q_row != nullptr) != row || (q.q_col != nullptr) != col ||
+        (q.had_row != nullptr || q.had_col != nullptr) != had)
+      return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&J.tm[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q.in, uint64_t(q.C), uint64_t(q.R),
+                      uint64_t(q.ld) * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    // code outputs, stored by TMA: [stored rows][K/2] bytes, 128 x 64-byte boxes, 64B swizzle
+    J.tqr[i] = J.tqc[i] = J.tm[i];
+    if (row && !make_tmap_2d(&J.tqr[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, q.q_row, uint64_t(q.C / 2), uint64_t(q.R),
+                             uint64_t(q.C / 2), 64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    if (col && !make_tmap_2d(&J.tqc[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, q.q_col, uint64_t(q.R / 2), uint64_t(q.C),
+                             uint64_t(q.R / 2), 64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    qtc::Job& jj = J.j[i];
+    jj.R = q.R; jj.C = q.C;
+    jj.rtiles = int((q.R + 127) / 128);
+    jj.tile0 = tiles;
+    tiles += jj.rtiles * int((q.C + 127) / 128);
+    jj.kch_row = sf_kchunks(q.C);
+    jj.kch_col = sf_kchunks(q.R);
+    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, q.slice_row, q.had_row};
+    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, q.slice_col, q.had_col};
+    masks |= (row && q.nrow_zero > 0) || (col && q.ncol_zero > 0);
+  }
+  J.ntiles = tiles;
+  if (row && col) {
+    if (had) return launch_tc<true, true, true>(J, masks, num_sms, st);
+    return launch_tc<true, true, false>(J, masks, num_sms, st);
+  }
+  if (row) {
+    if (had) return launch_tc<true, false, true>(J, masks, num_sms, st);
+    return launch_tc<true, false, false>(J, masks, num_sms, st);
+  }
+  if (col) {
+    if (had) return launch_tc<false, true, true>(J, masks, num_sms, st);
+    return launch_tc<false, true, false>(J, masks, num_sms, st);
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld, const int32_t* row_zero,
                             int nrow_zero, __nv_bfloat16* slice_row, uint8_t* q_row, uint8_t* sf_row, float* had_row,
                             const int32_t* col_zero, int ncol_zero, __nv_bfloat16* slice_col, uint8_t* q_col,
                             uint8_t* sf_col, float* had_col, int num_sms, cudaStream_t st) {
-  CUtensorMap tm;
-  if (!make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(C), uint64_t(R), uint64_t(ld) * 2, 64, 128,
-                    CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  const bool row = q_row != nullptr, col = q_col != nullptr;
-  // code outputs, stored by TMA: [stored rows][K/2] bytes, 128 x 64-byte boxes, 64B swizzle
-  CUtensorMap tqr = tm, tqc = tm;
-  if (row && !make_tmap_2d(&tqr, CU_TENSOR_MAP_DATA_TYPE_UINT8, q_row, uint64_t(C / 2), uint64_t(R), uint64_t(C / 2),
-                           64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
-    return cudaErrorInvalidValue;
-  if (col && !make_tmap_2d(&tqc, CU_TENSOR_MAP_DATA_TYPE_UINT8, q_col, uint64_t(R / 2), uint64_t(C), uint64_t(R / 2),
-                           64, 128, CU_TENSOR_MAP_SWIZZLE_64B))
-    return cudaErrorInvalidValue;
-  qtc::Out orow{q_row, sf_row, row_zero, row ? nrow_zero : 0, slice_row, had_row};
-  qtc::Out ocol{q_col, sf_col, col_zero, col ? ncol_zero : 0, slice_col, had_col};
-  const bool masks = (row && nrow_zero > 0) || (col && ncol_zero > 0);
-  const bool had = had_row != nullptr || had_col != nullptr;
-  if (row && col) {
-    if (had) return launch_tc<true, true, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-    return launch_tc<true, true, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-  }
-  if (row) {
-    if (had) return launch_tc<true, false, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-    return launch_tc<true, false, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-  }
-  if (col) {
-    if (had) return launch_tc<false, true, true>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-    return launch_tc<false, true, false>(tm, tqr, tqc, R, C, orow, ocol, masks, num_sms, st);
-  }
-  return cudaSuccess;
+  const QuantTcJob q{in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, had_row,
+                     col_zero, ncol_zero, slice_col, q_col, sf_col, had_col};
+  return launch_quant_tc_multi(&q, 1, num_sms, st);
 }
 
 }  // namespace adahop
