@@ -394,10 +394,11 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
   ADAHOP_LAUNCH(launch_iht_quant(A, false, M, K, lda, a_kstrided, oe_left ? idx : nullptr,
                                  oe_left ? g.kk : 0, qa, qa_sf, nullptr, oe_left ? slice : nullptr,
                                  false, dev.sms, cs));
+  launches += quant_last_launches();
   ADAHOP_LAUNCH(launch_iht_quant(B, false, N, K, ldb, b_kstrided, oe_right ? idx : nullptr,
                                  oe_right ? g.kk : 0, qb, qb_sf, nullptr, oe_right ? slice : nullptr,
                                  false, dev.sms, cs));
-  launches += 2;
+  launches += quant_last_launches();
   stage_mark(2, cs);
   // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
   Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K};
@@ -592,8 +593,9 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
   }
   if (n_tc) {
-    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, dev.sms, cs));
-    launches += 1;
+    int nl = 0;
+    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, dev.sms, cs, &nl));
+    launches += nl;
   }
   for (int t = 0; t < 3; ++t) {
     if (in_tc[t]) continue;
@@ -609,17 +611,17 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     if (L.need_row[t] && L.need_col[t] && dual_quant_supported(R, C, rz != nullptr, cz != nullptr)) {
       ADAHOP_LAUNCH(launch_iht_quant_dual(src[t], R, C, C, rz, L.kk_row[t], srow, w + L.q_row[t], w + L.sf_row[t],
                                           cz, L.kk_col[t], scol, w + L.q_col[t], w + L.sf_col[t], dev.sms, cs));
-      launches += 1;
+      launches += quant_last_launches();
     } else {
       if (L.need_row[t]) {
         ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], w + L.q_row[t], w + L.sf_row[t],
                                        nullptr, srow, false, dev.sms, cs));
-        launches += 1;
+        launches += quant_last_launches();
       }
       if (L.need_col[t]) {
         ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], w + L.q_col[t], w + L.sf_col[t],
                                        nullptr, scol, false, dev.sms, cs));
-        launches += 1;
+        launches += quant_last_launches();
       }
     }
   }

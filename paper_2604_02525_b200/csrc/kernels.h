@@ -23,7 +23,8 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
                                   cudaStream_t st);
 bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask);
 // quant_tc.cu — Hadamard on the tensor cores, quantisation in the epilogue (bf16 sources).
-bool quant_use_tc();   // ADAHOP_QUANT_IMPL=scalar selects the butterfly kernels
+bool quant_use_tc();
+int quant_last_launches();   // kernels launched by the last launch_iht_quant / launch_iht_quant_dual   // ADAHOP_QUANT_IMPL=scalar selects the butterfly kernels
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask);
 struct QuantTcJob {
   const __nv_bfloat16* in; int64_t R, C, ld;
@@ -31,7 +32,8 @@ struct QuantTcJob {
   const int32_t* col_zero; int ncol_zero; __nv_bfloat16* slice_col; uint8_t* q_col; uint8_t* sf_col; float* had_col;
 };
 // Up to 3 tensors in one persistent launch (same orientation set for all).
-cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st);
+// OE slices are produced by a separate gather launch; *launches (nullable) counts every launch.
+cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st, int* launches);
 cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld, const int32_t* row_zero,
                             int nrow_zero, __nv_bfloat16* slice_row, uint8_t* q_row, uint8_t* sf_row, float* had_row,
                             const int32_t* col_zero, int ncol_zero, __nv_bfloat16* slice_col, uint8_t* q_col,

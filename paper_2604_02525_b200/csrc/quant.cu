@@ -621,14 +621,21 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_iht_quant_dual(const __grid
   }
 }
 
+thread_local int g_quant_launches = 0;
+int quant_last_launches() { return g_quant_launches; }
+
 cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld,
                                   const int32_t* row_zero, int nrow_zero, __nv_bfloat16* slice_row,
                                   uint8_t* q_row, uint8_t* sf_row, const int32_t* col_zero, int ncol_zero,
                                   __nv_bfloat16* slice_col, uint8_t* q_col, uint8_t* sf_col, int num_sms,
                                   cudaStream_t st) {
-  if (quant_use_tc() && quant_tc_supported(R, C, ld, in, nrow_zero > 0, ncol_zero > 0))
-    return launch_quant_tc(in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, nullptr, col_zero, ncol_zero,
-                           slice_col, q_col, sf_col, nullptr, num_sms, st);
+  g_quant_launches = 1;
+  if (quant_use_tc() && quant_tc_supported(R, C, ld, in, nrow_zero > 0, ncol_zero > 0)) {
+    const QuantTcJob q{in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, nullptr,
+                       col_zero, ncol_zero, slice_col, q_col, sf_col, nullptr};
+    g_quant_launches = 0;
+    return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+  }
   if ((ld * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0) return cudaErrorInvalidValue;
   CUtensorMap tm;
   if (!make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, uint64_t(C), uint64_t(R), uint64_t(ld) * 2, 64,
@@ -792,14 +799,21 @@ cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, 
                              int kstrided, const int32_t* zero_rows, int nzero, uint8_t* codes,
                              uint8_t* sf, float* had_out, __nv_bfloat16* slice, bool sw_cvt,
                              int num_sms, cudaStream_t st) {
+  g_quant_launches = 1;
   if (!in_f32 && !sw_cvt && quant_use_tc()) {
     const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(in);
-    if (!kstrided && quant_tc_supported(R, K, ld, in, nzero > 0, false))   // T = [R][K], row orientation
-      return launch_quant_tc(src, R, K, ld, zero_rows, nzero, slice, codes, sf, had_out, nullptr, 0, nullptr,
-                             nullptr, nullptr, nullptr, num_sms, st);
-    if (kstrided && quant_tc_supported(K, R, ld, in, false, nzero > 0))     // T = [K][R], column orientation
-      return launch_quant_tc(src, K, R, ld, nullptr, 0, nullptr, nullptr, nullptr, nullptr, zero_rows, nzero, slice,
-                             codes, sf, had_out, num_sms, st);
+    if (!kstrided && quant_tc_supported(R, K, ld, in, nzero > 0, false)) {   // T = [R][K], row orientation
+      const QuantTcJob q{src, R, K, ld, zero_rows, nzero, slice, codes, sf, had_out,
+                         nullptr, 0, nullptr, nullptr, nullptr, nullptr};
+      g_quant_launches = 0;
+      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+    }
+    if (kstrided && quant_tc_supported(K, R, ld, in, false, nzero > 0)) {   // T = [K][R], column orientation
+      const QuantTcJob q{src, K, R, ld, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
+                         zero_rows, nzero, slice, codes, sf, had_out};
+      g_quant_launches = 0;
+      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+    }
   }
 #define ADAHOP_Q(T, H, S)                                                                   \
   return launch_quant_t<T, H, S>(static_cast<const T*>(in), R, K, ld, kstrided, zero_rows, \

@@ -153,9 +153,11 @@ __device__ __forceinline__ void quant_block(const uint32_t (&d)[32], uint4& code
 // Several tensors in one persistent launch: the global tile index runs over the tiles of job 0,
 // then job 1, ...; every role finds its tile's job by the prefix offsets.
 constexpr int kMaxJobs = 3;
+// Tiles run along the rows of T first (ct fastest): concurrent CTAs stream whole row bands,
+// so the bf16 reads are long contiguous runs.
 struct Job {
   int64_t R, C;
-  int rtiles, tile0;
+  int ctiles, tile0;
   int64_t kch_row, kch_col;
   Out orow, ocol;
 };
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 2);   // MMA commit + slice-copy warp
+      ptx::mbar_init(&empty[s], 1);   // MMA commit
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
@@ -233,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     uint32_t phase = 0;
     for (int tile = first; tile < ntiles; tile += stride) {
       const int jb = job_of(J, tile);
-      const int lt0 = tile - J.j[jb].tile0, rtiles = J.j[jb].rtiles;
-      const int rt = lt0 % rtiles, ct = lt0 / rtiles;
+      const int lt0 = tile - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
+      const int rt = lt0 / ctiles, ct = lt0 % ctiles;
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       QTC_T(0, (tile - first) / stride);
       uint8_t* dst = ring + stage * kTile;
@@ -292,9 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     int lt = 0;
     for (int tile = first; tile < ntiles; tile += stride, ++lt) {
       const int jb = job_of(J, tile);
-      const Job& jj = J.j[jb];
+      const Job jj = J.j[jb];   // by value: one param-space read per tile
       const int lt0 = tile - jj.tile0;
-      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
+      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
       const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
       ptx::mbar_wait(&staged[buf], use & 1);
       if (ptx::elect_one()) {
@@ -321,65 +323,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
     if (ptx::elect_one()) ptx::bulk_wait_group<0>();
     __syncwarp();
-  } else if (warp == 3) {
-    // ------------------------------------------------------------ OE slice copies
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int tile = first; tile < ntiles; tile += stride) {
-      const int jb = job_of(J, tile);
-      const Job& jj = J.j[jb];
-      const int lt0 = tile - jj.tile0;
-      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
-      const int64_t R = jj.R, C = jj.C;
-      const Out& orow = jj.orow;
-      const Out& ocol = jj.ocol;
-      const Mask* mrow = &masks[2 * jb];
-      const Mask* mcol = &masks[2 * jb + 1];
-      ptx::mbar_wait(&full[stage], phase);
-      const uint8_t* tb = ring + stage * kTile;
-      if (kRow && orow.nzero > 0 && orow.slice) {
-        // extracted rows of this tile: 128 raw values each -> slice_row[slot][c0 ..]
-        for (int r0 = 0; r0 < 128; r0 += 32) {
-          uint32_t hits = __ballot_sync(~0u, rt * 128 + r0 + lane < R && mask_hit(mrow, rt * 128 + r0 + lane));
-          while (hits) {
-          const int rr = r0 + __ffs(hits) - 1;
-          hits &= hits - 1;
-          const int64_t r = rt * 128 + rr;
-          const int slot = mask_slot(mrow, orow.nzero, r);
-          // lane l copies 16-byte chunk (l & 7) of box (l >> 3) [16 chunks per row]
-          if (lane < 16) {
-            const int bx = lane >> 3, j = lane & 7;
-            const int64_t col = ct * 128 + bx * 64 + j * 8;
-            if (col < C) {
-              const uint4 v = *reinterpret_cast<const uint4*>(tb + bx * kBox + rr * 128 + ((j ^ (rr & 7)) << 4));
-              *reinterpret_cast<uint4*>(orow.slice + int64_t(slot) * C + col) = v;
-            }
-          }
-          }
-        }
-      }
-      if (kCol && ocol.nzero > 0 && ocol.slice) {
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t hits = __ballot_sync(~0u, ct * 128 + c0 + lane < C && mask_hit(mcol, ct * 128 + c0 + lane));
-          while (hits) {
-          const int cc = c0 + __ffs(hits) - 1;
-          hits &= hits - 1;
-          const int64_t c = ct * 128 + cc;
-          const int slot = mask_slot(mcol, ocol.nzero, c);
-          const int bx = cc >> 6, cb = (cc & 63) * 2;
-          for (int rr = lane; rr < 128; rr += 32) {
-            const int64_t r = rt * 128 + rr;
-            if (r < R)
-              ocol.slice[int64_t(slot) * R + r] = *reinterpret_cast<const __nv_bfloat16*>(
-                  tb + bx * kBox + rr * 128 + ((((cb >> 4) ^ (rr & 7)) << 4) | (cb & 15)));
-          }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[stage]);
-      if (++stage == kStages) { stage = 0; phase ^= 1; }
-    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     // Dual launch: groups 0,1 -> row blocks {0,1},{2,3}; groups 2,3 -> column blocks {0,1},{2,3}.
@@ -400,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     int lt = 0;
     for (int tile = first; tile < ntiles; tile += stride, ++lt) {
       const int jb = job_of(J, tile);
-      const Job& jj = J.j[jb];
+      const Job jj = J.j[jb];   // by value: one param-space read per tile
       const int lt0 = tile - jj.tile0;
-      const int rt = lt0 % jj.rtiles, ct = lt0 / jj.rtiles;
+      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
       const Out& o = col_side ? jj.ocol : jj.orow;
       const Mask* m = &masks[2 * jb + (col_side ? 1 : 0)];
       const int64_t K = col_side ? jj.R : jj.C;
@@ -500,8 +443,60 @@ static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaSt
 // Each job: T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) and / or column
 // outputs (stored rows = C, K = R); all jobs of one launch produce the same orientations.
 // had_* (debug, nullable) receive the fp32 Hadamard output of the respective orientation.
-cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st) {
+// OE slices (the extracted rows / columns, raw bf16) for the BF16 outlier GEMM:
+//   orient 0: out[s][c] = T[idx[s], c]  (c < C)      orient 1: out[s][r] = T[r, idx[s]]  (r < R)
+// Column gathers: a block covers 32 rows; lane = row (coalesced 64-byte writes per slice row).
+__global__ void __launch_bounds__(256) k_oe_gather(const __nv_bfloat16* __restrict__ T, int64_t R, int64_t C,
+                                                   int64_t ld, int orient, const int32_t* __restrict__ idx, int n,
+                                                   __nv_bfloat16* __restrict__ out) {
+  if (orient == 0) {
+    // block (s, chunk): 256 threads x 8 elements
+    const int s = blockIdx.y;
+    const int64_t c = (int64_t(blockIdx.x) * 256 + threadIdx.x) * 8;
+    if (s >= n || c >= C) return;
+    const __nv_bfloat16* src = T + int64_t(idx[s]) * ld + c;
+    __nv_bfloat16* dst = out + int64_t(s) * C + c;
+    if (c + 8 <= C && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
+    } else {
+      for (int i = 0; i < 8 && c + i < C; ++i) dst[i] = src[i];
+    }
+  } else {
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;   // 8 warps: slots wy, wy + 8, ...
+    const int64_t r = int64_t(blockIdx.x) * 32 + lane;
+    if (r >= R) return;
+    for (int s = wy; s < n; s += 8) out[int64_t(s) * R + r] = T[r * ld + idx[s]];
+  }
+}
+
+static cudaError_t launch_oe_gather(const __nv_bfloat16* T, int64_t R, int64_t C, int64_t ld, int orient,
+                                    const int32_t* idx, int n, __nv_bfloat16* out, cudaStream_t st) {
+  if (n <= 0 || out == nullptr) return cudaSuccess;
+  if (orient == 0) {
+    const dim3 grid(unsigned((C + 2047) / 2048), unsigned(n));
+    k_oe_gather<<<grid, 256, 0, st>>>(T, R, C, ld, 0, idx, n, out);
+  } else {
+    k_oe_gather<<<unsigned((R + 31) / 32), 256, 0, st>>>(T, R, C, ld, 1, idx, n, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st, int* launches) {
   if (n <= 0) return cudaSuccess;
+  // the OE slices come from a separate gather (copying them inside the quant pipeline stalls it)
+  for (int i = 0; i < n; ++i) {
+    const QuantTcJob& q = jobs[i];
+    if (q.q_row && q.nrow_zero > 0 && q.slice_row) {
+      cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 0, q.row_zero, q.nrow_zero, q.slice_row, st);
+      if (e != cudaSuccess) return e;
+      if (launches) ++*launches;
+    }
+    if (q.q_col && q.ncol_zero > 0 && q.slice_col) {
+      cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 1, q.col_zero, q.ncol_zero, q.slice_col, st);
+      if (e != cudaSuccess) return e;
+      if (launches) ++*launches;
+    }
+  }
   if (n > qtc::kMaxJobs) return cudaErrorInvalidValue;
   qtc::Jobs J;
   memset(&J, 0, sizeof(J));
@@ -528,16 +523,17 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cu
       return cudaErrorInvalidValue;
     qtc::Job& jj = J.j[i];
     jj.R = q.R; jj.C = q.C;
-    jj.rtiles = int((q.R + 127) / 128);
+    jj.ctiles = int((q.C + 127) / 128);
     jj.tile0 = tiles;
-    tiles += jj.rtiles * int((q.C + 127) / 128);
+    tiles += jj.ctiles * int((q.R + 127) / 128);
     jj.kch_row = sf_kchunks(q.C);
     jj.kch_col = sf_kchunks(q.R);
-    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, q.slice_row, q.had_row};
-    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, q.slice_col, q.had_col};
+    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, nullptr, q.had_row};
+    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, nullptr, q.had_col};
     masks |= (row && q.nrow_zero > 0) || (col && q.ncol_zero > 0);
   }
   J.ntiles = tiles;
+  if (launches) ++*launches;
   if (row && col) {
     if (had) return launch_tc<true, true, true>(J, masks, num_sms, st);
     return launch_tc<true, true, false>(J, masks, num_sms, st);
@@ -559,7 +555,7 @@ cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64
                             uint8_t* sf_col, float* had_col, int num_sms, cudaStream_t st) {
   const QuantTcJob q{in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, had_row,
                      col_zero, ncol_zero, slice_col, q_col, sf_col, had_col};
-  return launch_quant_tc_multi(&q, 1, num_sms, st);
+  return launch_quant_tc_multi(&q, 1, num_sms, st, nullptr);
 }
 
 }  // namespace adahop

@@ -97,13 +97,17 @@ def test_iht_quant_residual_mask(k_strided):
 
 
 @pytest.mark.parametrize("R,C,masks", [(256, 512, False), (384, 160, True), (2048, 1024, True),
-                                        (4096, 96, True)])
+                                        (4096, 96, True), (256, 384, "dense")])
 def test_quant_dual_equals_single_orientation(R, C, masks):
     # one pass over T emitting both layouts == the row quantisation of T and of T^T, bitwise,
-    # and both == the oracle quantiser on the Hadamard output (protocol (a))
+    # and both == the oracle quantiser on the Hadamard output (protocol (a)); "dense" puts more
+    # extracted rows + columns in one tile than the kernel's slice staging ring holds
     x, _ = synth.operand(R, C, "R", "X", case_id=R * 7 + C, bf16=True)
-    rz = sorted({0, 3, R // 2, R - 1}) if masks else None
-    cz = sorted({1, C // 3, C - 2}) if masks else None
+    if masks == "dense":
+        rz, cz = list(range(0, R, 2)), list(range(0, C, 3))
+    else:
+        rz = sorted({0, 3, R // 2, R - 1}) if masks else None
+        cz = sorted({1, C // 3, C - 2}) if masks else None
     t = dev_bf16(x)
     qr, sr, qc, sc, slr, slc = ah.debug_quant_dual(t, row_zero=rz, col_zero=cz, want_slices=True)
     codes_r, scales_r, had_r = ah.debug_iht_quant(t, zero_rows=rz, want_had=True)
