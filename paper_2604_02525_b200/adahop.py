@@ -310,9 +310,10 @@ def debug_e2m1_exhaustive(lo: int = 0, hi: int = 1 << 32, device=None):
 
 class StageEvents:
     """Five CUDA events recorded by the library between the hot-path stages of one call
-    (FOID | quant | MXFP4 GEMM | outlier GEMM + scatter), mirroring tab:latency."""
+    (FOID | quant | BF16 outlier GEMM | MXFP4 GEMM + fused outlier scatter), mirroring tab:latency
+    (P:451-473)."""
 
-    NAMES = ("foid", "quant", "gemm_mxf4", "outlier")
+    NAMES = ("foid", "quant", "outlier", "gemm_mxf4")
 
     def __init__(self):
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(5)]

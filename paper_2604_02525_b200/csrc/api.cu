@@ -119,7 +119,7 @@ struct GemmPlan {
   int64_t npad = 0;
   int splits = 1;
   size_t qa_codes = 0, qa_sf = 0, qb_codes = 0, qb_sf = 0;
-  size_t keys = 0, idx = 0, slice = 0, part = 0;
+  size_t keys = 0, idx = 0, slice = 0, part = 0, dt = 0;
   size_t total = 0;
 };
 
@@ -146,6 +146,7 @@ bool plan_gemm(int64_t M, int64_t N, int64_t K, adahop_strategy_t s, const adaho
     g->npad = bf16_gemm_npad(g->kk);
     g->splits = bf16_gemm_splits(g->mbig, K, num_sms);
     g->part = c.take(size_t(g->splits) * size_t(g->mbig) * size_t(g->npad) * 4);
+    g->dt = c.take(size_t(g->kk) * size_t(g->mbig) * 4);
   }
   g->total = c.take(0) + 256;
   return true;
@@ -400,12 +401,8 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
                                  false, dev.sms, cs));
   launches += quant_last_launches();
   stage_mark(2, cs);
-  // ---- 3. block-scaled MXFP4 GEMM (P:762 stage 3)
-  Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K};
-  ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
-  launches += 1;
-  stage_mark(3, cs);
-  // ---- 4. BF16 outlier GEMM + scatter-add into C (P:762-763 stages 3-4)
+  // ---- 3. BF16 outlier GEMM: split-K partials, written into C by the GEMM epilogue
+  OePatch patch{};
   if (g.kk > 0) {
     Bf16GemmArgs ga{};
     if (oe_right) {  // D[M x k] = A (M x K) . B_out^T
@@ -417,10 +414,17 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
     ga.Mb = g.mbig; ga.Nb = g.kk; ga.K = K; ga.mode = 1;
     ga.part = reinterpret_cast<float*>(w + g.part); ga.splits = g.splits; ga.npad = g.npad;
     ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
-    ADAHOP_LAUNCH(launch_outlier_reduce(ga.part, g.splits, g.mbig, g.npad, g.kk, idx, oe_right, C,
-                                        out_f32, ldc, cs));
+    float* Dt = reinterpret_cast<float*>(w + g.dt);
+    ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, g.kk, Dt, cs));
     launches += 2;
+    patch = OePatch{Dt, idx, ga.Mb, g.kk, oe_right ? 1 : 2};
   }
+  stage_mark(3, cs);
+  // ---- 4. block-scaled MXFP4 GEMM (P:762 stage 3); its epilogue writes the outlier entries
+  //         (fused scatter: the residual product is exactly zero there)
+  Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, C, out_f32, ldc, M, N, K, patch};
+  ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
+  launches += 1;
   stage_mark(4, cs);
   g_launches = launches;
   return ADAHOP_OK;
@@ -441,7 +445,8 @@ struct LayerPlan {
   // masks: which FOID feeds which (tensor, orientation)
   int kk_row[3], kk_col[3];
   size_t idx_row[3], idx_col[3], slice_row[3], slice_col[3];
-  size_t keys_row[3], keys_col[3], part = 0;   // per-FOID scratch
+  size_t keys_row[3], keys_col[3];   // per-FOID scratch
+  size_t part[3], dt[3];               // per-path outlier split-K partials and folded Dt
   int splits[3];
   int64_t npad[3], mbig[3];
   size_t total = 0;
@@ -488,7 +493,7 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
       L->keys_col[t] = c.take(foid_ws_bytes(C));
     }
   }
-  size_t part_bytes = 0;
+
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   for (int path = 0; path < 3; ++path) {
     L->splits[path] = 1; L->npad[path] = 0; L->mbig[path] = 0;
@@ -499,9 +504,9 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     L->mbig[path] = left ? MNK[path][1] : MNK[path][0];
     L->npad[path] = bf16_gemm_npad(kk);
     L->splits[path] = bf16_gemm_splits(L->mbig[path], MNK[path][2], sms);
-    part_bytes = std::max(part_bytes, size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4);
+    L->part[path] = c.take(size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4);
+    L->dt[path] = c.take(size_t(kk) * size_t(L->mbig[path]) * 4);
   }
-  if (part_bytes) L->part = c.take(part_bytes);
   L->total = c.take(0) + 256;
 }
 
@@ -626,7 +631,6 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     }
   }
   stage_mark(2, cs);
-  // ---- 3. the three MXFP4 GEMMs (or BF16 for Lv2 CC)
   void* out[3] = {Y, GX, GW};
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   const int64_t ldc[3] = {d_out, d_in, d_in};
@@ -637,6 +641,30 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
   const void* rawB[3] = {W, W, X};
   const int rawBks[3] = {0, 1, 1};
   const int64_t rawBld[3] = {d_in, d_in, d_in};
+  // ---- 3. BF16 outlier GEMMs: split-K partials, written into C by the MXFP4 GEMM epilogue
+  OePatch patch[3] = {};
+  for (int path = 0; path < 3; ++path) {
+    if (L.mbig[path] == 0) continue;
+    const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
+    const int t = left ? kPathA[path] : kPathB[path];
+    const bool col = left ? kPathAo[path] : kPathBo[path];
+    const int kk = col ? L.kk_col[t] : L.kk_row[t];
+    const int32_t* idx = reinterpret_cast<const int32_t*>(w + (col ? L.idx_col[t] : L.idx_row[t]));
+    const __nv_bfloat16* slice = reinterpret_cast<const __nv_bfloat16*>(w + (col ? L.slice_col[t] : L.slice_row[t]));
+    Bf16GemmArgs ga{};
+    if (!left) { ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path]; }
+    else { ga.A = static_cast<const __nv_bfloat16*>(rawB[path]); ga.a_mn = rawBks[path]; ga.lda = rawBld[path]; }
+    ga.B = slice; ga.b_mn = 0; ga.ldb = MNK[path][2];
+    ga.Mb = L.mbig[path]; ga.Nb = kk; ga.K = MNK[path][2]; ga.mode = 1;
+    ga.part = reinterpret_cast<float*>(w + L.part[path]); ga.splits = L.splits[path]; ga.npad = L.npad[path];
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    float* Dt = reinterpret_cast<float*>(w + L.dt[path]);
+    ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, kk, Dt, cs));
+    launches += 2;
+    patch[path] = OePatch{Dt, idx, ga.Mb, kk, left ? 2 : 1};
+  }
+  stage_mark(3, cs);
+  // ---- 4. the three MXFP4 GEMMs (or BF16 for Lv2 CC); the epilogue writes the outlier entries
   for (int path = 0; path < 3; ++path) {
     const int64_t M = MNK[path][0], N = MNK[path][1], K = MNK[path][2];
     if (s[path] == ADAHOP_BF16) {
@@ -653,30 +681,9 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     const uint8_t* qa_sf = w + (kPathAo[path] ? L.sf_col[ta] : L.sf_row[ta]);
     const uint8_t* qb = w + (kPathBo[path] ? L.q_col[tb] : L.q_row[tb]);
     const uint8_t* qb_sf = w + (kPathBo[path] ? L.sf_col[tb] : L.sf_row[tb]);
-    Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], out_f32, ldc[path], M, N, K};
+    Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], out_f32, ldc[path], M, N, K, patch[path]};
     ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
     launches += 1;
-  }
-  stage_mark(3, cs);
-  // ---- 4. BF16 outlier GEMMs + scatter into the outputs (disjoint support)
-  for (int path = 0; path < 3; ++path) {
-    if (L.mbig[path] == 0) continue;
-    const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
-    const int t = left ? kPathA[path] : kPathB[path];
-    const bool col = left ? kPathAo[path] : kPathBo[path];
-    const int kk = col ? L.kk_col[t] : L.kk_row[t];
-    const int32_t* idx = reinterpret_cast<const int32_t*>(w + (col ? L.idx_col[t] : L.idx_row[t]));
-    const __nv_bfloat16* slice = reinterpret_cast<const __nv_bfloat16*>(w + (col ? L.slice_col[t] : L.slice_row[t]));
-    Bf16GemmArgs ga{};
-    if (!left) { ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path]; }
-    else { ga.A = static_cast<const __nv_bfloat16*>(rawB[path]); ga.a_mn = rawBks[path]; ga.lda = rawBld[path]; }
-    ga.B = slice; ga.b_mn = 0; ga.ldb = MNK[path][2];
-    ga.Mb = L.mbig[path]; ga.Nb = kk; ga.K = MNK[path][2]; ga.mode = 1;
-    ga.part = reinterpret_cast<float*>(w + L.part); ga.splits = L.splits[path]; ga.npad = L.npad[path];
-    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
-    ADAHOP_LAUNCH(launch_outlier_reduce(ga.part, ga.splits, ga.Mb, ga.npad, kk, idx, !left, out[path], out_f32,
-                                        ldc[path], cs));
-    launches += 2;
   }
   stage_mark(4, cs);
   g_launches = launches;

@@ -90,4 +90,75 @@ __device__ __forceinline__ void epi_store_rows128(uint8_t* stg, const uint32_t (
   __syncwarp();
 }
 
+// OE outlier values written into C by the MXFP4 GEMM epilogue ("Fused Scatter-Add"):
+// the residual operand has the OE rows (OE-Left) / columns (OE-Right) zeroed, so the main
+// product is exactly 0 there and those entries of C are the BF16 outlier product alone:
+//   OE-Right (mode 1): C[m][idx[j]] = Dt[j][m]       OE-Left (mode 2): C[idx[j]][n] = Dt[j][n]
+// with Dt the split-K-folded, transposed outlier product (launch_outlier_fold).
+struct OePatch {
+  const float* Dt;         // [k][Mb]
+  const int32_t* idx;      // sorted, k entries
+  int64_t Mb;
+  int k, mode;             // mode 0: none
+};
+
+// [j0, j1) = the entries of sorted idx in [lo, hi): one pass of the warp over idx (k <= 256)
+__device__ __forceinline__ void idx_range(const int32_t* __restrict__ idx, int k, int64_t lo, int64_t hi, int& j0,
+                                          int& j1) {
+  const int lane = threadIdx.x & 31;
+  int below = 0, inside = 0;
+  for (int b = 0; b < k; b += 32) {
+    const int64_t v = b + lane < k ? int64_t(__ldg(idx + b + lane)) : hi;
+    below += __popc(__ballot_sync(~0u, v < lo));
+    inside += __popc(__ballot_sync(~0u, v >= lo && v < hi));
+  }
+  j0 = below;
+  j1 = below + inside;
+}
+
+// Patch the staged 32-row block (rows m0 .. m0+31, columns n0 .. n0+ncols-1) of C in the warp's
+// smem stage; call between staging and flushing (whole warp).
+__device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& op, int64_t m0, int64_t n0,
+                                                   int ncols, int elt, int64_t M, int64_t N) {
+  if (op.mode == 0) return;
+  const int lane = threadIdx.x & 31;
+  int j0, j1;
+  if (op.mode == 1) idx_range(op.idx, op.k, n0, n0 + ncols, j0, j1);
+  else idx_range(op.idx, op.k, m0, m0 + 32, j0, j1);
+  if (j0 == j1) return;
+  __syncwarp();
+  if (op.mode == 1) {   // columns idx[j] in [n0, n0 + ncols): lane = row
+    const int64_t m = m0 + lane;
+    if (m < M)
+      for (int j = j0; j < j1; ++j) {
+        const int cl = int(__ldg(op.idx + j) - n0);
+        const float v = __ldg(op.Dt + int64_t(j) * op.Mb + m);
+        uint8_t* dst = stg + lane * kEpiPitch + cl * elt;
+        if (elt == 4) *reinterpret_cast<float*>(dst) = v;
+        else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
+      }
+  } else {              // rows idx[j] in [m0, m0 + 32): lane = column
+    for (int j = j0; j < j1; ++j) {
+      const int rl = int(__ldg(op.idx + j) - m0);
+      for (int c = lane; c < ncols; c += 32) {
+        const int64_t n = n0 + c;
+        if (n >= N) continue;
+        const float v = __ldg(op.Dt + int64_t(j) * op.Mb + n);
+        uint8_t* dst = stg + rl * kEpiPitch + c * elt;
+        if (elt == 4) *reinterpret_cast<float*>(dst) = v;
+        else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void epi_stage_only128(uint8_t* stg, const uint32_t (&w)[32]) {
+  const int lane = threadIdx.x & 31;
+  uint4* srow = reinterpret_cast<uint4*>(stg + lane * kEpiPitch);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) srow[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  __syncwarp();
+}
+
 }  // namespace adahop

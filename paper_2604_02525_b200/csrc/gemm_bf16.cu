@@ -197,23 +197,21 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Deterministic split-K fold + scatter into C, through a 32 x 32 smem tile so that both
-// the partial reads (along j) and the OE-Left row writes (along m) are coalesced.
-__global__ void __launch_bounds__(1024) k_outlier_reduce(const float* __restrict__ part, int splits,
-                                                        int64_t Mb, int64_t npad, int k,
-                                                        const int32_t* __restrict__ idx,
-                                                        int scatter_cols, void* C, int out_f32,
-                                                        int64_t ldc) {
+// Deterministic split-K fold into the transposed outlier product Dt[j][m] = sum_s part[s][m][j]
+// (fixed order s = 0, 1, ...), through a 32 x 32 smem tile so that both the partial reads
+// (along j) and the Dt writes (along m) are coalesced. The MXFP4 GEMM epilogue then reads Dt
+// with lanes along m (OE-Right) or along n (OE-Left): coalesced in both cases.
+__global__ void __launch_bounds__(1024) k_outlier_fold(const float* __restrict__ part, int splits, int64_t Mb,
+                                                      int64_t npad, int k, float* __restrict__ Dt) {
   __shared__ float tile[32][33];
   const int64_t m0 = int64_t(blockIdx.x) * 32;
   const int j0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int mm = ty; mm < 32; mm += blockDim.y) {
-    const int64_t m = m0 + mm;
+  {
+    const int64_t m = m0 + ty;
     const int j = j0 + tx;
     float v = 0.f;
     if (m < Mb && j < k) {
-      // fixed summation order s = 0, 1, 2, ... (deterministic); loads batched 8 at a time
       const float* pp = part + m * npad + j;
       const int64_t stride = Mb * npad;
       int s = 0;
@@ -226,28 +224,12 @@ __global__ void __launch_bounds__(1024) k_outlier_reduce(const float* __restrict
       }
       for (; s < splits; ++s) v += pp[s * stride];
     }
-    tile[mm][tx] = v;
+    tile[ty][tx] = v;
   }
   __syncthreads();
-  if (scatter_cols) {  // OE-Right: C[m][idx[j]]
-    for (int mm = ty; mm < 32; mm += blockDim.y) {
-      const int64_t m = m0 + mm;
-      const int j = j0 + tx;
-      if (m >= Mb || j >= k) continue;
-      const int64_t off = m * ldc + idx[j];
-      if (out_f32) static_cast<float*>(C)[off] = tile[mm][tx];
-      else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(tile[mm][tx]);
-    }
-  } else {             // OE-Left (transposed product): C[idx[j]][m]
-    for (int jj = ty; jj < 32; jj += blockDim.y) {
-      const int j = j0 + jj;
-      const int64_t m = m0 + tx;
-      if (m >= Mb || j >= k) continue;
-      const int64_t off = int64_t(idx[j]) * ldc + m;
-      if (out_f32) static_cast<float*>(C)[off] = tile[tx][jj];
-      else static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(tile[tx][jj]);
-    }
-  }
+  const int j = j0 + ty;
+  const int64_t m = m0 + tx;
+  if (m < Mb && j < k) Dt[int64_t(j) * Mb + m] = tile[tx][ty];
 }
 
 }  // namespace bf16g
@@ -320,12 +302,10 @@ cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st) {
   }
 }
 
-cudaError_t launch_outlier_reduce(const float* part, int splits, int64_t Mb, int64_t npad, int k,
-                                  const int32_t* idx, bool scatter_cols, void* C, bool out_f32,
-                                  int64_t ldc, cudaStream_t st) {
+cudaError_t launch_outlier_fold(const float* part, int splits, int64_t Mb, int64_t npad, int k, float* Dt,
+                                cudaStream_t st) {
   dim3 grid(unsigned((Mb + 31) / 32), unsigned((k + 31) / 32));
-  bf16g::k_outlier_reduce<<<grid, dim3(32, 32), 0, st>>>(part, splits, Mb, npad, k, idx, scatter_cols ? 1 : 0,
-                                                C, out_f32 ? 1 : 0, ldc);
+  bf16g::k_outlier_fold<<<grid, dim3(32, 32), 0, st>>>(part, splits, Mb, npad, k, Dt);
   return cudaGetLastError();
 }
 

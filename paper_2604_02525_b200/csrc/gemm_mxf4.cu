@@ -65,7 +65,7 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                 const uint8_t* __restrict__ sfa, const uint8_t* __restrict__ sfb, void* C,
-                int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
+                int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* epi_smem = smem + size_t(kStages) * kStageBytes;
@@ -205,9 +205,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t nrem = N - n0;
         const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
-        if (rows_valid > 0 && bytes_valid > 0)
-          epi_store_rows128(stg, w, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid,
-                            bytes_valid, elt, vec_ok);
+        if (rows_valid > 0 && bytes_valid > 0) {
+          epi_stage_only128(stg, w);
+          epi_patch_outliers(stg, oe, m0, n0, cols_per_grp, elt, M, N);
+          epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid, bytes_valid, elt,
+                       vec_ok);
+          __syncwarp();
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -244,7 +248,7 @@ cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st
   const int64_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int grid = int(tiles < num_sms ? tiles : num_sms);
   k_gemm_mxf4<<<grid, kThreads, kSmemBytes, st>>>(tma, tmb, a.a_sf, a.b_sf, a.C, a.out_f32 ? 1 : 0,
-                                                  a.ldc, a.M, a.N, a.K);
+                                                  a.ldc, a.M, a.N, a.K, a.oe);
   return cudaGetLastError();
 }
 

@@ -70,7 +70,7 @@ template <int BN, int BUFS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
-                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K) {
+                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe) {
   using G = Cfg<BN, BUFS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           epi_stage_row128(stg, g == 0 ? w0 : w1);
           __syncwarp();
           const int64_t n0 = nb * BN + half * (BN / 2) + g * 64;
+          epi_patch_outliers(stg, oe, m0, n0, 64, 2, M, N);
           const int64_t nrem = N - n0;
           const int bytes_valid = int(nrem >= 64 ? 128 : (nrem > 0 ? nrem * 2 : 0));
           if (rows_valid > 0 && bytes_valid > 0)
@@ -271,9 +272,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t nrem = N - n0;
         const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
-        if (rows_valid > 0 && bytes_valid > 0)
-          epi_store_rows128(stg, w, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid,
-                            bytes_valid, elt, vec_ok);
+        if (rows_valid > 0 && bytes_valid > 0) {
+          epi_stage_only128(stg, w);
+          epi_patch_outliers(stg, oe, m0, n0, cols_per_grp, elt, M, N);
+          epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid, bytes_valid, elt,
+                       vec_ok);
+          __syncwarp();
+        }
       }
     }
   }
@@ -335,7 +340,7 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>, tma, tmb, tsfa, tsfb, a.C,
-                            a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K);
+                            a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
 
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st) {

@@ -1,5 +1,6 @@
 // kernels.h — host-side launchers of the AdaHOP sm_100a kernels (internal to libadahop).
 #pragma once
+#include "epilogue.cuh"
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -76,6 +77,7 @@ struct Mxf4GemmArgs {
   void* C;
   bool out_f32;
   int64_t ldc, M, N, K;
+  OePatch oe;   // outlier entries written by the epilogue (oe.mode 0: none)
 };
 cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st);
 // gemm_mxf4_2sm.cu — CTA-pair (cta_group::2) version; variant = 128 (256x128 tiles, double-
@@ -110,9 +112,9 @@ cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st);
 // scatter_cols (OE-Right): C[m][idx[j]] = val;  else (OE-Left): C[idx[j]][m] = val.
 // The MXFP4 product is exactly 0 at those positions (disjoint support), so the store
 // equals the add.
-cudaError_t launch_outlier_reduce(const float* part, int splits, int64_t Mb, int64_t npad, int k,
-                                  const int32_t* idx, bool scatter_cols, void* C, bool out_f32,
-                                  int64_t ldc, cudaStream_t st);
+// Dt[j][m] = sum over the split-K partials (fixed order) of the outlier product D[m][j].
+cudaError_t launch_outlier_fold(const float* part, int splits, int64_t Mb, int64_t npad, int k, float* Dt,
+                                cudaStream_t st);
 
 // tensor maps (api.cu)
 bool make_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
