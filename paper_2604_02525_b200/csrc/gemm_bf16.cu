@@ -20,7 +20,7 @@ namespace bf16g {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // bf16 elements per stage (128 bytes along K)
-constexpr int kStages = 4;
+constexpr int kStagesMax = 4;
 constexpr int kThreads = 128;
 
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n, int a_mn, int b_mn) {
@@ -39,6 +39,9 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  // skinny outlier tiles (BN <= 64): 3 stages so that two CTAs share an SM (the split-K grid is
+  // sized for two per SM); wider tiles: 4 stages, one CTA per SM
+  static constexpr int kStages = BN <= 64 ? 3 : kStagesMax;
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 4 * kEpiStageBytes + 1024 + 256;
 };
 
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(kThreads)
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
+  constexpr int kStages = G::kStages;
   uint8_t* epi_smem = smem + size_t(kStages) * G::kStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + 4 * kEpiStageBytes);
   uint64_t* full = bars;
