@@ -19,6 +19,11 @@
 #ifndef GEMM_TRACE
 #define GEMM_TRACE 0
 #endif
+// Experiment knob (never set in the product build): bit 0 skips the scale-factor tcgen05.cp,
+// bit 1 the MMAs, bit 2 the scale-factor TMA loads, bit 3 the epilogue stores.
+#ifndef GEMM_ABLATE
+#define GEMM_ABLATE 0
+#endif
 #if GEMM_TRACE
 #include <cstdio>
 __device__ long long g_gt[6][64];
@@ -46,6 +51,7 @@ struct Cfg {
   static constexpr int kAccCols = BN;
   static constexpr int kSfaCol = 256;                 // after the accumulator buffers
   static constexpr int kSfbCol = 264;
+  static constexpr int kSfSet = 32;                   // second scale-factor column set
   static constexpr size_t kSmem = size_t(kStages) * kStage + kEpiWarps * kEpiBufs * kEpiStageBytes + 1024 + 512;
   static_assert(BUFS * BN <= 256, "accumulators must fit below the scale-factor columns");
 };
@@ -126,15 +132,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* ssfa = sb + G::kB;
         uint8_t* ssfb = ssfa + G::kSfa;
         const uint32_t fb = ptx::mapa(&full[stage], 0);
-        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * G::kStage);
+        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (GEMM_ABLATE & 4) ? 2 * (G::kA + G::kB) : 2 * G::kStage);
         ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + rank * 128));
         ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + rank * (BN / 2)));
-        ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + rank));
-        ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
+        if (!(GEMM_ABLATE & 4)) {
+          ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + rank));
+          ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
+        }
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
+  } else if (warp == 1 && leader) {
+    // whole warp: waits and descriptor math stay warp-uniform (uniform registers); one elected
+    // lane issues the tcgen05 operations
     // ------------------------------------------------------------ MMA issuer (leader)
     constexpr uint32_t idesc = make_idesc(256, BN);
     int stage = 0;
@@ -150,34 +160,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ks = 0; ks < nks; ++ks) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
+        const bool issuer = ptx::elect_one();
         uint8_t* sa = smem + size_t(stage) * G::kStage;
         uint8_t* sb = sa + G::kA;
         uint8_t* ssfa = sb + G::kB;
         uint8_t* ssfb = ssfa + G::kSfa;
+        // scale factors alternate between two TMEM column sets by k-step parity, so the copies
+        // for step ks+1 do not overwrite columns the MMAs of step ks still read
+        const uint32_t sfo = uint32_t(ks & 1) * G::kSfSet;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfaCol + 4 * c,
+          if ((GEMM_ABLATE & 1) || !issuer) break;
+          ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfaCol + sfo + 4 * c,
                                           ptx::make_sdesc(ptx::smem_u32(ssfa + c * 512), 0, 128, 0));
 #pragma unroll
           for (int g = 0; g < BN / 128; ++g)
-            ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfbCol + (BN / 32) * c + 4 * g,
+            ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfbCol + sfo + (BN / 32) * c + 4 * g,
                                             ptx::make_sdesc(ptx::smem_u32(ssfb + g * 1024 + c * 512), 0, 128, 0));
         }
         const uint32_t a_addr = ptx::smem_u32(sa), b_addr = ptx::smem_u32(sb);
 #pragma unroll
         for (int j = 0; j < BK / 64; ++j) {
           const uint32_t sf_id = uint32_t(j & 1) * 2;
-          const uint32_t sfa_t = (tmem_base + G::kSfaCol + 4 * (j >> 1)) | (sf_id << 30);
-          const uint32_t sfb_t = (tmem_base + G::kSfbCol + (BN / 32) * (j >> 1)) | (sf_id << 30);
+          const uint32_t sfa_t = (tmem_base + G::kSfaCol + sfo + 4 * (j >> 1)) | (sf_id << 30);
+          const uint32_t sfb_t = (tmem_base + G::kSfbCol + sfo + (BN / 32) * (j >> 1)) | (sf_id << 30);
           const uint32_t id = idesc | (sf_id << 4) | (sf_id << 29);
+          if ((GEMM_ABLATE & 2) || !issuer) continue;
           ptx::mma_mxf4_2sm(d_tmem, ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2),
                             ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2), id, sfa_t, sfb_t,
                             (ks > 0 || j > 0) ? 1u : 0u);
         }
-        ptx::tc_commit_2sm(&empty[stage]);
+        if (issuer) ptx::tc_commit_2sm(&empty[stage]);
+        __syncwarp();
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
       }
-      ptx::tc_commit_2sm(&tfull[buf]);
+      if (ptx::elect_one()) ptx::tc_commit_2sm(&tfull[buf]);
+      __syncwarp();
       GT(1, lt);
     }
   } else if (warp >= 4) {
@@ -235,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           epi_patch_outliers(stg, oe, m0, n0, 64, 2, M, N);
           const int64_t nrem = N - n0;
           const int bytes_valid = int(nrem >= 64 ? 128 : (nrem > 0 ? nrem * 2 : 0));
-          if (rows_valid > 0 && bytes_valid > 0)
+          if (rows_valid > 0 && bytes_valid > 0 && !(GEMM_ABLATE & 8))
             epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * 2, ldc * 2, rows_valid, bytes_valid, 2,
                          vec_ok);
           __syncwarp();
