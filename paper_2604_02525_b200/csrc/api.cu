@@ -163,6 +163,14 @@ adahop_status_t validate_params(const adahop_params_t* p) {
 
 }  // namespace
 
+// ============================================================================ PDL switch
+namespace adahop {
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("ADAHOP_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+}  // namespace adahop
+
 // ============================================================================ tensor maps
 namespace adahop {
 bool make_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,

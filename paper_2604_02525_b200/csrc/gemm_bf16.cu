@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kThreads)
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<G::kTmemCols>(tmem_slot);
+  ptx::griddep_launch();
+  ptx::griddep_wait();   // the prologue above overlapped the previous kernel's tail
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -207,6 +209,8 @@ __global__ void __launch_bounds__(kThreads)
 // with lanes along m (OE-Right) or along n (OE-Left): coalesced in both cases.
 __global__ void __launch_bounds__(1024) k_outlier_fold(const float* __restrict__ part, int splits, int64_t Mb,
                                                       int64_t npad, int k, float* __restrict__ Dt) {
+  ptx::griddep_launch();
+  ptx::griddep_wait();
   __shared__ float tile[32][33];
   const int64_t m0 = int64_t(blockIdx.x) * 32;
   const int j0 = blockIdx.y * 32;
@@ -289,10 +293,8 @@ static cudaError_t launch_bn(const Bf16GemmArgs& a, cudaStream_t st) {
   const int splits = a.mode == 1 ? a.splits : 1;
   dim3 grid(unsigned((a.Mb + bf16g::BM - 1) / bf16g::BM),
             unsigned(a.mode == 1 ? 1 : (a.Nb + BN - 1) / BN), unsigned(splits));
-  bf16g::k_gemm_bf16<BN><<<grid, bf16g::kThreads, G::kSmem, st>>>(
-      tma, tmb, a.a_mn, a.b_mn, a.Mb, a.Nb, a.K, a.mode, a.C, a.out_f32 ? 1 : 0, a.ldc, a.part,
-      a.npad);
-  return cudaGetLastError();
+  return launch_k(bf16g::k_gemm_bf16<BN>, grid, dim3(bf16g::kThreads), G::kSmem, st, 1, tma, tmb, a.a_mn, a.b_mn,
+                  a.Mb, a.Nb, a.K, a.mode, a.C, a.out_f32 ? 1 : 0, a.ldc, a.part, a.npad);
 }
 
 cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st) {
@@ -309,8 +311,7 @@ cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st) {
 cudaError_t launch_outlier_fold(const float* part, int splits, int64_t Mb, int64_t npad, int k, float* Dt,
                                 cudaStream_t st) {
   dim3 grid(unsigned((Mb + 31) / 32), unsigned((k + 31) / 32));
-  bf16g::k_outlier_fold<<<grid, dim3(32, 32), 0, st>>>(part, splits, Mb, npad, k, Dt);
-  return cudaGetLastError();
+  return launch_k(bf16g::k_outlier_fold, grid, dim3(32, 32), 0, st, 1, part, splits, Mb, npad, k, Dt);
 }
 
 }  // namespace adahop

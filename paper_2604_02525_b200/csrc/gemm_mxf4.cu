@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::griddep_launch();
+  ptx::griddep_wait();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -247,9 +249,8 @@ cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st
   }
   const int64_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int grid = int(tiles < num_sms ? tiles : num_sms);
-  k_gemm_mxf4<<<grid, kThreads, kSmemBytes, st>>>(tma, tmb, a.a_sf, a.b_sf, a.C, a.out_f32 ? 1 : 0,
-                                                  a.ldc, a.M, a.N, a.K, a.oe);
-  return cudaGetLastError();
+  return launch_k(k_gemm_mxf4, dim3(grid), dim3(kThreads), kSmemBytes, st, 1, tma, tmb, a.a_sf, a.b_sf, a.C,
+                  a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
 
 }  // namespace adahop

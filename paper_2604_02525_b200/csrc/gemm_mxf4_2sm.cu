@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
+  ptx::griddep_launch();
+  ptx::griddep_wait();   // the prologue above overlapped the previous kernel's tail
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -345,20 +347,8 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   }
   const int64_t tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
   const int64_t clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(2 * clusters));
-  cfg.blockDim = dim3(mxf4x2::kThreads);
-  cfg.dynamicSmemBytes = G::kSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = 2;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>, tma, tmb, tsfa, tsfb, a.C,
-                            a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
+  return launch_k(mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>, dim3(unsigned(2 * clusters)), dim3(mxf4x2::kThreads), G::kSmem,
+                  st, 2, tma, tmb, tsfa, tsfb, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
 
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st) {

@@ -967,6 +967,8 @@ __device__ __forceinline__ unsigned* foid_counter(const FoidJobDev& J) {
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_foid_keys_batch(const __grid_constant__ FoidBatchDev B) {
+  ptx::griddep_launch();
+  ptx::griddep_wait();
   const int jb = foid_job_of(B.kb_off, B.n, blockIdx.x);
   const FoidJobDev& J = B.j[jb];
   const int bid = blockIdx.x - B.kb_off[jb];
@@ -1089,6 +1091,8 @@ __device__ void topk_core(const unsigned long long* __restrict__ src_key, const 
 __device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 #endif
 __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_constant__ FoidBatchDev B) {
+  ptx::griddep_launch();
+  ptx::griddep_wait();
 #if FOID_TRACE
   const long long t0 = gtime();
 #endif
@@ -1192,8 +1196,9 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
     B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
     B.sb_off[i + 1] = B.sb_off[i] + int((J.R + kTopkThreads - 1) / kTopkThreads);
   }
-  if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
-  else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
+  cudaError_t e0 = in_f32 ? launch_k(k_foid_keys_batch<float>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B)
+                          : launch_k(k_foid_keys_batch<__nv_bfloat16>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B);
+  if (e0 != cudaSuccess) return e0;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1201,8 +1206,7 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_foid_select<<<B.sb_off[n], kTopkThreads, kTopkMaxCand * 12, st>>>(B);
-  return cudaGetLastError();
+  return launch_k(k_foid_select, dim3(B.sb_off[n]), dim3(kTopkThreads), size_t(kTopkMaxCand) * 12, st, 1, B);
 }
 
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,

@@ -218,6 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         __float2bfloat16_rn(neg ? -1.f : 1.f);
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::griddep_launch();
+  ptx::griddep_wait();   // the prologue above overlapped the previous kernel's tail
   for (int jb = 0; jb < J.n; ++jb) {
     if (kRow && J.j[jb].orow.nzero > 0) mask_build(&masks[2 * jb], J.j[jb].orow.zero, J.j[jb].orow.nzero, J.j[jb].R);
     if (kCol && J.j[jb].ocol.nzero > 0) mask_build(&masks[2 * jb + 1], J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
@@ -436,8 +438,7 @@ static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaSt
     attr = true;
   }
   const unsigned grid = unsigned(J.ntiles < num_sms ? J.ntiles : num_sms);
-  qtc::k_quant_tc<kRow, kCol, kHad><<<grid, qtc::kThreads, smem, st>>>(J);
-  return cudaGetLastError();
+  return launch_k(qtc::k_quant_tc<kRow, kCol, kHad>, dim3(grid), dim3(qtc::kThreads), smem, st, 1, J);
 }
 
 // Each job: T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) and / or column
@@ -449,6 +450,8 @@ static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaSt
 __global__ void __launch_bounds__(256) k_oe_gather(const __nv_bfloat16* __restrict__ T, int64_t R, int64_t C,
                                                    int64_t ld, int orient, const int32_t* __restrict__ idx, int n,
                                                    __nv_bfloat16* __restrict__ out) {
+  ptx::griddep_launch();
+  ptx::griddep_wait();
   if (orient == 0) {
     // block (s, chunk): 256 threads x 8 elements
     const int s = blockIdx.y;
@@ -474,11 +477,9 @@ static cudaError_t launch_oe_gather(const __nv_bfloat16* T, int64_t R, int64_t C
   if (n <= 0 || out == nullptr) return cudaSuccess;
   if (orient == 0) {
     const dim3 grid(unsigned((C + 2047) / 2048), unsigned(n));
-    k_oe_gather<<<grid, 256, 0, st>>>(T, R, C, ld, 0, idx, n, out);
-  } else {
-    k_oe_gather<<<unsigned((R + 31) / 32), 256, 0, st>>>(T, R, C, ld, 1, idx, n, out);
+    return launch_k(k_oe_gather, grid, dim3(256), 0, st, 1, T, R, C, ld, 0, idx, n, out);
   }
-  return cudaGetLastError();
+  return launch_k(k_oe_gather, dim3(unsigned((R + 31) / 32)), dim3(256), 0, st, 1, T, R, C, ld, 1, idx, n, out);
 }
 
 cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st, int* launches) {
