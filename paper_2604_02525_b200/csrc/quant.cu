@@ -1196,9 +1196,8 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
     B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
     B.sb_off[i + 1] = B.sb_off[i] + int((J.R + kTopkThreads - 1) / kTopkThreads);
   }
-  cudaError_t e0 = in_f32 ? launch_k(k_foid_keys_batch<float>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B)
-                          : launch_k(k_foid_keys_batch<__nv_bfloat16>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B);
-  if (e0 != cudaSuccess) return e0;
+  if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
+  else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1206,7 +1205,9 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(k_foid_select, dim3(B.sb_off[n]), dim3(kTopkThreads), size_t(kTopkMaxCand) * 12, st, 1, B);
+  // (the FOID kernels are launched without PDL: early-resident select CTAs measured slower)
+  k_foid_select<<<B.sb_off[n], kTopkThreads, size_t(kTopkMaxCand) * 12, st>>>(B);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
