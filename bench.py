@@ -435,14 +435,45 @@ def main():
         h2d = sum(t.numel() * t.element_size() for d in host_in.values() for t in d.values())
         d2h = sum(t.numel() * t.element_size() for d in host_out.values() for t in d.values())
 
+        # three-stage pipeline over the layer's linears: the host->device copy of linear i+1
+        # (copy engine, stream s_in) and the device->host copy of linear i-1 (stream s_out) run
+        # under the AdaHOP calls of linear i (current stream); events order each linear's stages
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        names = list(lin)
+
         def step_e2e():
-            for k, L in lin.items():
-                for n in ("x", "w", "gy"):
-                    L[n].copy_(host_in[k][n], non_blocking=True)
-            step_adahop()
-            for k, L in lin.items():
-                for n in ("y", "gx", "gw"):
-                    host_out[k][n].copy_(L[n], non_blocking=True)
+            cur = torch.cuda.current_stream()
+            s_in.wait_stream(cur)
+            s_out.wait_stream(cur)
+            ev_in = []
+            for k in names:
+                with torch.cuda.stream(s_in):
+                    for n in ("x", "w", "gy"):
+                        lin[k][n].copy_(host_in[k][n], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(s_in)
+                ev_in.append(e)
+            for i, k in enumerate(names):
+                L = lin[k]
+                cur.wait_event(ev_in[i])
+                if args.per_path:
+                    sf, sd, sw = strat3[k]
+                    ah.linear_fwd(L["x"], L["w"], sf, params, out=L["y"], ws=ws)
+                    ah.linear_dgrad(L["gy"], L["w"], sd, params, out=L["gx"], ws=ws)
+                    ah.linear_wgrad(L["gy"], L["x"], sw, params, out=L["gw"], ws=ws)
+                else:
+                    ah.linear_layer(L["x"], L["w"], L["gy"], strat3[k], params, out=(L["y"], L["gx"], L["gw"]),
+                                    ws=ws)
+                if world > 1:
+                    ahd.allreduce_wgrad(L["gw"])
+                e = torch.cuda.Event()
+                e.record(cur)
+                s_out.wait_event(e)
+                with torch.cuda.stream(s_out):
+                    for n in ("y", "gx", "gw"):
+                        host_out[k][n].copy_(L[n], non_blocking=True)
+            cur.wait_stream(s_out)
+            cur.wait_stream(s_in)
 
         ms_e2e, _ = timed(step_e2e, args.e2e_steps, 1)
         e2e = {"value": flops_step * world / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
@@ -451,7 +482,7 @@ def main():
     # ---- roofline of the dominant kernel
     peaks = load_peaks()
     dom = max(stage_tot, key=stage_tot.get)
-    roof = roofline(dom, gemms, stage_tot, peaks, T, model, per_path=args.per_path)
+    roof = roofline(dom, gemms, stage_tot, peaks, T, model, per_path=args.per_path, workload=args.workload)
 
     # ---- CPU oracle baseline (rank 0, bounded sample)
     cpu = None
@@ -486,15 +517,39 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False):
-    """Achieved = algorithmic work of the dominant stage per step / its measured time."""
-    fp4_peak = peaks["bf16_sustained"] * 4.0            # nominal fp4/bf16 dense ratio 9/2.25
+def profiled_traffic(workload, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, averaged over the
+    launches of one step, from the committed ncu capture (profiles/traffic.json, written by
+    scripts/ncu_summary.py traffic); None when no capture of this workload exists."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[workload][kernel]
+        return {"bytes_per_launch": e["bytes_per_launch"], "algorithmic_bytes_per_launch": e.get("algorithmic"),
+                "source": e["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False, workload=None):
+    """Achieved = algorithmic work of the dominant stage per step / its measured time (CUDA events
+    recorded by the library around the stage on the launching stream) = the launch-weighted
+    average of work per launch / duration per launch."""
+    # the GEMM runs at max SM clock inside the step (clocks in the bench line), so its peak is the
+    # BURST bf16 figure x 4 (nominal dense fp4 / bf16 = 9 / 2.25); sustained x 4 given beside it
+    fp4_peak = peaks["bf16"] * 4.0
     if dom == "gemm_mxf4":
         work = sum(g["flops"] for g in gemms if g["strategy"] != "BF16")
         ach = work / (stage_tot[dom] * 1e-3) / 1e12
-        return {"kernel": "k_gemm_mxf4 (tcgen05 kind::mxf4)", "bound": "tensor", "achieved": ach,
-                "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak, "traffic": None,
-                "peak_src": f"{peaks['src']} bf16 sustained x 4 (nominal fp4/bf16)"}
+        n = sum(1 for g in gemms if g["strategy"] != "BF16")
+        tr = profiled_traffic(workload, "k_gemm_mxf4_2sm")
+        return {"kernel": "k_gemm_mxf4_2sm (tcgen05 kind::mxf4, cta_group::2)", "bound": "tensor", "achieved": ach,
+                "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak,
+                "traffic": tr["bytes_per_launch"] if tr else None, "traffic_detail": tr,
+                "launches_per_step": n, "flop_per_launch": work / n,
+                "peak_src": f"{peaks['src']} bf16 burst {peaks['bf16']} TF/s x 4 (nominal fp4/bf16); "
+                            f"vs sustained x 4 ({peaks['bf16_sustained'] * 4:.0f}): {ach / (peaks['bf16_sustained'] * 4):.3f}"}
     if dom == "quant":
         if per_path:
             # 2 B in + 0.5 B codes + 1/32 B scale per element of both operands of every GEMM
@@ -506,8 +561,10 @@ def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False):
                 for n_el in (T * d_in, d_out * d_in, T * d_out):
                     by += n_el * (2 + 2 * (0.5 + 1 / 32))
         ach = by / (stage_tot[dom] * 1e-3) / 1e9
-        return {"kernel": "k_iht_quant_row/col", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_src": peaks["src"]}
+        tr = profiled_traffic(workload, "k_quant_tc")
+        return {"kernel": "k_quant_tc", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_detail": tr, "peak_src": peaks["src"]}
     if dom == "outlier":
         by = 0.0
         for g in gemms:
@@ -516,7 +573,7 @@ def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False):
             elif g["strategy"] == "OE_RIGHT_IHT":
                 by += g["M"] * g["K"] * 2
         ach = by / (stage_tot[dom] * 1e-3) / 1e9
-        return {"kernel": "k_gemm_bf16 (outlier) + k_outlier_reduce", "bound": "hbm", "achieved": ach,
+        return {"kernel": "k_gemm_bf16 (outlier) + k_outlier_fold", "bound": "hbm", "achieved": ach,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
                 "peak_src": peaks["src"]}
     by = sum(g["M"] * 128 for g in gemms)   # FOID probe bytes (64 bf16 per row)

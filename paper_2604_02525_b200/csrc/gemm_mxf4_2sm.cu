@@ -72,7 +72,12 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t 
   nb = local / gm;
 }
 
-template <int BN, int BUFS>
+// PM x PN CTA pairs per cluster (cluster = 2 PM PN CTAs, rank = 2 (pm PN + pn) + x, x = the
+// CTA's half of the pair). A cluster computes a super tile of (256 PM) x (BN PN): the pairs in
+// one cluster row (same pm) read the same A rows and the pairs in one cluster column the same
+// B rows, so each CTA loads 1/PN of its A box and 1/PM of its B box and multicasts them to the
+// CTAs that share them — the L2->SM operand traffic per flop drops by (1/PN + 1/PM)/2 ... 1.
+template <int BN, int BUFS, int PM, int PN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
@@ -89,13 +94,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + BUFS);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  constexpr int NP = PM * PN, CS = 2 * NP;
   const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t x = rank & 1, pp = rank >> 1, pm = pp / PN, pn = pp % PN;
+  const bool leader = x == 0;
+  const uint32_t leader_rank = rank & ~1u;
   const int64_t mblocks = (M + 255) / 256;
   const int64_t nblocks = (N + BN - 1) / BN;
-  const int64_t ntiles = mblocks * nblocks;
+  const int64_t smblocks = (mblocks + PM - 1) / PM, snblocks = (nblocks + PN - 1) / PN;
+  const int64_t ntiles = smblocks * snblocks;
   const int nks = int((K + BK - 1) / BK);
-  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int64_t cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
+  // multicast groups: the CTAs with this x and pm (A rows) / this x and pn (B rows)
+  uint16_t mask_a = 0, mask_b = 0;
+#pragma unroll
+  for (int j = 0; j < PN; ++j) mask_a |= uint16_t(1u << (2 * (pm * PN + j) + x));
+#pragma unroll
+  for (int i = 0; i < PM; ++i) mask_b |= uint16_t(1u << (2 * (i * PN + pn) + x));
+  constexpr uint16_t mask_all = uint16_t((1u << CS) - 1);
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tm_a);
@@ -104,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tm_sfb);
     for (int s = 0; s < G::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], NP);   // one commit per pair of the cluster
     }
     for (int b = 0; b < BUFS; ++b) {
       ptx::mbar_init(&tfull[b], 1);
@@ -125,20 +141,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = cluster; tile < ntiles; tile += nclusters) {
-      int64_t mb, nb;
-      tile_coords(tile, mblocks, nblocks, mb, nb);
+      int64_t smb, snb;
+      tile_coords(tile, smblocks, snblocks, smb, snb);
+      // blocks past the edge of a ragged super tile are computed on clamped (valid) data
+      // and never stored: every pair must still take part in the multicasts and commits
+      const int64_t mb = min(smb * PM + pm, mblocks - 1), nb = min(snb * PN + pn, nblocks - 1);
       for (int ks = 0; ks < nks; ++ks) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + size_t(stage) * G::kStage;
         uint8_t* sb = sa + G::kA;
         uint8_t* ssfa = sb + G::kB;
         uint8_t* ssfb = ssfa + G::kSfa;
-        const uint32_t fb = ptx::mapa(&full[stage], 0);
+        const uint32_t fb = ptx::mapa(&full[stage], leader_rank);
         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (GEMM_ABLATE & 4) ? 2 * (G::kA + G::kB) : 2 * G::kStage);
-        ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + rank * 128));
-        ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + rank * (BN / 2)));
+        if (PN == 1) {
+          ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + x * 128));
+        } else {
+          constexpr int sub = 128 / PN;
+          ptx::tma_load_2d_2sm_mc(sa + pn * sub * 128, &tm_a, &full[stage], ks * (BK / 2),
+                                  int32_t(mb * 256 + x * 128 + pn * sub), mask_a);
+        }
+        if (PM == 1) {
+          ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + x * (BN / 2)));
+        } else {
+          constexpr int sub = (BN / 2) / PM;
+          ptx::tma_load_2d_2sm_mc(sb + pm * sub * 128, &tm_b, &full[stage], ks * (BK / 2),
+                                  int32_t(nb * BN + x * (BN / 2) + pm * sub), mask_b);
+        }
         if (!(GEMM_ABLATE & 4)) {
-          ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + rank));
+          ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + x));
           ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
         }
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
@@ -192,11 +223,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2), id, sfa_t, sfb_t,
                             (ks > 0 || j > 0) ? 1u : 0u);
         }
-        if (issuer) ptx::tc_commit_2sm(&empty[stage]);
+        if (issuer) {
+          if (NP == 1) ptx::tc_commit_2sm(&empty[stage]);
+          else ptx::tc_commit_2sm_mask(&empty[stage], mask_all);   // every CTA fed by this pair's loads
+        }
         __syncwarp();
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
       }
-      if (ptx::elect_one()) ptx::tc_commit_2sm(&tfull[buf]);
+      if (ptx::elect_one()) ptx::tc_commit_2sm_mask(&tfull[buf], uint16_t(3u << leader_rank));
       __syncwarp();
       GT(1, lt);
     }
@@ -208,17 +242,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int elt = out_f32 ? 4 : 2;
     const int cols_per_grp = 128 / elt;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
-    const uint32_t empty_leader = ptx::mapa(&tempty[0], 0);
+    const uint32_t empty_leader = ptx::mapa(&tempty[0], leader_rank);
     int64_t lt = 0;
     for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
-      int64_t mb, nb;
-      tile_coords(tile, mblocks, nblocks, mb, nb);
+      int64_t smb, snb;
+      tile_coords(tile, smblocks, snblocks, smb, snb);
+      const int64_t mb = smb * PM + pm, nb = snb * PN + pn;   // past the edge: rows/cols invalid, no stores
       const uint32_t buf = uint32_t(lt % BUFS);
       const uint32_t use = uint32_t(lt / BUFS);
       ptx::mbar_wait(&tfull[buf], use & 1);
       if (warp == 4 && lane == 0) GT(2, lt);
       ptx::tc_fence_after();
-      const int64_t m0 = mb * 256 + rank * 128 + q * 32;
+      const int64_t m0 = mb * 256 + x * 128 + q * 32;
       const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
       if (BUFS == 1 && !out_f32) {
         // bf16 single accumulator: read both column groups out of TMEM (one through the smem
@@ -320,16 +355,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace mxf4x2
 
-template <int BN, int BUFS>
+template <int BN, int BUFS, int PM, int PN>
 static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st) {
   using G = mxf4x2::Cfg<BN, BUFS>;
+  constexpr int CS = 2 * PM * PN;
+  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN>;
   CUtensorMap tma, tmb, tsfa, tsfb;
   const int64_t kch = sf_kchunks(a.K);
   if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
-                    uint64_t(a.K / 2), 128, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+                    uint64_t(a.K / 2), 128, 128 / PN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
-                    uint64_t(a.K / 2), 128, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B))
+                    uint64_t(a.K / 2), 128, (BN / 2) / PM, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   // scale factors as uint32 rows of one 128-row group: [groups][kch * 128] u32
   if (!make_tmap_2d(&tsfa, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.a_sf, uint64_t(kch * 128), uint64_t((a.M + 127) / 128),
@@ -338,22 +375,55 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   if (!make_tmap_2d(&tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
                     uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+  // resident clusters of this shape (GPC packing decides it for clusters of 4 and 8)
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (CS > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(CS * (num_sms / CS)));
+    cfg.blockDim = dim3(mxf4x2::kThreads);
+    cfg.dynamicSmemBytes = G::kSmem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = unsigned(CS);
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    if (e != cudaSuccess || n <= 0) n = num_sms / CS;
+    max_clusters = n;
   }
-  const int64_t tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
-  const int64_t clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_k(mxf4x2::k_gemm_mxf4_2sm<BN, BUFS>, dim3(unsigned(2 * clusters)), dim3(mxf4x2::kThreads), G::kSmem,
-                  st, 2, tma, tmb, tsfa, tsfb, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
+  const int64_t tiles = ((a.M + 256 * PM - 1) / (256 * PM)) * ((a.N + BN * PN - 1) / (BN * PN));
+  const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
+                  tsfb, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
+}
+
+// ADAHOP_GEMM_CLUSTER = pairs per cluster as PMxPN: 1 (1x1, default), 2 (1x2), 4 (1x4), 22 (2x2)
+static int cluster_shape() {
+  static int v = [] {
+    const char* e = getenv("ADAHOP_GEMM_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st) {
-  if (variant == 256) return launch_2sm<256, 1>(a, num_sms, st);
-  return launch_2sm<128, 2>(a, num_sms, st);
+  if (variant != 256) return launch_2sm<128, 2, 1, 1>(a, num_sms, st);
+  switch (cluster_shape()) {
+    case 2: return launch_2sm<256, 1, 1, 2>(a, num_sms, st);
+    case 4: return launch_2sm<256, 1, 1, 4>(a, num_sms, st);
+    case 21: return launch_2sm<256, 1, 2, 1>(a, num_sms, st);
+    case 22: return launch_2sm<256, 1, 2, 2>(a, num_sms, st);
+    default: return launch_2sm<256, 1, 1, 1>(a, num_sms, st);
+  }
 }
 
 }  // namespace adahop
