@@ -401,6 +401,14 @@ def main():
     launches[0] = 0
     step_adahop(stage_ev)
     launches_per_step = launches[0]
+    # value: the step as a user runs it (no stage events between the kernels: event nodes would
+    # break the programmatic-dependent-launch edges of the graph)
+    run_plain = as_graph(lambda: step_adahop())
+    sampler = ClockSampler(local)
+    ms_ada, clocks = timed(run_plain, args.steps, args.warmup, None, sampler)
+    value = flops_step * world / (ms_ada * 1e-3) / 1e12
+
+    # stage breakdown + roofline: the same step replayed with the library's stage events
     run_ada = as_graph(lambda: step_adahop(stage_ev))
     acc = [{n: 0.0 for n in ah.StageEvents.NAMES} for _ in units]
 
@@ -409,9 +417,7 @@ def main():
             for n, v in stage_ev[gi].times_ms().items():
                 acc[gi][n] += v / args.steps
 
-    sampler = ClockSampler(local)
-    ms_ada, clocks = timed(run_ada, args.steps, args.warmup, collect, sampler)
-    value = flops_step * world / (ms_ada * 1e-3) / 1e12
+    ms_instr, _ = timed(run_ada, args.steps, args.warmup, collect)
 
     # per-stage breakdown (tab:latency analogue), summed over the step
     stage_tot = {n: 0.0 for n in ah.StageEvents.NAMES}
@@ -420,6 +426,25 @@ def main():
         for n in acc[gi]:
             stage_tot[n] += acc[gi][n]
         per_unit.append(dict(g, **{k: round(v, 4) for k, v in acc[gi].items()}))
+
+    # ---- calibration pass (a1, config 5): one stats + classify step over the layer's 21 tensors
+    #      (X, W, G_Y of every linear), timed like the step; 2 B read per element is the work
+    cal_t = [L[n] for L in lin.values() for n in ("x", "w", "gy")]
+    cal_ws = torch.empty(max(ah.calibrate_workspace_bytes(*t.shape) for t in cal_t), dtype=torch.uint8, device=dev)
+    cal_cv = torch.empty((len(cal_t), 2), dtype=torch.float64, device=dev)
+    cal_pat = torch.empty(len(cal_t), dtype=torch.uint8, device=dev)
+
+    def step_calib():
+        for i, t in enumerate(cal_t):
+            ah.calibrate_async(t, cal_ws, cal_cv[i], cal_pat[i:i + 1], params)
+
+    step_calib()
+    ms_cal, _ = timed(as_graph(step_calib), args.steps, args.warmup)
+    cal_bytes = sum(t.numel() * 2 for t in cal_t)
+    calib = {"ms_per_calibration_step": ms_cal, "tensors": len(cal_t), "bytes_read": cal_bytes,
+             "GB_per_s": cal_bytes / (ms_cal * 1e-3) / 1e9,
+             "frac_of_hbm": cal_bytes / (ms_cal * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
+             "patterns": "".join("NRC"[int(v)] for v in cal_pat.cpu().tolist())}
 
     # ---- cuBLAS BF16 baseline (same GEMMs, same flush protocol)
     ms_cub = None
@@ -506,6 +531,8 @@ def main():
                 "cublas_bf16": {"value": flops_step * world / (ms_cub * 1e-3) / 1e12, "ms_per_step": ms_cub}
                 if ms_cub else None,
                 "stages_ms_per_step": {k: round(v, 4) for k, v in stage_tot.items()},
+                "ms_per_step_instrumented": ms_instr,
+                "calibration": calib,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches_per_step * args.steps),
                 "launch": "eager" if args.no_graph else "cuda_graph"}
@@ -544,6 +571,9 @@ def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False, worklo
         ach = work / (stage_tot[dom] * 1e-3) / 1e12
         n = sum(1 for g in gemms if g["strategy"] != "BF16")
         tr = profiled_traffic(workload, "k_gemm_mxf4_2sm")
+        if tr:   # FP4 codes + E8M0 scales of both operands in, bf16 C out
+            tr["algorithmic_bytes_per_launch"] = sum((g["M"] + g["N"]) * g["K"] * 17 / 32 + g["M"] * g["N"] * 2
+                                                     for g in gemms if g["strategy"] != "BF16") / n
         return {"kernel": "k_gemm_mxf4_2sm (tcgen05 kind::mxf4, cta_group::2)", "bound": "tensor", "achieved": ach,
                 "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak,
                 "traffic": tr["bytes_per_launch"] if tr else None, "traffic_detail": tr,
@@ -562,6 +592,8 @@ def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False, worklo
                     by += n_el * (2 + 2 * (0.5 + 1 / 32))
         ach = by / (stage_tot[dom] * 1e-3) / 1e9
         tr = profiled_traffic(workload, "k_quant_tc")
+        if tr:
+            tr["algorithmic_bytes_per_launch"] = by / len(model["linears"])
         return {"kernel": "k_quant_tc", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": tr["bytes_per_launch"] if tr else None,
                 "traffic_detail": tr, "peak_src": peaks["src"]}

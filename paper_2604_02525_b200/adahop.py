@@ -134,6 +134,21 @@ def calibrate(t: torch.Tensor, params: Params | None = None):
     return PAT_NAME[int(pat.item())], float(cvh[0]) / rows, float(cvh[1]) / cols
 
 
+def calibrate_async(t: torch.Tensor, ws: torch.Tensor, cv: torch.Tensor, pat: torch.Tensor,
+                    params: Params | None = None) -> None:
+    """adahop_calibrate without the host read-back (graph-capturable): cv (2 fp64) receives the
+    per-row / per-column CV sums and pat (1 uint8) the pattern code, both on the device.
+    ws must hold calibrate_workspace_bytes(rows, cols) bytes."""
+    p = params or Params()
+    rows, cols = t.shape
+    check("adahop_calibrate", lib.adahop_calibrate(_ptr(t), _dt(t), rows, cols, t.stride(0), C.byref(p),
+                                                   _ptr(ws), ws.numel(), _ptr(cv), _ptr(pat), _stream()))
+
+
+def calibrate_workspace_bytes(rows: int, cols: int) -> int:
+    return int(lib.adahop_calibrate_workspace_bytes(rows, cols))
+
+
 # ------------------------------------------------------------------------- hot path
 def gemm(a, a_kstrided: bool, b, b_kstrided: bool, M: int, N: int, K: int, strategy,
          params: Params | None = None, out: torch.Tensor | None = None,
