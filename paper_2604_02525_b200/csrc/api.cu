@@ -252,7 +252,7 @@ adahop_pattern_t adahop_classify_cv(double cv_row, double cv_col, const adahop_p
 // ------------------------------------------------------------------------ calibration
 size_t adahop_stats_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return 0;
-  return size_t(stats_chunks(rows)) * size_t(cols) * 32 + 256;
+  return stats_ws_bytes(rows, cols);
 }
 
 adahop_status_t adahop_stats(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
@@ -268,7 +268,7 @@ adahop_status_t adahop_stats(const void* T, adahop_dtype_t dt, int64_t rows, int
   g_launches = 0;
   ADAHOP_LAUNCH(launch_stats(T, dt == ADAHOP_DT_F32, rows, cols, ld, row_stats, col_stats,
                              static_cast<double*>(ws), reinterpret_cast<cudaStream_t>(stream)));
-  g_launches = 3;
+  g_launches = 2;
   return ADAHOP_OK;
 }
 
@@ -292,6 +292,7 @@ size_t adahop_calibrate_workspace_bytes(int64_t rows, int64_t cols) {
   c.take(size_t(rows) * 32);
   c.take(size_t(cols) * 32);
   c.take(adahop_stats_workspace_bytes(rows, cols));
+  c.take(calib_cvpart_bytes(rows, cols));
   return c.take(0) + 256;
 }
 
@@ -308,12 +309,15 @@ adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows,
   double* rs = reinterpret_cast<double*>(base + c.take(size_t(rows) * 32));
   double* cs = reinterpret_cast<double*>(base + c.take(size_t(cols) * 32));
   const size_t sw = adahop_stats_workspace_bytes(rows, cols);
-  void* sws = base + c.take(sw);
-  adahop_status_t st = adahop_stats(T, dt, rows, cols, ld, rs, cs, sws, sw, stream);
+  double* sws = reinterpret_cast<double*>(base + c.take(sw));
+  double* cvpart = reinterpret_cast<double*>(base + c.take(calib_cvpart_bytes(rows, cols)));
+  if (dt != ADAHOP_DT_BF16 && dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_device(nullptr);
   if (st != ADAHOP_OK) return st;
-  st = adahop_classify(rs, rows, cs, cols, rows, p, d_cv, d_pattern, stream);
-  g_launches = 4;
-  return st;
+  ADAHOP_LAUNCH(launch_calibrate(T, dt == ADAHOP_DT_F32, rows, cols, ld, rs, cs, sws, cvpart, double(p->eps),
+                                 double(p->tau), d_cv, d_pattern, reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 3;
+  return ADAHOP_OK;
 }
 
 // ------------------------------------------------------------------------ hot path

@@ -88,7 +88,12 @@ struct FoidJob {
   const void* in; int64_t R, K, ld; int kstrided, k, probe; double* scratch; int32_t* idx;
 };
 cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStream_t st);
-int64_t stats_chunks(int64_t R);
+size_t stats_ws_bytes(int64_t R, int64_t C);   // workspace of launch_stats (bytes)
+// one calibration step of one tensor: stats, CV partials, classification (3 launches)
+size_t calib_cvpart_bytes(int64_t R, int64_t C);
+cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld, double* rs, double* cs,
+                             double* part, double* cvpart, double eps, double tau, double* d_cv, uint8_t* pattern,
+                             cudaStream_t st);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);
 cudaError_t launch_classify(const double* rs, int64_t rows, int64_t row_len, const double* cs,

@@ -1233,74 +1233,262 @@ bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask) {
 int foid_launches(int64_t, int64_t, int) { return 2; }
 
 // ================================================================== calibration stats
-// Row statistics: one warp per row, fp64 accumulation, fixed-order shuffle reduction.
-template <typename T>
-__global__ void k_stats_rows(const T* __restrict__ in, int64_t R, int64_t C, int64_t ld,
-                             double* __restrict__ rs) {
-  const int64_t r = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= R) return;
-  double s = 0, s2 = 0, sa = 0, mx = 0;
-  for (int64_t j = lane; j < C; j += 32) {
-    const double x = double(load_as_float(in, r * ld + j));
-    s += x; s2 += x * x; sa += fabs(x); mx = fmax(mx, fabs(x));
+// One pass over T [R x C] for both statistics (App. A: per-row and per-column
+// sum x, sum x^2, sum |x|, max |x|). Block (cb, chunk) covers columns [256 cb, +256) and rows
+// [rb chunk, +rb) (rb = stats_rb: 64..512, two waves of blocks) in tiles of 64 rows staged in shared memory by coalesced 16-byte
+// loads; then thread t accumulates column t down the tile, and 4 threads per row accumulate 64
+// columns each (combined by two xor shuffles). Sums are fp64 (max is exact in fp32); every
+// reduction runs in a fixed order, so the result is deterministic.
+//   row partial  rpart[cb][r]      col partial  cpart[chunk][c]
+// k_stats_reduce folds them (cb, then chunk, ascending) into rs[R][4] and cs[C][4].
+constexpr int kStatsRBMax = 512;
+// rows per block: enough blocks for two waves of 148 SMs, 64..512 rows (a multiple of 64)
+__host__ __device__ inline int64_t stats_rb(int64_t R, int64_t C) {
+  const int64_t ncb = (C + 255) / 256;
+  int64_t rb = (R * ncb / 296 + 63) / 64 * 64;
+  return rb < 64 ? 64 : (rb > kStatsRBMax ? kStatsRBMax : rb);
+}
+constexpr int kStatsThreads = 256;
+constexpr int kStatsTileRows = 64;
+constexpr int kStatsPitch = 256 * 2 + 16;   // padded row pitch (bytes): conflict-free row reads
+
+struct StatAcc {
+  double s = 0, s2 = 0, sa = 0;
+  float mx = 0.f;
+  __device__ __forceinline__ void add(float v) {
+    const double x = double(v);
+    s = __dadd_rn(s, x);
+    s2 = __fma_rn(x, x, s2);
+    sa = __dadd_rn(sa, fabs(x));
+    mx = fmaxf(mx, fabsf(v));
   }
+  __device__ __forceinline__ void merge(const StatAcc& o) {
+    s = __dadd_rn(s, o.s);
+    s2 = __dadd_rn(s2, o.s2);
+    sa = __dadd_rn(sa, o.sa);
+    mx = fmaxf(mx, o.mx);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kStatsThreads) k_stats_tile(const T* __restrict__ in, int64_t R, int64_t C,
+                                                              int64_t ld, int64_t rb_rows, double* __restrict__ rpart,
+                                                              double* __restrict__ cpart) {
+  __shared__ __align__(16) uint8_t tile[kStatsTileRows * kStatsPitch];   // bf16 inputs only
+  const int tid = threadIdx.x;
+  const int cb = blockIdx.x, chunk = blockIdx.y;
+  const int64_t c0 = int64_t(cb) * 256;
+  const int64_t r_end = min(R, int64_t(chunk) * rb_rows + rb_rows);
+  const bool vec = sizeof(T) == 2 && c0 + 256 <= C && ((ld * 2) % 16) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  StatAcc col;
+  const int rr = tid >> 2, q = tid & 3;   // row stats: row rr of the tile, columns [64 q, 64 q + 64)
+  for (int64_t r0 = int64_t(chunk) * rb_rows; r0 < r_end; r0 += kStatsTileRows) {
+    const int nrows = int(min(int64_t(kStatsTileRows), r_end - r0));
+    // ---- stage 64 x 256 values as bf16 bit patterns (fp32 inputs: generic path below)
+    if (vec) {
+      uint4 u[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    sa += __shfl_xor_sync(0xffffffffu, sa, o);
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int i = 0; i < 8; ++i) {
+        const int e = tid + i * kStatsThreads, row = e >> 5, c16 = e & 31;
+        u[i] = row < nrows ? __ldg(reinterpret_cast<const uint4*>(in + (r0 + row) * ld + c0 + c16 * 8))
+                           : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = tid + i * kStatsThreads, row = e >> 5, c16 = e & 31;
+        *reinterpret_cast<uint4*>(tile + row * kStatsPitch + c16 * 16) = u[i];
+      }
+    } else if (sizeof(T) == 2) {   // ragged / unaligned bf16: element loads (exact bit copies)
+      for (int e = tid; e < kStatsTileRows * 256; e += kStatsThreads) {
+        const int row = e >> 8, c = e & 255;
+        float v = 0.f;
+        if (row < nrows && c0 + c < C) v = load_as_float(in, (r0 + row) * ld + c0 + c);
+        reinterpret_cast<uint16_t*>(tile + row * kStatsPitch)[c] = uint16_t(__float_as_uint(v) >> 16);
+      }
+    }
+    __syncthreads();
+    if (sizeof(T) == 2) {
+      // column tid down the tile
+      const uint16_t* cp = reinterpret_cast<const uint16_t*>(tile) + tid;
+#pragma unroll 8
+      for (int row = 0; row < nrows; ++row) col.add(__uint_as_float(uint32_t(cp[row * (kStatsPitch / 2)]) << 16));
+      // row rr, 64 columns
+      StatAcc racc;
+      if (rr < nrows) {
+        const uint4* rp = reinterpret_cast<const uint4*>(tile + rr * kStatsPitch + q * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 u = rp[i];
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            racc.add(__uint_as_float(w[t] << 16));
+            racc.add(__uint_as_float(w[t] & 0xFFFF0000u));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        racc.s = __dadd_rn(racc.s, __shfl_xor_sync(0xffffffffu, racc.s, o));
+        racc.s2 = __dadd_rn(racc.s2, __shfl_xor_sync(0xffffffffu, racc.s2, o));
+        racc.sa = __dadd_rn(racc.sa, __shfl_xor_sync(0xffffffffu, racc.sa, o));
+        racc.mx = fmaxf(racc.mx, __shfl_xor_sync(0xffffffffu, racc.mx, o));
+      }
+      if (q == 0 && rr < nrows) {
+        double* p = rpart + (int64_t(cb) * R + r0 + rr) * 4;
+        p[0] = racc.s; p[1] = racc.s2; p[2] = racc.sa; p[3] = double(racc.mx);
+      }
+    }
+    __syncthreads();
+    if (sizeof(T) != 2) {
+      // fp32 inputs (tests only): direct global reads, thread per column / 4 threads per row
+      for (int row = 0; row < nrows; ++row)
+        if (c0 + tid < C) col.add(load_as_float(in, (r0 + row) * ld + c0 + tid));
+      StatAcc racc;
+      if (rr < nrows)
+        for (int c = q * 64; c < q * 64 + 64; ++c)
+          if (c0 + c < C) racc.add(load_as_float(in, (r0 + rr) * ld + c0 + c));
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        racc.s = __dadd_rn(racc.s, __shfl_xor_sync(0xffffffffu, racc.s, o));
+        racc.s2 = __dadd_rn(racc.s2, __shfl_xor_sync(0xffffffffu, racc.s2, o));
+        racc.sa = __dadd_rn(racc.sa, __shfl_xor_sync(0xffffffffu, racc.sa, o));
+        racc.mx = fmaxf(racc.mx, __shfl_xor_sync(0xffffffffu, racc.mx, o));
+      }
+      if (q == 0 && rr < nrows) {
+        double* p = rpart + (int64_t(cb) * R + r0 + rr) * 4;
+        p[0] = racc.s; p[1] = racc.s2; p[2] = racc.sa; p[3] = double(racc.mx);
+      }
+    }
   }
-  if (lane == 0) {
-    rs[r * 4 + 0] = s; rs[r * 4 + 1] = s2; rs[r * 4 + 2] = sa; rs[r * 4 + 3] = mx;
+  if (c0 + tid < C) {
+    double* p = cpart + (int64_t(chunk) * C + c0 + tid) * 4;
+    p[0] = col.s; p[1] = col.s2; p[2] = col.sa; p[3] = double(col.mx);
   }
-}
-// Column statistics, pass 1: thread per column over a chunk of rows.
-template <typename T>
-__global__ void k_stats_cols_part(const T* __restrict__ in, int64_t R, int64_t C, int64_t ld,
-                                  int64_t rows_per_chunk, double* __restrict__ part) {
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= C) return;
-  const int64_t r0 = int64_t(blockIdx.y) * rows_per_chunk;
-  const int64_t r1 = min(R, r0 + rows_per_chunk);
-  double s = 0, s2 = 0, sa = 0, mx = 0;
-  for (int64_t r = r0; r < r1; ++r) {
-    const double x = double(load_as_float(in, r * ld + j));
-    s += x; s2 += x * x; sa += fabs(x); mx = fmax(mx, fabs(x));
-  }
-  double* p = part + (int64_t(blockIdx.y) * C + j) * 4;
-  p[0] = s; p[1] = s2; p[2] = sa; p[3] = mx;
-}
-__global__ void k_stats_cols_reduce(const double* __restrict__ part, int64_t nch, int64_t C,
-                                    double* __restrict__ cs) {
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= C) return;
-  double s = 0, s2 = 0, sa = 0, mx = 0;
-  for (int64_t c = 0; c < nch; ++c) {
-    const double* p = part + (c * C + j) * 4;
-    s += p[0]; s2 += p[1]; sa += p[2]; mx = fmax(mx, p[3]);
-  }
-  cs[j * 4 + 0] = s; cs[j * 4 + 1] = s2; cs[j * 4 + 2] = sa; cs[j * 4 + 3] = mx;
 }
 
-int64_t stats_chunks(int64_t R) { return (R + 511) / 512; }
+// cvpart (nullable): per-block partial sums of the CV terms std/(mean|x| + eps) of the rows
+// (cvpart[2 b]) and columns (cvpart[2 b + 1]) this block finalised (App. A), for
+// k_classify_partials. Fixed-order tree sums: deterministic.
+constexpr int kReduceThreads = 256;
+__device__ __forceinline__ double cv_term(double s, double s2, double sa, double n, double eps) {
+  const double mu = s / n;
+  const double var = fmax(s2 / n - mu * mu, 0.0);
+  return sqrt(var) / (sa / n + eps);
+}
+__global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* __restrict__ rpart, int64_t ncb,
+                                                                 int64_t R, const double* __restrict__ cpart,
+                                                                 int64_t nch, int64_t C, double* __restrict__ rs,
+                                                                 double* __restrict__ cs, double* __restrict__ cvpart,
+                                                                 double eps) {
+  __shared__ double red[2][kReduceThreads];
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool is_row = i < R;
+  const int64_t j = is_row ? i : i - R;
+  const bool live = is_row || j < C;
+  double a = 0, b = 0, d = 0, m = 0;
+  if (live) {
+    const double* src = is_row ? rpart : cpart;
+    const int64_t n = is_row ? ncb : nch, stride = is_row ? R : C;
+    int64_t q = 0;
+    for (; q + 4 <= n; q += 4) {   // four loads in flight, summed in order
+      double4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double4*>(src + ((q + u) * stride + j) * 4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a = __dadd_rn(a, v[u].x); b = __dadd_rn(b, v[u].y); d = __dadd_rn(d, v[u].z); m = fmax(m, v[u].w);
+      }
+    }
+    for (; q < n; ++q) {
+      const double4 v = *reinterpret_cast<const double4*>(src + (q * stride + j) * 4);
+      a = __dadd_rn(a, v.x); b = __dadd_rn(b, v.y); d = __dadd_rn(d, v.z); m = fmax(m, v.w);
+    }
+    double* dst = (is_row ? rs : cs) + j * 4;
+    dst[0] = a; dst[1] = b; dst[2] = d; dst[3] = m;
+  }
+  if (cvpart == nullptr) return;   // block-uniform
+  const double t = live ? cv_term(a, b, d, double(is_row ? C : R), eps) : 0.0;
+  red[0][threadIdx.x] = live && is_row ? t : 0.0;
+  red[1][threadIdx.x] = live && !is_row ? t : 0.0;
+  __syncthreads();
+  for (int h = kReduceThreads / 2; h > 0; h >>= 1) {
+    if (int(threadIdx.x) < h) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + h];
+      red[1][threadIdx.x] += red[1][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    cvpart[2 * blockIdx.x] = red[0][0];
+    cvpart[2 * blockIdx.x + 1] = red[1][0];
+  }
+}
+
+// Sum of the blocks' CV partials (fixed order) and the single-rank classification (P:535-541,
+// DESIGN R7): same rule as k_classify.
+__global__ void __launch_bounds__(256) k_classify_partials(const double* __restrict__ cvpart, int nb, int64_t rows,
+                                                          int64_t cols, double tau, double* __restrict__ d_cv,
+                                                          uint8_t* __restrict__ pattern) {
+  __shared__ double red[2][256];
+  double a = 0, b = 0;
+  for (int k = threadIdx.x; k < nb; k += 256) { a += cvpart[2 * k]; b += cvpart[2 * k + 1]; }
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (int(threadIdx.x) < h) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + h];
+      red[1][threadIdx.x] += red[1][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    d_cv[0] = red[0][0];
+    d_cv[1] = red[1][0];
+    const double cv_row = red[0][0] / double(rows), cv_col = red[1][0] / double(cols);
+    const bool row_hit = cv_col > tau, col_hit = cv_row > tau;
+    uint8_t p = 0;
+    if (row_hit && (!col_hit || cv_col >= cv_row)) p = 1;
+    else if (col_hit) p = 2;
+    pattern[0] = p;
+  }
+}
+
+size_t calib_cvpart_bytes(int64_t R, int64_t C) { return size_t((R + C + kReduceThreads - 1) / kReduceThreads) * 16; }
+
+size_t stats_ws_bytes(int64_t R, int64_t C) {
+  const int64_t ncb = (C + 255) / 256, rb = stats_rb(R, C), nch = (R + rb - 1) / rb;
+  return size_t(ncb * R + nch * C) * 32 + 256;
+}
 
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st) {
-  const unsigned rb = unsigned((R + 7) / 8);
-  const int64_t nch = stats_chunks(R);
-  dim3 cg(unsigned((C + 255) / 256), unsigned(nch));
-  if (in_f32) {
-    const float* p = static_cast<const float*>(in);
-    k_stats_rows<float><<<rb, 256, 0, st>>>(p, R, C, ld, rs);
-    k_stats_cols_part<float><<<cg, 256, 0, st>>>(p, R, C, ld, 512, part);
-  } else {
-    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(in);
-    k_stats_rows<__nv_bfloat16><<<rb, 256, 0, st>>>(p, R, C, ld, rs);
-    k_stats_cols_part<__nv_bfloat16><<<cg, 256, 0, st>>>(p, R, C, ld, 512, part);
-  }
-  k_stats_cols_reduce<<<unsigned((C + 255) / 256), 256, 0, st>>>(part, nch, C, cs);
+  const int64_t ncb = (C + 255) / 256, rb = stats_rb(R, C), nch = (R + rb - 1) / rb;
+  double* rpart = part;
+  double* cpart = part + ncb * R * 4;
+  const dim3 grid{unsigned(ncb), unsigned(nch)};
+  if (in_f32) k_stats_tile<float><<<grid, kStatsThreads, 0, st>>>(static_cast<const float*>(in), R, C, ld, rb, rpart, cpart);
+  else k_stats_tile<__nv_bfloat16><<<grid, kStatsThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, C, ld,
+                                                                   rb, rpart, cpart);
+  k_stats_reduce<<<unsigned((R + C + kReduceThreads - 1) / kReduceThreads), kReduceThreads, 0, st>>>(
+      rpart, ncb, R, cpart, nch, C, rs, cs, nullptr, 0.0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld, double* rs, double* cs,
+                             double* part, double* cvpart, double eps, double tau, double* d_cv, uint8_t* pattern,
+                             cudaStream_t st) {
+  const int64_t ncb = (C + 255) / 256, rb = stats_rb(R, C), nch = (R + rb - 1) / rb;
+  double* rpart = part;
+  double* cpart = part + ncb * R * 4;
+  const dim3 grid{unsigned(ncb), unsigned(nch)};
+  if (in_f32) k_stats_tile<float><<<grid, kStatsThreads, 0, st>>>(static_cast<const float*>(in), R, C, ld, rb, rpart, cpart);
+  else k_stats_tile<__nv_bfloat16><<<grid, kStatsThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, C, ld,
+                                                                   rb, rpart, cpart);
+  const int nb = int((R + C + kReduceThreads - 1) / kReduceThreads);
+  k_stats_reduce<<<unsigned(nb), kReduceThreads, 0, st>>>(rpart, ncb, R, cpart, nch, C, rs, cs, cvpart, eps);
+  k_classify_partials<<<1, 256, 0, st>>>(cvpart, nb, R, C, tau, d_cv, pattern);
   return cudaGetLastError();
 }
 

@@ -468,7 +468,21 @@ __global__ void __launch_bounds__(256) k_oe_gather(const __nv_bfloat16* __restri
     const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;   // 8 warps: slots wy, wy + 8, ...
     const int64_t r = int64_t(blockIdx.x) * 32 + lane;
     if (r >= R) return;
-    for (int s = wy; s < n; s += 8) out[int64_t(s) * R + r] = T[r * ld + idx[s]];
+    const __nv_bfloat16* row = T + r * ld;
+    // eight independent loads in flight per thread before the stores
+    for (int s0 = wy; s0 < n; s0 += 64) {
+      __nv_bfloat16 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int s = s0 + 8 * u;
+        v[u] = s < n ? row[__ldg(idx + s)] : __nv_bfloat16();
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int s = s0 + 8 * u;
+        if (s < n) out[int64_t(s) * R + r] = v[u];
+      }
+    }
   }
 }
 
@@ -482,23 +496,49 @@ static cudaError_t launch_oe_gather(const __nv_bfloat16* T, int64_t R, int64_t C
   return launch_k(k_oe_gather, dim3(unsigned((R + 31) / 32)), dim3(256), 0, st, 1, T, R, C, ld, 1, idx, n, out);
 }
 
-cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st, int* launches) {
+// ADAHOP_GATHER_AFTER=1: gathers after the quant pass, the gathered tensor's tiles last (so the
+// gather reads L2) — measured slower (quant stage 0.65 vs 0.53 ms per Llama-3.2-1B layer step)
+static bool gather_after_quant() {
+  static int v = [] {
+    const char* e = getenv("ADAHOP_GATHER_AFTER");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms, cudaStream_t st, int* launches) {
   if (n <= 0) return cudaSuccess;
-  // the OE slices come from a separate gather (copying them inside the quant pipeline stalls it)
-  for (int i = 0; i < n; ++i) {
-    const QuantTcJob& q = jobs[i];
-    if (q.q_row && q.nrow_zero > 0 && q.slice_row) {
-      cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 0, q.row_zero, q.nrow_zero, q.slice_row, st);
-      if (e != cudaSuccess) return e;
-      if (launches) ++*launches;
-    }
-    if (q.q_col && q.ncol_zero > 0 && q.slice_col) {
-      cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 1, q.col_zero, q.ncol_zero, q.slice_col, st);
-      if (e != cudaSuccess) return e;
-      if (launches) ++*launches;
-    }
-  }
   if (n > qtc::kMaxJobs) return cudaErrorInvalidValue;
+  // The OE slices come from a separate gather (copying them inside the quant pipeline stalls
+  // it), launched before the quant pass (see gather_after_quant for the measured alternative).
+  const bool after = gather_after_quant();
+  QuantTcJob jobs[qtc::kMaxJobs];
+  int m = 0;
+  for (int pass = 0; pass < (after ? 2 : 1); ++pass)
+    for (int i = 0; i < n; ++i) {
+      const bool colg = jobs_in[i].q_col && jobs_in[i].ncol_zero > 0 && jobs_in[i].slice_col;
+      if (!after || colg == (pass == 1)) jobs[m++] = jobs_in[i];
+    }
+  auto gathers = [&]() -> cudaError_t {
+    for (int i = 0; i < n; ++i) {
+      const QuantTcJob& q = jobs[i];
+      if (q.q_row && q.nrow_zero > 0 && q.slice_row) {
+        cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 0, q.row_zero, q.nrow_zero, q.slice_row, st);
+        if (e != cudaSuccess) return e;
+        if (launches) ++*launches;
+      }
+      if (q.q_col && q.ncol_zero > 0 && q.slice_col) {
+        cudaError_t e = launch_oe_gather(q.in, q.R, q.C, q.ld, 1, q.col_zero, q.ncol_zero, q.slice_col, st);
+        if (e != cudaSuccess) return e;
+        if (launches) ++*launches;
+      }
+    }
+    return cudaSuccess;
+  };
+  if (!after) {
+    cudaError_t e = gathers();
+    if (e != cudaSuccess) return e;
+  }
   qtc::Jobs J;
   memset(&J, 0, sizeof(J));
   J.n = n;
@@ -535,19 +575,15 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cu
   }
   J.ntiles = tiles;
   if (launches) ++*launches;
-  if (row && col) {
-    if (had) return launch_tc<true, true, true>(J, masks, num_sms, st);
-    return launch_tc<true, true, false>(J, masks, num_sms, st);
-  }
-  if (row) {
-    if (had) return launch_tc<true, false, true>(J, masks, num_sms, st);
-    return launch_tc<true, false, false>(J, masks, num_sms, st);
-  }
-  if (col) {
-    if (had) return launch_tc<false, true, true>(J, masks, num_sms, st);
-    return launch_tc<false, true, false>(J, masks, num_sms, st);
-  }
-  return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (row && col) e = had ? launch_tc<true, true, true>(J, masks, num_sms, st)
+                          : launch_tc<true, true, false>(J, masks, num_sms, st);
+  else if (row) e = had ? launch_tc<true, false, true>(J, masks, num_sms, st)
+                        : launch_tc<true, false, false>(J, masks, num_sms, st);
+  else if (col) e = had ? launch_tc<false, true, true>(J, masks, num_sms, st)
+                        : launch_tc<false, true, false>(J, masks, num_sms, st);
+  if (e != cudaSuccess) return e;
+  return after ? gathers() : cudaSuccess;
 }
 
 cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld, const int32_t* row_zero,
