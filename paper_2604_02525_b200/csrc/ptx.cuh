@@ -231,8 +231,12 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Arrive on a barrier of another CTA of the cluster with the default (.release.cta) semantics,
+// as CUTLASS does for its remote consumer arrives: it orders this thread's tcgen05 ops (after
+// tcgen05.fence::before_thread_sync) without the GPU-scope MEMBAR that .release.cluster
+// compiles to (which waits for this thread's outstanding global stores).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA load: data lands in this CTA's smem, completion is signalled on the mbarrier
 // at `bar_cluster_addr` (the leader CTA's barrier).
