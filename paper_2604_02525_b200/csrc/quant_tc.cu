@@ -67,6 +67,15 @@ __device__ __forceinline__ void mask_build(Mask* m, const int32_t* __restrict__ 
   for (int i = threadIdx.x; i < n; i += blockDim.x) atomicOr(&m->bits[idx[i] >> 5], 1u << (idx[i] & 31));
   __syncthreads();
 }
+// first position in the sorted list idx[0, n) whose value is >= v
+__device__ __forceinline__ int lower_bound_idx(const int32_t* idx, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (idx[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 __device__ __forceinline__ bool mask_hit(const Mask* m, int64_t r) { return (m->bits[r >> 5] >> (r & 31)) & 1u; }
 __device__ __forceinline__ int mask_slot(const Mask* m, int n, int64_t r) {
   int lo = 0, hi = n - 1;
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);   // MMA commit
+      ptx::mbar_init(&empty[s], 2);   // MMA commit + OE-slice gather warp
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
@@ -287,6 +296,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         ptx::tc_commit(&tfull[buf]);
       }
       __syncwarp();
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ OE-slice gather warp
+    // Copies the extracted rows / columns of T that fall in this tile from the staged tile
+    // (128B-swizzled boxes) into the raw bf16 slices, then releases the stage together with
+    // the MMA commit. out_row[s][c] = T[idx[s], c], out_col[s][r] = T[r, idx[s]].
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = first; tile < ntiles; tile += stride) {
+      const int jb = job_of(J, tile);
+      const Job& jj = J.j[jb];
+      const int lt0 = tile - jj.tile0;
+      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
+      ptx::mbar_wait(&full[stage], phase);
+      const uint8_t* base = ring + stage * kTile;
+      if (kCol && jj.ocol.slice != nullptr && jj.ocol.nzero > 0) {
+        const Mask* m = &masks[2 * jb + 1];
+        const int n = jj.ocol.nzero;
+        int j = lower_bound_idx(m->idx, n, ct * 128);
+        const int j1 = lower_bound_idx(m->idx, n, ct * 128 + 128);
+        for (; j < j1; ++j) {
+          const int c = m->idx[j] - ct * 128, box = c >> 6, cc = c & 63;
+          for (int r = int(lane); r < 128; r += 32) {
+            const int64_t row = int64_t(rt) * 128 + r;
+            if (row >= jj.R) break;
+            const int off = box * kBox + r * 128 + ((((cc >> 3) ^ (r & 7)) << 4) | ((cc & 7) << 1));
+            jj.ocol.slice[int64_t(j) * jj.R + row] = *reinterpret_cast<const __nv_bfloat16*>(base + off);
+          }
+        }
+      }
+      if (kRow && jj.orow.slice != nullptr && jj.orow.nzero > 0) {
+        const Mask* m = &masks[2 * jb];
+        const int n = jj.orow.nzero;
+        int j = lower_bound_idx(m->idx, n, rt * 128);
+        const int j1 = lower_bound_idx(m->idx, n, rt * 128 + 128);
+        for (; j < j1; ++j) {
+          const int r = m->idx[j] - rt * 128;
+          const int c = int(lane) * 4;   // 4 columns (8 bytes, inside one 16-byte chunk) per lane
+          if (int64_t(ct) * 128 + c < jj.C) {
+            const int box = c >> 6, cc = c & 63;
+            const int off = box * kBox + r * 128 + ((((cc >> 3) ^ (r & 7)) << 4) | ((cc & 7) << 1));
+            *reinterpret_cast<uint2*>(jj.orow.slice + int64_t(j) * jj.C + int64_t(ct) * 128 + c) =
+                *reinterpret_cast<const uint2*>(base + off);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[stage]);
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 2) {
@@ -498,6 +556,16 @@ static cudaError_t launch_oe_gather(const __nv_bfloat16* T, int64_t R, int64_t C
 
 // ADAHOP_GATHER_AFTER=1: gathers after the quant pass, the gathered tensor's tiles last (so the
 // gather reads L2) — measured slower (quant stage 0.65 vs 0.53 ms per Llama-3.2-1B layer step)
+// ADAHOP_GATHER_FUSED=1: OE slices copied by the quant kernel's gather warp (warp 3) from the
+// staged tiles instead of the separate k_oe_gather launches — measured slower (quant stage 0.59
+// vs 0.54 ms per Llama-3.2-1B layer step: the stage release waits for the copies)
+static bool gather_fused() {
+  static int v = [] {
+    const char* e = getenv("ADAHOP_GATHER_FUSED");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
 static bool gather_after_quant() {
   static int v = [] {
     const char* e = getenv("ADAHOP_GATHER_AFTER");
@@ -512,6 +580,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
   // The OE slices come from a separate gather (copying them inside the quant pipeline stalls
   // it), launched before the quant pass (see gather_after_quant for the measured alternative).
   const bool after = gather_after_quant();
+  const bool fused = gather_fused() && !after;
   QuantTcJob jobs[qtc::kMaxJobs];
   int m = 0;
   for (int pass = 0; pass < (after ? 2 : 1); ++pass)
@@ -535,7 +604,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     }
     return cudaSuccess;
   };
-  if (!after) {
+  if (!after && !fused) {
     cudaError_t e = gathers();
     if (e != cudaSuccess) return e;
   }
@@ -569,8 +638,8 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     tiles += jj.ctiles * int((q.R + 127) / 128);
     jj.kch_row = sf_kchunks(q.C);
     jj.kch_col = sf_kchunks(q.R);
-    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, nullptr, q.had_row};
-    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, nullptr, q.had_col};
+    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, fused ? q.slice_row : nullptr, q.had_row};
+    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, fused ? q.slice_col : nullptr, q.had_col};
     masks |= (row && q.nrow_zero > 0) || (col && q.ncol_zero > 0);
   }
   J.ntiles = tiles;
