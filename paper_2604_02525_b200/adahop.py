@@ -25,7 +25,8 @@ __all__ = [
     "majority_vote", "classify_cv", "stats", "classify", "calibrate", "gemm", "linear",
     "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant", "debug_quant_dual",
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
-    "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes",
+    "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
+    "calibrate_workspace_bytes",
 ]
 
 
