@@ -96,8 +96,13 @@ int gemm_variant() {
 }
 
 cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
-  const int v = gemm_variant();
+  int v = gemm_variant();
   if (v == 1 || a.M <= 128) return launch_gemm_mxf4(a, sms, st);
+  // long-K GEMMs with fewer 256x256 tiles than half the CTA pairs (e.g. the Llama-3.2-1B k/v
+  // wgrad, 512 x 2048, K = 16384): the 256x128 double-buffered tiles keep twice as many pairs
+  // busy (27 -> 22 us measured)
+  const int64_t tiles256 = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  if (v == 256 && a.K >= 8192 && 2 * tiles256 < sms / 2) v = 128;
   return launch_gemm_mxf4_2sm(a, sms, v, st);
 }
 
