@@ -307,6 +307,7 @@ def main():
 
     def step_adahop(stage_events=None):
         n = 0
+        works = []   # wgrad all-reduces in flight: linear i's overlaps the kernels of linear i+1
         for gi, g in enumerate(units):
             L = lin[g["linear"]]
             ctx = stage_events[gi] if stage_events is not None else None
@@ -316,7 +317,7 @@ def main():
                 ah.linear_layer(L["x"], L["w"], L["gy"], strat3[g["linear"]], params, out=(L["y"], L["gx"], L["gw"]),
                                 ws=ws)
                 if world > 1:
-                    ahd.allreduce_wgrad(L["gw"])     # token-sharded DP: sum the wgrad partials
+                    works.append(ahd.allreduce_wgrad(L["gw"], async_op=True))   # DP: sum the wgrad partials
             elif g["path"] == "fwd":
                 ah.linear_fwd(L["x"], L["w"], g["strategy"], params, out=L["y"], ws=ws)
             elif g["path"] == "dgrad":
@@ -324,10 +325,12 @@ def main():
             else:
                 ah.linear_wgrad(L["gy"], L["x"], g["strategy"], params, out=L["gw"], ws=ws)
                 if world > 1:
-                    ahd.allreduce_wgrad(L["gw"])     # token-sharded DP: sum the wgrad partials
+                    works.append(ahd.allreduce_wgrad(L["gw"], async_op=True))   # DP: sum the wgrad partials
             if ctx is not None:
                 ctx.__exit__()
             n += ah.last_launch_count()
+        for w in works:
+            w.wait()   # the step ends when every partial is summed
         launches[0] += n
 
     def step_cublas():
@@ -490,7 +493,7 @@ def main():
                     ah.linear_layer(L["x"], L["w"], L["gy"], strat3[k], params, out=(L["y"], L["gx"], L["gw"]),
                                     ws=ws)
                 if world > 1:
-                    ahd.allreduce_wgrad(L["gw"])
+                    ahd.allreduce_wgrad(L["gw"]).wait()   # before the copy-out of G_W
                 e = torch.cuda.Event()
                 e.record(cur)
                 s_out.wait_event(e)

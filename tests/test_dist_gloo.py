@@ -148,3 +148,21 @@ def test_sharded_calibration_matches_global_oracle():
             pat, cvr, cvc = out[r][p]
             assert pat == O.classify(t) == p
             assert abs(cvr - cr) < 1e-9 * cr and abs(cvc - cc) < 1e-9 * cc
+
+
+# ------------------------------------------------------------------ overlapped wgrad all-reduces
+def _dp_async_allreduce(rank, world):
+    # bench.py issues linear i's all-reduce asynchronously and waits for all of them at the end of
+    # the step: every partial must come back summed, independent of the issue order
+    parts = [torch.full((8, 16), float(rank + 1) * (i + 1), dtype=torch.float32) for i in range(7)]
+    works = [dist_mod.allreduce_wgrad(p, async_op=True) for p in parts]
+    for w in works:
+        w.wait()
+    return [p.numpy().copy() for p in parts]
+
+
+def test_async_wgrad_allreduces_sum_every_partial():
+    out = spawn(_dp_async_allreduce)
+    for r in (0, 1):
+        for i, p in enumerate(out[r]):
+            np.testing.assert_array_equal(p, np.full((8, 16), 3.0 * (i + 1), np.float32))
