@@ -467,7 +467,16 @@ def main():
         # (copy engine, stream s_in) and the device->host copy of linear i-1 (stream s_out) run
         # under the AdaHOP calls of linear i (current stream); events order each linear's stages
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        # only the first linear's copy-in and the last one's copy-out are exposed: start with the
+        # linear with the fewest input bytes and end with the one with the fewest output bytes
+        def nbytes(k, keys):
+            return sum(lin[k][n].numel() * lin[k][n].element_size() for n in keys)
+
         names = list(lin)
+        first = min(names, key=lambda k: nbytes(k, ("x", "w", "gy")))
+        rest = [k for k in names if k != first]
+        last = min(rest, key=lambda k: nbytes(k, ("y", "gx", "gw")))
+        names = [first] + [k for k in rest if k != last] + [last]
 
         def step_e2e():
             cur = torch.cuda.current_stream()
