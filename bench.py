@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="adahop", choices=["adahop", "reference"])
-    ap.add_argument("--workload", default="llama32_1b", choices=["llama32_1b", "llama3_8b"])
+    ap.add_argument("--workload", default="llama32_1b", choices=["llama32_1b", "llama3_8b", "instella_3b"])
     ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
     ap.add_argument("--oe-k", type=int, default=64)
     ap.add_argument("--level", type=int, default=1)
@@ -74,7 +74,7 @@ def fed_pair(path, px, pw, pg):
 
 
 def workload_spec(name):
-    model = synth.LLAMA32_1B if name == "llama32_1b" else synth.LLAMA3_8B
+    model = {"llama32_1b": synth.LLAMA32_1B, "llama3_8b": synth.LLAMA3_8B, "instella_3b": synth.INSTELLA_3B}[name]
     pats = synth.LLAMA32_1B_LAYER_PATTERNS
     return model, pats
 

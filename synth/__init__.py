@@ -115,6 +115,13 @@ LLAMA3_8B = {
     "linears": [("q", 4096, 4096), ("k", 4096, 1024), ("v", 4096, 1024), ("o", 4096, 4096),
                 ("gate", 4096, 14336), ("up", 4096, 14336), ("down", 14336, 4096)],
 }
+# Instella-3B (BASELINE configs[2]): 36 layers (Table 1: 252 linears / 7), hidden 2560, MLP 6912,
+# multi-head attention (k / v as wide as q) — the public model card's shapes, no weights needed.
+INSTELLA_3B = {
+    "hidden": 2560, "mlp": 6912, "kv": 2560, "layers": 36, "tokens": 16384,
+    "linears": [("q", 2560, 2560), ("k", 2560, 2560), ("v", 2560, 2560), ("o", 2560, 2560),
+                ("gate", 2560, 6912), ("up", 2560, 6912), ("down", 6912, 2560)],
+}
 
 # Per-linear tensor patterns for one Llama-3.2-1B layer used by the bench step. They are
 # drawn from the Table-1 census classes: X is C or N,

@@ -1,7 +1,7 @@
 """Full-size GPU parity in the configuration bench.py times: adahop_linear_layer (all three
-GEMMs of one linear, dual-orientation quantisation) at T = 16384 tokens on Llama-3.2-1B and
-Llama-3-8B linear shapes (BASELINE configs[1] and configs[3], including the OE k sweep
-0 / 16 / 64), checked on sampled output entries against the CPU oracle (the oracle forms only
+GEMMs of one linear, dual-orientation quantisation) at T = 16384 tokens on Llama-3.2-1B,
+Instella-3B and Llama-3-8B linear shapes (BASELINE configs[1], [2] and [3], including the OE k
+sweep 0 / 16 / 64), checked on sampled output entries against the CPU oracle (the oracle forms only
 the sampled entries: FOID on the full probe, quantisation of the sampled rows). Also: bf16
 outputs equal RN_bf16 of the fp32 outputs bitwise, and a CUDA-graph replay of
 the layer call (as bench.py runs it) equals the eager call bitwise.
@@ -64,9 +64,10 @@ def sampled_check(path, strategy, got, x, w, gy, k, rng, n=2000):
     ("llama3_8b", "k", 0),          # configs[3] k sweep on the 8B kv projection
     ("llama3_8b", "k", 16),
     ("llama3_8b", "k", 64),
+    ("instella_3b", "down", 64),    # configs[2]: K = 6912 fwd, N = 6912 dgrad / wgrad
 ])
 def test_linear_layer_full_size_sampled(model, linear, k):
-    spec = synth.LLAMA32_1B if model == "llama32_1b" else synth.LLAMA3_8B
+    spec = {"llama32_1b": synth.LLAMA32_1B, "llama3_8b": synth.LLAMA3_8B, "instella_3b": synth.INSTELLA_3B}[model]
     _, d_in, d_out = next(t for t in spec["linears"] if t[0] == linear)
     px, pg = synth.LLAMA32_1B_LAYER_PATTERNS[linear]
     T = 16384
