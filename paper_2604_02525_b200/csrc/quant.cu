@@ -953,6 +953,7 @@ struct FoidJobDev {
 struct FoidBatchDev {
   FoidJobDev j[kFoidMaxJobs];
   int n;
+  int rows_per_block;   // select: rows ranked per CTA (1024 .. 4096)
   int kb_off[kFoidMaxJobs + 1], sb_off[kFoidMaxJobs + 1];
 };
 __device__ __forceinline__ int foid_job_of(const int* off, int n, int b) {
@@ -985,10 +986,21 @@ __global__ void __launch_bounds__(128) k_foid_keys_batch(const __grid_constant__
 //     maxima). At least kk entries (those maxima) are >= L, so every top-kk entry is >= L; an
 //     entry >= L lies in a group whose maximum is >= L, so at most kk * 8E entries are >= L;
 //  3. the entries >= L are compacted into shared memory and ranked exactly among themselves.
-// k_foid_select runs it per 1024-row block (rows -> the block's kk best), and the last block
+// k_foid_select runs it per block of up to 4096 rows (rows -> the block's kk best), and the last block
 // to finish runs it again over the blocks' nb * kk survivors. Keys are fp64 >= 0, so their
 // bit patterns order like the values; the index breaks ties, so the selected set is unique.
 constexpr int kTopkThreads = 1024;
+// rows per select block (<= 4 per thread, topk_core's bound): 4096 — most OE operands (d_in or
+// d_out = 2048 stored rows) then need one block and no merge (FOID stage 0.133 -> 0.118 ms per
+// Llama-3.2-1B layer step). ADAHOP_FOID_BLOCK_ROWS = 1024 / 2048 for comparison.
+static int foid_block_rows() {
+  static int v = [] {
+    const char* e = getenv("ADAHOP_FOID_BLOCK_ROWS");
+    const int r = e ? atoi(e) : 4096;
+    return r == 1024 || r == 2048 ? r : 4096;
+  }();
+  return v;
+}
 constexpr int kTopkGroupLanes = 8;
 constexpr int kTopkGroups = kTopkThreads / kTopkGroupLanes;
 constexpr int kTopkMaxPer = 4;                                   // n <= 4096
@@ -1107,11 +1119,12 @@ __global__ void __launch_bounds__(kTopkThreads) k_foid_select(const __grid_const
   unsigned long long* part_key = reinterpret_cast<unsigned long long*>(J.scratch + R);
   int* part_idx = reinterpret_cast<int*>(part_key + size_t(nb) * 256);
   unsigned* counter = foid_counter(J);
-  const int n_b = min(kTopkThreads, R - b * kTopkThreads);
+  const int rows_per = B.rows_per_block;
+  const int n_b = min(rows_per, R - b * rows_per);
   const int kb = min(kk, n_b);
   const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(J.scratch);
   // this block's kb best rows (padding up to kk with entries that rank after every row)
-  topk_core(keys + int64_t(b) * kTopkThreads, nullptr, b * kTopkThreads, n_b, kb, sm, ckey, cidx,
+  topk_core(keys + int64_t(b) * rows_per, nullptr, b * rows_per, n_b, kb, sm, ckey, cidx,
             part_key + int64_t(b) * kk, part_idx + int64_t(b) * kk);
   for (int t = kb + tid; t < kk; t += kTopkThreads) { part_key[int64_t(b) * kk + t] = 0ull; part_idx[int64_t(b) * kk + t] = 0x7FFFFFFF; }
 #if FOID_TRACE
@@ -1188,13 +1201,14 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
   if (n > kFoidMaxJobs) return cudaErrorInvalidValue;
   FoidBatchDev B{};
   B.n = n;
+  B.rows_per_block = foid_block_rows();
   B.kb_off[0] = B.sb_off[0] = 0;
   for (int i = 0; i < n; ++i) {
     const FoidJob& J = jobs[i];
     if (J.R > kFoidMaxRows || J.R <= 0 || J.k <= 0 || J.k > 256) return cudaErrorInvalidValue;
     B.j[i] = FoidJobDev{J.in, J.R, J.ld, J.kstrided, int(std::min<int64_t>(J.probe, J.K)), J.k, J.scratch, J.idx};
     B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
-    B.sb_off[i + 1] = B.sb_off[i] + int((J.R + kTopkThreads - 1) / kTopkThreads);
+    B.sb_off[i + 1] = B.sb_off[i] + int((J.R + B.rows_per_block - 1) / B.rows_per_block);
   }
   if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
   else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
