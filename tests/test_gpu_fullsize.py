@@ -114,3 +114,15 @@ def test_linear_layer_graph_replay_bitwise():
     torch.cuda.synchronize()
     for a, b in zip(eager, outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("rows,cols,pattern", [(16384, 2048, "R"), (16384, 512, "C"), (2048, 8192, "N")])
+def test_calibration_full_size(rows, cols, pattern):
+    # the calibration pass (a1) at bench sizes: stats tiles, fixed-order partial folds and CV
+    # terms against the oracle's fp64 CVs, and the classification
+    t, _ = synth.operand(rows, cols, pattern, "GY", case_id=700 + rows // 1024 + cols // 64)
+    pat, cvr, cvc = ah.calibrate(dev_bf16(t))
+    orow, ocol = O.cv_row_col(t)
+    assert abs(cvr - orow) <= 1e-9 * max(1, orow) and abs(cvc - ocol) <= 1e-9 * max(1, ocol)
+    assert pat == O.classify(t) == pattern
