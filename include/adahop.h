@@ -31,7 +31,8 @@
  *  - Shape rules: K % 32 == 0 (else ADAHOP_E_SHAPE; no padding);
  *    had_block must be 32 (else ADAHOP_E_UNSUPPORTED); oe_k > rows/cols of the
  *    extracted operand clamps; oe_k == 0 means "no OE"; oe_k <= 256; the OE operand has at
- *    most 16384 stored rows (ADAHOP_E_UNSUPPORTED beyond: FOID selects in one CTA).
+ *    most 16384 stored rows (ADAHOP_E_UNSUPPORTED beyond: the FOID select and the OE
+ *    masks are sized for it).
  *    Leading dimensions must keep every row 16-byte aligned.
  */
 #ifndef ADAHOP_H_
