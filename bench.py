@@ -262,10 +262,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if os.environ.get("ADAHOP_DIST_BACKEND", "nccl") != "nccl":
+        local = local % max(1, torch.cuda.device_count())   # several ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # ADAHOP_DIST_BACKEND=gloo runs the multi-rank path with several ranks on one GPU (a test
+        # of the sharding / reduction plumbing; NCCL needs one GPU per rank)
+        backend = os.environ.get("ADAHOP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2604_02525_b200 as ah
     import paper_2604_02525_b200.dist as ahd
@@ -502,7 +510,7 @@ def main():
                     ah.linear_layer(L["x"], L["w"], L["gy"], strat3[k], params, out=(L["y"], L["gx"], L["gw"]),
                                     ws=ws)
                 if world > 1:
-                    ahd.allreduce_wgrad(L["gw"]).wait()   # before the copy-out of G_W
+                    ahd.allreduce_wgrad(L["gw"], async_op=True).wait()   # before the copy-out of G_W
                 e = torch.cuda.Event()
                 e.record(cur)
                 s_out.wait_event(e)

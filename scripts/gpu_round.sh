@@ -31,3 +31,7 @@ if [ $MODE = full ]; then
     -o $OUT/quant $NCUB > $OUT/ncu_quant.log 2>&1
 fi
 echo done > $OUT/DONE
+# multi-rank plumbing smoke on one GPU (gloo; NCCL needs one GPU per rank): the torchrun path
+ADAHOP_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --e2e-steps 2 \
+  > $OUT/two_rank_gloo.log 2>&1; echo "rc=$?" >> $OUT/two_rank_gloo.log
