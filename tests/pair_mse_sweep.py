@@ -12,7 +12,9 @@ product of
   * the strategy the table picks (tab:strategy_summary P:305-326, Lv1) and the best measured.
 The GPU IHT error is also checked against the oracle's (same codes, fp32 vs fp64 sums).
 
-Usage (B200): python scripts/pair_mse.py [--seeds 5] [--json out.json]
+Usage (B200): python tests/pair_mse_sweep.py [--seeds 5] [--json out.json]
+(It lives under tests/ because it calls the oracle: only tests/, smoke() and bench.py's CPU
+legs may.)
 """
 from __future__ import annotations
 

@@ -1,5 +1,5 @@
 """Nine-pair error sweep on the GPU path (P:161-163 Imp metric), see
-scripts/pair_mse.py. Pins: (1) the GPU IHT error equals the oracle's (the codes are bit-exact;
+tests/pair_mse_sweep.py. Pins: (1) the GPU IHT error equals the oracle's (the codes are bit-exact;
 only the fp32 vs fp64 accumulation differs); (2) Thm. OE: extracting the
 outer-dimension outliers beats IHT alone — OE-Left for row-outlier A (RR, RC, RN), OE-Right
 for column-outlier B (RC, CC, NC); (3) Prop. transform effectiveness: IHT along K
@@ -15,8 +15,8 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
-import pair_mse  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import pair_mse_sweep as pair_mse  # noqa: E402
 
 
 @pytest.fixture(scope="module")
