@@ -1390,6 +1390,14 @@ __device__ __forceinline__ double cv_term(double s, double s2, double sa, double
   const double var = fmax(s2 / n - mu * mu, 0.0);
   return sqrt(var) / (sa / n + eps);
 }
+// Threads: one per row (the row section padded to whole warps), then `lanes` per column (8 for
+// narrow tensors, whose few columns each have many row-chunk partials; 1 for wide ones); the
+// lanes of a column sum the partials q = lane, lane + lanes, ... in order and combine by xor
+// shuffles (a fixed pattern: deterministic).
+__host__ __device__ inline int stats_col_lanes(int64_t C) { return C <= 2048 ? 8 : (C <= 4096 ? 4 : 1); }
+__host__ __device__ inline int64_t stats_reduce_threads(int64_t R, int64_t C) {
+  return (R + 31) / 32 * 32 + C * stats_col_lanes(C);
+}
 __global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* __restrict__ rpart, int64_t ncb,
                                                                  int64_t R, const double* __restrict__ cpart,
                                                                  int64_t nch, int64_t C, double* __restrict__ rs,
@@ -1397,34 +1405,51 @@ __global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* _
                                                                  double eps) {
   __shared__ double red[2][kReduceThreads];
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool is_row = i < R;
-  const int64_t j = is_row ? i : i - R;
-  const bool live = is_row || j < C;
+  const int64_t rpad = (R + 31) / 32 * 32;
+  const int lanes = stats_col_lanes(C);
+  const bool is_row = i < rpad;                                   // warp-uniform
+  const int sub = is_row ? 0 : int((i - rpad) % lanes);
+  const int64_t j = is_row ? i : (i - rpad) / lanes;
+  const bool live = is_row ? i < R : j < C;
   double a = 0, b = 0, d = 0, m = 0;
-  if (live) {
+  {
     const double* src = is_row ? rpart : cpart;
     const int64_t n = is_row ? ncb : nch, stride = is_row ? R : C;
-    int64_t q = 0;
-    for (; q + 4 <= n; q += 4) {   // four loads in flight, summed in order
-      double4 v[4];
+    const int step = is_row ? 1 : lanes;
+    int64_t q = sub;
+    if (live) {
+      for (; q + 3 * step < n; q += 4 * step) {   // four loads in flight, summed in order
+        double4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double4*>(src + ((q + u) * stride + j) * 4);
+        for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double4*>(src + ((q + u * step) * stride + j) * 4);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a = __dadd_rn(a, v[u].x); b = __dadd_rn(b, v[u].y); d = __dadd_rn(d, v[u].z); m = fmax(m, v[u].w);
+        for (int u = 0; u < 4; ++u) {
+          a = __dadd_rn(a, v[u].x); b = __dadd_rn(b, v[u].y); d = __dadd_rn(d, v[u].z); m = fmax(m, v[u].w);
+        }
+      }
+      for (; q < n; q += step) {
+        const double4 v = *reinterpret_cast<const double4*>(src + (q * stride + j) * 4);
+        a = __dadd_rn(a, v.x); b = __dadd_rn(b, v.y); d = __dadd_rn(d, v.z); m = fmax(m, v.w);
       }
     }
-    for (; q < n; ++q) {
-      const double4 v = *reinterpret_cast<const double4*>(src + (q * stride + j) * 4);
-      a = __dadd_rn(a, v.x); b = __dadd_rn(b, v.y); d = __dadd_rn(d, v.z); m = fmax(m, v.w);
+    if (!is_row) {
+      for (int o = 1; o < lanes; o <<= 1) {
+        a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        d = __dadd_rn(d, __shfl_xor_sync(0xffffffffu, d, o));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      }
     }
-    double* dst = (is_row ? rs : cs) + j * 4;
-    dst[0] = a; dst[1] = b; dst[2] = d; dst[3] = m;
+    if (live && sub == 0) {
+      double* dst = (is_row ? rs : cs) + j * 4;
+      dst[0] = a; dst[1] = b; dst[2] = d; dst[3] = m;
+    }
   }
   if (cvpart == nullptr) return;   // block-uniform
-  const double t = live ? cv_term(a, b, d, double(is_row ? C : R), eps) : 0.0;
-  red[0][threadIdx.x] = live && is_row ? t : 0.0;
-  red[1][threadIdx.x] = live && !is_row ? t : 0.0;
+  const bool owner = live && sub == 0;
+  const double t = owner ? cv_term(a, b, d, double(is_row ? C : R), eps) : 0.0;
+  red[0][threadIdx.x] = owner && is_row ? t : 0.0;
+  red[1][threadIdx.x] = owner && !is_row ? t : 0.0;
   __syncthreads();
   for (int h = kReduceThreads / 2; h > 0; h >>= 1) {
     if (int(threadIdx.x) < h) {
@@ -1469,7 +1494,9 @@ __global__ void __launch_bounds__(256) k_classify_partials(const double* __restr
   }
 }
 
-size_t calib_cvpart_bytes(int64_t R, int64_t C) { return size_t((R + C + kReduceThreads - 1) / kReduceThreads) * 16; }
+size_t calib_cvpart_bytes(int64_t R, int64_t C) {
+  return size_t((stats_reduce_threads(R, C) + kReduceThreads - 1) / kReduceThreads) * 16;
+}
 
 size_t stats_ws_bytes(int64_t R, int64_t C) {
   const int64_t ncb = (C + 255) / 256, rb = stats_rb(R, C), nch = (R + rb - 1) / rb;
@@ -1485,7 +1512,7 @@ cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int6
   if (in_f32) k_stats_tile<float><<<grid, kStatsThreads, 0, st>>>(static_cast<const float*>(in), R, C, ld, rb, rpart, cpart);
   else k_stats_tile<__nv_bfloat16><<<grid, kStatsThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, C, ld,
                                                                    rb, rpart, cpart);
-  k_stats_reduce<<<unsigned((R + C + kReduceThreads - 1) / kReduceThreads), kReduceThreads, 0, st>>>(
+  k_stats_reduce<<<unsigned((stats_reduce_threads(R, C) + kReduceThreads - 1) / kReduceThreads), kReduceThreads, 0, st>>>(
       rpart, ncb, R, cpart, nch, C, rs, cs, nullptr, 0.0);
   return cudaGetLastError();
 }
@@ -1500,7 +1527,7 @@ cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, 
   if (in_f32) k_stats_tile<float><<<grid, kStatsThreads, 0, st>>>(static_cast<const float*>(in), R, C, ld, rb, rpart, cpart);
   else k_stats_tile<__nv_bfloat16><<<grid, kStatsThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), R, C, ld,
                                                                    rb, rpart, cpart);
-  const int nb = int((R + C + kReduceThreads - 1) / kReduceThreads);
+  const int nb = int((stats_reduce_threads(R, C) + kReduceThreads - 1) / kReduceThreads);
   k_stats_reduce<<<unsigned(nb), kReduceThreads, 0, st>>>(rpart, ncb, R, cpart, nch, C, rs, cs, cvpart, eps);
   k_classify_partials<<<1, 256, 0, st>>>(cvpart, nb, R, C, tau, d_cv, pattern);
   return cudaGetLastError();
