@@ -442,7 +442,7 @@ def main():
     #      (X, W, G_Y of every linear), timed like the step; 2 B read per element is the work
     cal_t = [L[n] for L in lin.values() for n in ("x", "w", "gy")]
     cal_ws = torch.empty(max(ah.calibrate_workspace_bytes(*t.shape) for t in cal_t), dtype=torch.uint8, device=dev)
-    cal_cv = torch.empty((len(cal_t), 2), dtype=torch.float64, device=dev)
+    cal_cv = torch.empty((len(cal_t), 4), dtype=torch.float64, device=dev)
     cal_pat = torch.empty(len(cal_t), dtype=torch.uint8, device=dev)
 
     def step_calib():

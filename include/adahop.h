@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ADAHOP_ABI_VERSION 1
+#define ADAHOP_ABI_VERSION 2
 
 typedef struct CUstream_st* adahop_stream_t; /* == cudaStream_t */
 
@@ -60,7 +60,12 @@ typedef enum {
 } adahop_status_t;
 
 /* Outlier pattern of a tensor as fed to the matmul. */
-typedef enum { ADAHOP_PAT_NONE = 0, ADAHOP_PAT_ROW = 1, ADAHOP_PAT_COL = 2 } adahop_pattern_t;
+typedef enum {
+  ADAHOP_PAT_INVALID = -1,   /* returned by adahop_majority_vote for an empty / invalid record */
+  ADAHOP_PAT_NONE = 0,
+  ADAHOP_PAT_ROW = 1,
+  ADAHOP_PAT_COL = 2
+} adahop_pattern_t;
 
 /* Strategy (tab:strategy_summary). */
 typedef enum {
@@ -97,7 +102,8 @@ adahop_strategy_t adahop_strategy_for_pair(adahop_pattern_t left, adahop_pattern
                                            int32_t level);
 
 /* Majority vote over per-step patterns; ties resolve R > C > N (R9).
- * `per_step` is a host array of n >= 1 values. Returns ADAHOP_PAT_NONE for n <= 0. */
+ * `per_step` is a host array of n >= 1 pattern codes (0, 1, 2). Returns ADAHOP_PAT_INVALID for
+ * a NULL array, n <= 0, or any code outside {0, 1, 2} (an input error, like the oracle's). */
 adahop_pattern_t adahop_majority_vote(const int32_t* per_step, int32_t n);
 
 /* Classification rule of App. A on already-reduced CVs (host, pure):
@@ -117,18 +123,28 @@ adahop_status_t adahop_stats(const void* T, adahop_dtype_t dt, int64_t rows, int
                              int64_t ld, double* row_stats, double* col_stats, void* ws,
                              size_t ws_bytes, adahop_stream_t stream);
 
-/* CV sums from statistics (App. A; population std):
+/* CV sums from statistics (App. A; population std). d_cv is a device array of 4:
  * d_cv[0] = sum_i std(T_i,:)/(mean|T_i,:| + eps) over the `rows` given rows (each has
  * `cols` elements); d_cv[1] = sum_j std(T_:,j)/(mean|T_:,j| + eps) over `cols` columns,
- * each with `col_count` elements (the global row count under token sharding).
- * Also writes d_pattern[0] = classification with CV_row = d_cv[0]/rows and
- * CV_col = d_cv[1]/cols (correct for a single rank). */
+ * each with `col_count` elements (the global row count under token sharding);
+ * d_cv[2] = CV_row = d_cv[0] / rows, d_cv[3] = CV_col = d_cv[1] / cols, and
+ * d_pattern[0] = the App. A decision (R7) on them — the pattern of T on a
+ * single rank. Multi-rank (token-sharded) calibration, all arithmetic in the library:
+ *   adahop_stats -> all-reduce col_stats (SUM of [.,0..2], MAX of [.,3])
+ *   -> adahop_classify(col_count = global rows) -> all-reduce d_cv[0] (SUM)
+ *   -> adahop_classify_sums(rows_global) -> the global pattern, identical on every rank. */
 adahop_status_t adahop_classify(const double* row_stats, int64_t rows, const double* col_stats,
                                 int64_t cols, int64_t col_count, const adahop_params_t* p,
                                 double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
 
+/* The App. A decision from CV sums already reduced over all ranks: reads d_cv[0] (row-CV sum
+ * over the rows_global rows of all ranks) and d_cv[1] (column-CV sum over `cols` columns), writes
+ * d_cv[2] = d_cv[0] / rows_global, d_cv[3] = d_cv[1] / cols and d_pattern[0] (device). */
+adahop_status_t adahop_classify_sums(double* d_cv, int64_t rows_global, int64_t cols, const adahop_params_t* p,
+                                     uint8_t* d_pattern, adahop_stream_t stream);
+
 /* One-call calibration of one tensor for one step on a single rank: stats + classify.
- * d_cv (2 doubles) and d_pattern (1 byte) are device outputs.
+ * d_cv (4 doubles, as adahop_classify) and d_pattern (1 byte) are device outputs.
  * Workspace: adahop_calibrate_workspace_bytes(rows, cols). */
 size_t adahop_calibrate_workspace_bytes(int64_t rows, int64_t cols);
 adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows, int64_t cols,
@@ -178,15 +194,46 @@ adahop_status_t adahop_linear_wgrad(const void* GY, const void* X, void* GW, ada
  * three calls above, but every input tensor is read once: a dual-orientation quantisation
  * pass emits both FP4 layouts of X (fwd A, wgrad B), W (fwd B, dgrad B) and G_Y (dgrad A,
  * wgrad A) — the quantised copies the paper keeps for backward. Requires T, d_in,
- * d_out multiples of 32 and d_in, d_out multiples of 8. Outputs Y [T x d_out],
- * G_X [T x d_in], G_W [d_out x d_in] contiguous in out_dt. G_W is this rank's partial under
- * token sharding (the caller all-reduces it). */
+ * d_out multiples of 32. Outputs Y [T x d_out] and G_X [T x d_in] contiguous in out_dt,
+ * G_W [d_out x d_in] contiguous in gw_dt (fp32 for the data-parallel all-reduce).
+ * G_W is this rank's partial under token sharding (the caller all-reduces it). */
 size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
                                     const adahop_params_t* p);
 adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
-                                    adahop_dtype_t out_dt, int64_t T, int64_t d_in, int64_t d_out,
-                                    const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
+                                    adahop_dtype_t out_dt, adahop_dtype_t gw_dt, int64_t T, int64_t d_in,
+                                    int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
                                     size_t ws_bytes, adahop_stream_t stream);
+
+/* The same layer split into the two halves of a training step ("For activation tensors in
+ * the Forward path, both the quantized residual and the BF16 outlier tensor are saved to the
+ * context for backpropagation").
+ *   adahop_linear_forward:  FOID + dual quantisation of X and W, Y = X W^T (fwd strategy s[0]);
+ *                           writes the context `ctx` (caller-owned device memory of
+ *                           adahop_linear_ctx_bytes, 256-byte aligned): the column-layout FP4
+ *                           codes + E8M0 scales of X (wgrad B) and W (dgrad B), and the OE
+ *                           indices + raw BF16 slices of their extracted columns.
+ *   adahop_linear_backward: FOID + dual quantisation of G_Y, G_X = G_Y W and G_W = G_Y^T X from
+ *                           the context. X (bf16, T x d_in) is read only when the wgrad's BF16
+ *                           part multiplies by all of X — wgrad OE-Left (A_out B) or the
+ *                           Lv2 BF16 wgrad; adahop_linear_backward_needs_x tells the
+ *                           caller whether it must keep X alive (pass NULL otherwise).
+ * Results are bitwise those of adahop_linear_layer with the same arguments (same kernels, same
+ * inputs). The context must not be modified between the two calls; W must be unchanged. Both
+ * calls use the workspace size adahop_linear_split_workspace_bytes (scratch, may be shared). */
+size_t adahop_linear_ctx_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                               const adahop_params_t* p);
+size_t adahop_linear_split_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                           const adahop_params_t* p);
+int32_t adahop_linear_backward_needs_x(const adahop_strategy_t* s, const adahop_params_t* p);   /* host, pure */
+adahop_status_t adahop_linear_forward(const void* X, const void* W, void* Y, adahop_dtype_t out_dt, int64_t T,
+                                      int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                      const adahop_params_t* p, void* ctx, size_t ctx_bytes, void* ws,
+                                      size_t ws_bytes, adahop_stream_t stream);
+adahop_status_t adahop_linear_backward(const void* GY, const void* W, const void* X, void* GX, void* GW,
+                                       adahop_dtype_t gx_dt, adahop_dtype_t gw_dt, int64_t T, int64_t d_in,
+                                       int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p,
+                                       const void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream);
 
 /* ------------------------------------------------------- debug / parity entry points */
 
@@ -207,7 +254,8 @@ size_t adahop_debug_workspace_bytes(int64_t R, int64_t K);
 /* One-pass dual-orientation IHT + quantisation of a bf16 tensor T [R x C] (pitch ld elements):
  * the row operand (stored rows = R, K = C: q_row [R x C/2], scales_row [R x C/32]) and the
  * column operand (stored rows = C, K = R: q_col [C x R/2], scales_col [C x R/32]) — the two
- * layouts the three GEMMs of one linear need (eq:iht_fwd/dgrad/wgrad). row_zero /
+ * layouts the three GEMMs of one linear need (eq:forward / eq:backward_gw / eq:backward_gx,
+ * P:74-78; the quantised activations kept for backward). row_zero /
  * col_zero (sorted int32, device, <= 256 each) are the OE rows / columns: masked to zero blocks
  * and copied raw to slice_row [nrow_zero x C] / slice_col [ncol_zero x R] bf16 (nullable).
  * Canonical code / scale layouts as adahop_debug_iht_quant. R, C multiples of 32.
@@ -252,8 +300,9 @@ int32_t adahop_last_launch_count(void);
 
 /* Optional stage timing (tab:latency breakdown): `events` is a host array of 5
  * cudaEvent_t (or NULL to disable) used by the following hot-path calls on this thread:
- * [0] start, [1] after FOID + outlier gather, [2] after IHT+quant of both operands,
- * [3] after the MXFP4 GEMM (or the Lv2 BF16 GEMM), [4] after the outlier GEMM + scatter. */
+ * [0] start, [1] after FOID, [2] after IHT+quant of both operands (with the OE-slice gathers),
+ * [3] after the BF16 outlier GEMM + split-K fold, [4] after the MXFP4 GEMM whose epilogue writes
+ * the outlier entries (the fused scatter) — or after the Lv2 BF16 GEMM. */
 void adahop_set_stage_events(void* events);
 
 #ifdef __cplusplus

@@ -44,6 +44,7 @@ SIGNATURES = {
     "adahop_stats_workspace_bytes": (SZ, [I64, I64]),
     "adahop_stats": (I32, [P, I32, I64, I64, I64, P, P, P, SZ, P]),
     "adahop_classify": (I32, [P, I64, P, I64, I64, PP, P, P, P]),
+    "adahop_classify_sums": (I32, [P, I64, I64, PP, P, P]),
     "adahop_calibrate_workspace_bytes": (SZ, [I64, I64]),
     "adahop_calibrate": (I32, [P, I32, I64, I64, I64, PP, P, SZ, P, P, P]),
     "adahop_gemm_workspace_bytes": (SZ, [I64, I64, I64, I32, PP]),
@@ -53,7 +54,12 @@ SIGNATURES = {
     "adahop_linear_dgrad": (I32, [P, P, P, I32, I64, I64, I64, I32, PP, P, SZ, P]),
     "adahop_linear_wgrad": (I32, [P, P, P, I32, I64, I64, I64, I32, PP, P, SZ, P]),
     "adahop_layer_workspace_bytes": (SZ, [I64, I64, I64, C.POINTER(I32), PP]),
-    "adahop_linear_layer": (I32, [P, P, P, P, P, P, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P]),
+    "adahop_linear_layer": (I32, [P, P, P, P, P, P, I32, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P]),
+    "adahop_linear_ctx_bytes": (SZ, [I64, I64, I64, C.POINTER(I32), PP]),
+    "adahop_linear_split_workspace_bytes": (SZ, [I64, I64, I64, C.POINTER(I32), PP]),
+    "adahop_linear_backward_needs_x": (I32, [C.POINTER(I32), PP]),
+    "adahop_linear_forward": (I32, [P, P, P, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P, SZ, P]),
+    "adahop_linear_backward": (I32, [P, P, P, P, P, I32, I32, I64, I64, I64, C.POINTER(I32), PP, P, SZ, P, SZ, P]),
     "adahop_debug_iht_quant": (I32, [P, I32, I64, I64, I64, I32, P, I32, P, P, P, P, SZ, P]),
     "adahop_debug_quant_dual": (I32, [P, I32, I64, I64, I64, P, I32, P, I32, P, P, P, P, P, P, P, SZ, P]),
     "adahop_debug_workspace_bytes": (SZ, [I64, I64]),

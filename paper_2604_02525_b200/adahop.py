@@ -26,7 +26,8 @@ __all__ = [
     "linear_fwd", "linear_dgrad", "linear_wgrad", "workspace_bytes", "debug_iht_quant", "debug_quant_dual",
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
-    "calibrate_workspace_bytes",
+    "calibrate_workspace_bytes", "classify_sums", "LinearContext", "linear_forward", "linear_backward",
+    "split_workspace_bytes",
 ]
 
 
@@ -56,8 +57,12 @@ def strategy_for_pair(left: str, right: str, level: int = 1) -> str:
 
 
 def majority_vote(patterns) -> str:
-    arr = (C.c_int32 * len(patterns))(*[PAT[p] for p in patterns])
-    return PAT_NAME[lib.adahop_majority_vote(arr, len(patterns))]
+    """Mode of the per-step patterns (ties R > C > N); ValueError for an empty record."""
+    arr = (C.c_int32 * max(1, len(patterns)))(*[PAT.get(p, -1) for p in patterns])
+    v = lib.adahop_majority_vote(arr, len(patterns))
+    if v < 0:
+        raise ValueError(f"invalid calibration record {list(patterns)!r}")
+    return PAT_NAME[v]
 
 
 def classify_cv(cv_row: float, cv_col: float, params: Params | None = None) -> str:
@@ -94,9 +99,14 @@ def _ws(nbytes: int, ws: Workspace | None, device) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------------- calibration
+def _check_rowmajor(t: torch.Tensor) -> None:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a 2-D tensor with unit column stride (row-major rows)")
+
+
 def stats(t: torch.Tensor):
     """Per-row and per-column {sum x, sum x^2, sum |x|, max |x|} (fp64) of a 2-D tensor."""
-    assert t.dim() == 2 and t.stride(1) == 1
+    _check_rowmajor(t)
     rows, cols = t.shape
     rs = torch.empty((rows, 4), dtype=torch.float64, device=t.device)
     cs = torch.empty((cols, 4), dtype=torch.float64, device=t.device)
@@ -108,10 +118,11 @@ def stats(t: torch.Tensor):
 
 
 def classify(row_stats, col_stats, row_len: int, col_count: int, params: Params | None = None):
-    """CV sums (device, 2 doubles) and the single-rank pattern (device uint8)."""
+    """adahop_classify: cv (device, 4 doubles: row-CV sum, column-CV sum, CV_row, CV_col) and the
+    single-rank pattern (device uint8)."""
     p = params or Params()
     dev = row_stats.device
-    cv = torch.empty(2, dtype=torch.float64, device=dev)
+    cv = torch.empty(4, dtype=torch.float64, device=dev)
     pat = torch.empty(1, dtype=torch.uint8, device=dev)
     rows = row_stats.shape[0]
     cols = col_stats.shape[0]
@@ -121,26 +132,40 @@ def classify(row_stats, col_stats, row_len: int, col_count: int, params: Params 
     return cv, pat
 
 
+def classify_sums(cv: torch.Tensor, rows_global: int, cols: int, params: Params | None = None):
+    """adahop_classify_sums: the App. A decision from the all-reduced CV sums cv[0], cv[1] (device,
+    4 doubles, updated in place: cv[2] = CV_row, cv[3] = CV_col); returns the pattern (device uint8)."""
+    p = params or Params()
+    assert cv.dtype == torch.float64 and cv.numel() >= 4 and cv.is_contiguous()
+    pat = torch.empty(1, dtype=torch.uint8, device=cv.device)
+    check("adahop_classify_sums", lib.adahop_classify_sums(_ptr(cv), rows_global, cols, C.byref(p), _ptr(pat),
+                                                           _stream()))
+    return pat
+
+
 def calibrate(t: torch.Tensor, params: Params | None = None):
     """One calibration step of one tensor (App. A): returns (pattern 'R'|'C'|'N', cv_row, cv_col)."""
     p = params or Params()
+    _check_rowmajor(t)
     rows, cols = t.shape
     n = lib.adahop_calibrate_workspace_bytes(rows, cols)
     w = torch.empty(n, dtype=torch.uint8, device=t.device)
-    cv = torch.empty(2, dtype=torch.float64, device=t.device)
+    cv = torch.empty(4, dtype=torch.float64, device=t.device)
     pat = torch.empty(1, dtype=torch.uint8, device=t.device)
     check("adahop_calibrate", lib.adahop_calibrate(_ptr(t), _dt(t), rows, cols, t.stride(0), C.byref(p),
                                                    _ptr(w), n, _ptr(cv), _ptr(pat), _stream()))
-    cvh = cv.cpu()
-    return PAT_NAME[int(pat.item())], float(cvh[0]) / rows, float(cvh[1]) / cols
+    cvh = cv.cpu().tolist()
+    return PAT_NAME[int(pat.item())], cvh[2], cvh[3]
 
 
 def calibrate_async(t: torch.Tensor, ws: torch.Tensor, cv: torch.Tensor, pat: torch.Tensor,
                     params: Params | None = None) -> None:
-    """adahop_calibrate without the host read-back (graph-capturable): cv (2 fp64) receives the
-    per-row / per-column CV sums and pat (1 uint8) the pattern code, both on the device.
-    ws must hold calibrate_workspace_bytes(rows, cols) bytes."""
+    """adahop_calibrate without the host read-back (graph-capturable): cv (4 fp64) receives the
+    row / column CV sums and CV_row, CV_col, and pat (1 uint8) the pattern code, both on the
+    device. ws must hold calibrate_workspace_bytes(rows, cols) bytes."""
     p = params or Params()
+    _check_rowmajor(t)
+    assert cv.dtype == torch.float64 and cv.numel() >= 4 and cv.is_contiguous()
     rows, cols = t.shape
     check("adahop_calibrate", lib.adahop_calibrate(_ptr(t), _dt(t), rows, cols, t.stride(0), C.byref(p),
                                                    _ptr(ws), ws.numel(), _ptr(cv), _ptr(pat), _stream()))
@@ -349,29 +374,114 @@ class StageEvents:
         return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(self.NAMES)}
 
 
-def linear_layer(x, w, gy, strategies, params=None, out_dtype=torch.bfloat16, out=None, ws=None):
+def _strats(strategies):
+    return (C.c_int32 * 3)(*[_strategy(v) for v in strategies])
+
+
+def linear_layer(x, w, gy, strategies, params=None, out_dtype=torch.bfloat16, out=None, ws=None,
+                 gw_dtype=None):
     """fwd / dgrad / wgrad of one linear in one call (adahop_linear_layer): every input tensor
-    is quantised once in both orientations. strategies = (fwd, dgrad, wgrad)."""
+    is quantised once in both orientations. strategies = (fwd, dgrad, wgrad). Y and G_X are
+    written in out_dtype, G_W in gw_dtype (default: out_dtype)."""
     p = params or Params()
     T, d_in = x.shape
     d_out = w.shape[0]
     for t in (x, w, gy):
         assert t.is_contiguous() and t.dtype == torch.bfloat16
-    s = (C.c_int32 * 3)(*[_strategy(v) for v in strategies])
+    assert tuple(w.shape) == (d_out, d_in) and tuple(gy.shape) == (T, d_out)
+    s = _strats(strategies)
+    gw_dtype = gw_dtype or out_dtype
     if out is None:
         out = (torch.empty((T, d_out), dtype=out_dtype, device=x.device),
                torch.empty((T, d_in), dtype=out_dtype, device=x.device),
-               torch.empty((d_out, d_in), dtype=out_dtype, device=x.device))
+               torch.empty((d_out, d_in), dtype=gw_dtype, device=x.device))
     y, gx, gw = out
+    for o, shape, dt in ((y, (T, d_out), y.dtype), (gx, (T, d_in), y.dtype), (gw, (d_out, d_in), gw.dtype)):
+        if tuple(o.shape) != shape or not o.is_contiguous() or o.dtype != dt:
+            raise ValueError(f"linear_layer outputs must be contiguous tensors of shapes {(T, d_out)}, "
+                             f"{(T, d_in)}, {(d_out, d_in)} (Y and G_X of one dtype)")
     n = lib.adahop_layer_workspace_bytes(T, d_in, d_out, s, C.byref(p))
     wbuf = _ws(n, ws, x.device)
     check("adahop_linear_layer",
-          lib.adahop_linear_layer(_ptr(x), _ptr(w), _ptr(gy), _ptr(y), _ptr(gx), _ptr(gw), _dt(y), T, d_in, d_out,
-                                  s, C.byref(p), _ptr(wbuf), wbuf.numel(), _stream()))
+          lib.adahop_linear_layer(_ptr(x), _ptr(w), _ptr(gy), _ptr(y), _ptr(gx), _ptr(gw), _dt(y), _dt(gw), T, d_in,
+                                  d_out, s, C.byref(p), _ptr(wbuf), wbuf.numel(), _stream()))
     return y, gx, gw
 
 
 def layer_workspace_bytes(T, d_in, d_out, strategies, params=None) -> int:
     p = params or Params()
-    s = (C.c_int32 * 3)(*[_strategy(v) for v in strategies])
-    return lib.adahop_layer_workspace_bytes(T, d_in, d_out, s, C.byref(p))
+    return lib.adahop_layer_workspace_bytes(T, d_in, d_out, _strats(strategies), C.byref(p))
+
+
+class LinearContext:
+    """What adahop_linear_forward saves for adahop_linear_backward: the column-layout FP4
+    copies of X and W with their OE indices and BF16 outlier slices, in one device buffer; plus a
+    reference to X itself only when the wgrad strategy needs all of X in BF16 (wgrad OE-Left or
+    the Lv2 BF16 wgrad; adahop_linear_backward_needs_x)."""
+
+    def __init__(self, T, d_in, d_out, strategies, params, device):
+        self.shape = (T, d_in, d_out)
+        self.strategies = tuple(strategies)
+        self.params = params
+        s = _strats(strategies)
+        n = lib.adahop_linear_ctx_bytes(T, d_in, d_out, s, C.byref(params))
+        self.buf = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+        self.needs_x = bool(lib.adahop_linear_backward_needs_x(s, C.byref(params)))
+        self.x = None
+
+    @property
+    def saved_bytes(self) -> int:
+        """Device bytes kept alive between forward and backward for this linear."""
+        return self.buf.numel() + (self.x.numel() * self.x.element_size() if self.x is not None else 0)
+
+
+def split_workspace_bytes(T, d_in, d_out, strategies, params=None) -> int:
+    p = params or Params()
+    return lib.adahop_linear_split_workspace_bytes(T, d_in, d_out, _strats(strategies), C.byref(p))
+
+
+def linear_forward(x, w, strategies, params=None, out=None, out_dtype=torch.bfloat16, ws=None, ctx=None):
+    """Y = X W^T and the saved context (adahop_linear_forward). Returns (Y, ctx)."""
+    p = params or Params()
+    T, d_in = x.shape
+    d_out = w.shape[0]
+    for t in (x, w):
+        assert t.is_contiguous() and t.dtype == torch.bfloat16
+    if ctx is None or ctx.shape != (T, d_in, d_out) or ctx.strategies != tuple(strategies):
+        ctx = LinearContext(T, d_in, d_out, strategies, p, x.device)
+    ctx.params = p
+    if out is None:
+        out = torch.empty((T, d_out), dtype=out_dtype, device=x.device)
+    assert tuple(out.shape) == (T, d_out) and out.is_contiguous()
+    s = _strats(strategies)
+    n = lib.adahop_linear_split_workspace_bytes(T, d_in, d_out, s, C.byref(p))
+    wbuf = _ws(n, ws, x.device)
+    check("adahop_linear_forward",
+          lib.adahop_linear_forward(_ptr(x), _ptr(w), _ptr(out), _dt(out), T, d_in, d_out, s, C.byref(p),
+                                    _ptr(ctx.buf), ctx.buf.numel(), _ptr(wbuf), wbuf.numel(), _stream()))
+    ctx.x = x if ctx.needs_x else None
+    return out, ctx
+
+
+def linear_backward(gy, w, ctx: LinearContext, out=None, gx_dtype=torch.bfloat16, gw_dtype=torch.float32,
+                    ws=None):
+    """G_X = G_Y W and G_W = G_Y^T X from the saved context (adahop_linear_backward)."""
+    T, d_in, d_out = ctx.shape
+    p = ctx.params
+    for t in (gy, w):
+        assert t.is_contiguous() and t.dtype == torch.bfloat16
+    assert tuple(gy.shape) == (T, d_out) and tuple(w.shape) == (d_out, d_in)
+    if out is None:
+        out = (torch.empty((T, d_in), dtype=gx_dtype, device=gy.device),
+               torch.empty((d_out, d_in), dtype=gw_dtype, device=gy.device))
+    gx, gw = out
+    assert tuple(gx.shape) == (T, d_in) and tuple(gw.shape) == (d_out, d_in)
+    assert gx.is_contiguous() and gw.is_contiguous()
+    s = _strats(ctx.strategies)
+    n = lib.adahop_linear_split_workspace_bytes(T, d_in, d_out, s, C.byref(p))
+    wbuf = _ws(n, ws, gy.device)
+    check("adahop_linear_backward",
+          lib.adahop_linear_backward(_ptr(gy), _ptr(w), _ptr(ctx.x), _ptr(gx), _ptr(gw), _dt(gx), _dt(gw), T, d_in,
+                                     d_out, s, C.byref(p), _ptr(ctx.buf), ctx.buf.numel(), _ptr(wbuf),
+                                     wbuf.numel(), _stream()))
+    return gx, gw

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <initializer_list>
 #include <mutex>
 
 #include "../../include/adahop.h"
@@ -88,10 +89,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // MXFP4 GEMM kernel choice: ADAHOP_GEMM_VARIANT = 1 (1-CTA 128x128), 128 or 256 (CTA pairs).
 int gemm_variant() {
-  static int v = [] {
-    const char* e = getenv("ADAHOP_GEMM_VARIANT");
-    return e ? atoi(e) : 256;
-  }();
+  static const int v = knob("ADAHOP_GEMM_VARIANT", 256);
   return v;
 }
 
@@ -170,8 +168,13 @@ adahop_status_t validate_params(const adahop_params_t* p) {
 
 // ============================================================================ PDL switch
 namespace adahop {
+int current_device() {
+  int d = -1;
+  return cudaGetDevice(&d) == cudaSuccess && d >= 0 && d < 64 ? d : -1;
+}
+
 bool pdl_enabled() {
-  static const bool on = [] { const char* e = getenv("ADAHOP_PDL"); return !(e && e[0] == '0'); }();
+  static const bool on = knob("ADAHOP_PDL", 1) != 0;
   return on;
 }
 }  // namespace adahop
@@ -236,10 +239,12 @@ adahop_strategy_t adahop_strategy_for_pair(adahop_pattern_t l, adahop_pattern_t 
 }
 
 adahop_pattern_t adahop_majority_vote(const int32_t* per_step, int32_t n) {
-  if (!per_step || n <= 0) return ADAHOP_PAT_NONE;
+  if (!per_step || n <= 0) return ADAHOP_PAT_INVALID;
   int cnt[3] = {0, 0, 0};
-  for (int i = 0; i < n; ++i)
-    if (per_step[i] >= 0 && per_step[i] <= 2) cnt[per_step[i]]++;
+  for (int i = 0; i < n; ++i) {
+    if (per_step[i] < 0 || per_step[i] > 2) return ADAHOP_PAT_INVALID;
+    cnt[per_step[i]]++;
+  }
   const int best = std::max(cnt[0], std::max(cnt[1], cnt[2]));
   if (cnt[ADAHOP_PAT_ROW] == best) return ADAHOP_PAT_ROW;
   if (cnt[ADAHOP_PAT_COL] == best) return ADAHOP_PAT_COL;
@@ -287,6 +292,18 @@ adahop_status_t adahop_classify(const double* row_stats, int64_t rows, const dou
   ADAHOP_LAUNCH(launch_classify(row_stats, rows, cols, col_stats, cols, col_count, double(p->eps),
                                 double(p->tau), d_cv, d_pattern,
                                 reinterpret_cast<cudaStream_t>(stream)));
+  g_launches = 1;
+  return ADAHOP_OK;
+}
+
+adahop_status_t adahop_classify_sums(double* d_cv, int64_t rows_global, int64_t cols, const adahop_params_t* p,
+                                     uint8_t* d_pattern, adahop_stream_t stream) {
+  if (!d_cv || !d_pattern || !p) return ADAHOP_E_INVALID_ARG;
+  if (rows_global <= 0 || cols <= 0) return ADAHOP_E_SHAPE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  ADAHOP_LAUNCH(launch_classify_sums(d_cv, rows_global, cols, double(p->tau), d_pattern,
+                                     reinterpret_cast<cudaStream_t>(stream)));
   g_launches = 1;
   return ADAHOP_OK;
 }
@@ -449,32 +466,52 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
 
 // ------------------------------------------------------------------------ layer step
 // One linear layer's three matmuls with each operand tensor read ONCE by the
-// dual-orientation quantiser (X: fwd + wgrad, W: fwd + dgrad, G_Y: dgrad + wgrad).
+// dual-orientation quantiser (X: fwd + wgrad, W: fwd + dgrad, G_Y: dgrad + wgrad), either in one
+// call (adahop_linear_layer) or split into the forward and the backward of a training step
+// (adahop_linear_forward / adahop_linear_backward) with a caller-owned context in between.
 }  // extern "C"
 
 namespace {
+
+// A carved buffer: byte offset in the workspace (space 0) or in the saved context (space 1).
+struct Buf {
+  size_t off = 0;
+  int space = 0;
+};
 
 struct LayerPlan {
   // per tensor (0 = X [T x d_in], 1 = W [d_out x d_in], 2 = G_Y [T x d_out])
   int64_t R[3], C[3];
   bool need_row[3], need_col[3];
-  size_t q_row[3], sf_row[3], q_col[3], sf_col[3];
+  Buf q_row[3], sf_row[3], q_col[3], sf_col[3];
   // masks: which FOID feeds which (tensor, orientation)
   int kk_row[3], kk_col[3];
-  size_t idx_row[3], idx_col[3], slice_row[3], slice_col[3];
-  size_t keys_row[3], keys_col[3];   // per-FOID scratch
-  size_t part[3], dt[3];               // per-path outlier split-K partials and folded Dt
+  Buf idx_row[3], idx_col[3], slice_row[3], slice_col[3];
+  Buf keys_row[3], keys_col[3];   // per-FOID scratch
+  Buf part[3], dt[3];             // per-path outlier split-K partials and folded Dt
   int splits[3];
   int64_t npad[3], mbig[3];
-  size_t total = 0;
+  size_t ws_total = 0, ctx_total = 0;
+};
+
+struct Spaces {
+  uint8_t* base[2];
+  template <typename T>
+  T* p(const Buf& b) const { return reinterpret_cast<T*>(base[b.space] + b.off); }
 };
 
 // path p: (A tensor, A orientation, B tensor, B orientation); orientation 0 = row, 1 = col
 constexpr int kPathA[3] = {0, 2, 2}, kPathAo[3] = {0, 0, 1};
 constexpr int kPathB[3] = {1, 1, 0}, kPathBo[3] = {0, 1, 1};
+// phases: the forward prepares X and W and runs path 0; the backward prepares G_Y and runs 1, 2
+constexpr int kFwd = 1, kBwd = 2;
+inline int tensor_phase(int t) { return t == 2 ? kBwd : kFwd; }
+inline int path_phase(int path) { return path == 0 ? kFwd : kBwd; }
 
+// split: the buffers the forward produces for the backward — the column (K = tokens / d_out)
+// FP4 layouts of X and W with their OE indices and BF16 slices — are carved in the context.
 void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p,
-                int sms, LayerPlan* L) {
+                int sms, bool split, LayerPlan* L) {
   *L = LayerPlan{};
   L->R[0] = T; L->C[0] = d_in;
   L->R[1] = d_out; L->C[1] = d_in;
@@ -494,23 +531,27 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
       (o ? L->kk_col : L->kk_row)[t] = kk;
     }
   }
-  Carver c;
+  Carver c[2];
+  auto take = [&](Buf& b, size_t bytes, bool ctx) {
+    b.space = ctx ? 1 : 0;
+    b.off = c[b.space].take(bytes);
+  };
   for (int t = 0; t < 3; ++t) {
     const int64_t R = L->R[t], C = L->C[t];
-    if (L->need_row[t]) { L->q_row[t] = c.take(size_t(R) * size_t(C / 2)); L->sf_row[t] = c.take(size_t(sf_bytes(R, C))); }
-    if (L->need_col[t]) { L->q_col[t] = c.take(size_t(C) * size_t(R / 2)); L->sf_col[t] = c.take(size_t(sf_bytes(C, R))); }
+    const bool keep = split && t != 2;   // X / W column layouts outlive the forward
+    if (L->need_row[t]) { take(L->q_row[t], size_t(R) * size_t(C / 2), false); take(L->sf_row[t], size_t(sf_bytes(R, C)), false); }
+    if (L->need_col[t]) { take(L->q_col[t], size_t(C) * size_t(R / 2), keep); take(L->sf_col[t], size_t(sf_bytes(C, R)), keep); }
     if (L->kk_row[t]) {
-      L->idx_row[t] = c.take(size_t(L->kk_row[t]) * 4);
-      L->slice_row[t] = c.take(size_t(L->kk_row[t]) * size_t(C) * 2);
-      L->keys_row[t] = c.take(foid_ws_bytes(R));
+      take(L->idx_row[t], size_t(L->kk_row[t]) * 4, false);
+      take(L->slice_row[t], size_t(L->kk_row[t]) * size_t(C) * 2, false);
+      take(L->keys_row[t], foid_ws_bytes(R), false);
     }
     if (L->kk_col[t]) {
-      L->idx_col[t] = c.take(size_t(L->kk_col[t]) * 4);
-      L->slice_col[t] = c.take(size_t(L->kk_col[t]) * size_t(R) * 2);
-      L->keys_col[t] = c.take(foid_ws_bytes(C));
+      take(L->idx_col[t], size_t(L->kk_col[t]) * 4, keep);
+      take(L->slice_col[t], size_t(L->kk_col[t]) * size_t(R) * 2, keep);
+      take(L->keys_col[t], foid_ws_bytes(C), false);
     }
   }
-
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   for (int path = 0; path < 3; ++path) {
     L->splits[path] = 1; L->npad[path] = 0; L->mbig[path] = 0;
@@ -521,70 +562,67 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     L->mbig[path] = left ? MNK[path][1] : MNK[path][0];
     L->npad[path] = bf16_gemm_npad(kk);
     L->splits[path] = bf16_gemm_splits(L->mbig[path], MNK[path][2], sms);
-    L->part[path] = c.take(size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4);
-    L->dt[path] = c.take(size_t(kk) * size_t(L->mbig[path]) * 4);
+    take(L->part[path], size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4, false);
+    take(L->dt[path], size_t(kk) * size_t(L->mbig[path]) * 4, false);
   }
-  L->total = c.take(0) + 256;
+  L->ws_total = c[0].take(0) + 256;
+  L->ctx_total = split ? c[1].take(0) + 256 : 0;
 }
 
-}  // namespace
-
-extern "C" {
-
-size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
-                                    const adahop_params_t* p) {
-  if (!s || !p || T <= 0 || d_in <= 0 || d_out <= 0) return 0;
-  DevInfo d = dev_info();
-  LayerPlan L;
-  plan_layer(T, d_in, d_out, s, p, d.ok ? d.sms : 148, &L);
-  return L.total;
+// The backward reads the full X in BF16 only for a wgrad whose BF16 part multiplies by all of X:
+// OE-Left (A_out . B with B = X) and the Lv2 BF16 wgrad. Everything else the
+// backward needs from the forward is in the context (FP4 + BF16 outlier slices).
+bool backward_needs_x(const adahop_strategy_t* s, const adahop_params_t* p) {
+  return s[2] == ADAHOP_BF16 || (s[2] == ADAHOP_OE_LEFT_IHT && p->oe_k > 0);
 }
 
-adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
-                                    adahop_dtype_t out_dt, int64_t T, int64_t d_in, int64_t d_out,
-                                    const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
-                                    size_t ws_bytes, adahop_stream_t stream) {
-  if (!X || !W || !GY || !Y || !GX || !GW || !s || !p) return ADAHOP_E_INVALID_ARG;
+adahop_status_t check_layer_args(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                 const adahop_params_t* p, std::initializer_list<const void*> ptrs) {
+  if (!s || !p) return ADAHOP_E_INVALID_ARG;
   adahop_status_t st = validate_params(p);
   if (st != ADAHOP_OK) return st;
   for (int i = 0; i < 3; ++i)
     if (s[i] < ADAHOP_IHT || s[i] > ADAHOP_BF16) return ADAHOP_E_INVALID_ARG;
-  if (out_dt != ADAHOP_DT_BF16 && out_dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
   if (T <= 0 || d_in <= 0 || d_out <= 0) return ADAHOP_E_SHAPE;
   if (T % 32 || d_in % 32 || d_out % 32) return ADAHOP_E_SHAPE;
-  if ((d_in % 8) || (d_out % 8)) return ADAHOP_E_INVALID_ARG;
-  for (const void* q : {X, W, GY, static_cast<const void*>(Y), static_cast<const void*>(GX), static_cast<const void*>(GW)})
-    if (!aligned16(q)) return ADAHOP_E_INVALID_ARG;
+  for (const void* q : ptrs)
+    if (!q || !aligned16(q)) return ADAHOP_E_INVALID_ARG;
   if (T * (std::max(d_in, d_out) / 64 + 1) >= (int64_t(1) << 31)) return ADAHOP_E_UNSUPPORTED;
-  DevInfo dev;
-  st = check_device(&dev);
-  if (st != ADAHOP_OK) return st;
-  LayerPlan L;
-  plan_layer(T, d_in, d_out, s, p, dev.sms, &L);
-  if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  return ADAHOP_OK;
+}
+
+adahop_status_t check_oe_rows(const LayerPlan& L, int phases) {
   for (int t = 0; t < 3; ++t) {
+    if (!(tensor_phase(t) & phases)) continue;
     if (L.kk_row[t] && L.R[t] > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
     if (L.kk_col[t] && L.C[t] > kFoidMaxRows) return ADAHOP_E_UNSUPPORTED;
   }
-  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  const bool out_f32 = out_dt == ADAHOP_DT_F32;
+  return ADAHOP_OK;
+}
+
+// The layer's kernels for the given phases. Inputs a phase does not use may be NULL; out[path]
+// is written in odt[path].
+adahop_status_t run_layer(int phases, const void* X, const void* W, const void* GY, void* const out[3],
+                          const adahop_dtype_t odt[3], int64_t T, int64_t d_in, int64_t d_out,
+                          const adahop_strategy_t* s, const adahop_params_t* p, const LayerPlan& L,
+                          const Spaces& sp, int sms, cudaStream_t cs) {
   const __nv_bfloat16* src[3] = {static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W),
                                  static_cast<const __nv_bfloat16*>(GY)};
   int32_t launches = 0;
   stage_mark(0, cs);
-  // ---- 1. FOID for every OE operand: row orientation = rows of the tensor
-  //         (K-contiguous probe), column orientation = columns (probe = first 64 rows)
+  // ---- 1. FOID for every OE operand of these phases: row orientation = rows of the
+  //         tensor (K-contiguous probe), column orientation = columns (probe = first 64 rows)
   {
     FoidJob jobs[kFoidMaxJobs];
     int nj = 0;
     for (int t = 0; t < 3; ++t) {
+      if (!(tensor_phase(t) & phases)) continue;
       if (L.kk_row[t])
         jobs[nj++] = FoidJob{src[t], L.R[t], L.C[t], L.C[t], 0, L.kk_row[t], p->foid_probe,
-                             reinterpret_cast<double*>(w + L.keys_row[t]), reinterpret_cast<int32_t*>(w + L.idx_row[t])};
+                             sp.p<double>(L.keys_row[t]), sp.p<int32_t>(L.idx_row[t])};
       if (L.kk_col[t])
         jobs[nj++] = FoidJob{src[t], L.C[t], L.R[t], L.C[t], 1, L.kk_col[t], p->foid_probe,
-                             reinterpret_cast<double*>(w + L.keys_col[t]), reinterpret_cast<int32_t*>(w + L.idx_col[t])};
+                             sp.p<double>(L.keys_col[t]), sp.p<int32_t>(L.idx_col[t])};
     }
     if (nj) {
       ADAHOP_LAUNCH(launch_foid_batch(jobs, nj, false, cs));
@@ -598,6 +636,7 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
   int n_tc = 0;
   bool in_tc[3] = {false, false, false};
   for (int t = 0; t < 3; ++t) {
+    if (!(tensor_phase(t) & phases)) continue;
     const int64_t R = L.R[t], C = L.C[t];
     if (!(L.need_row[t] && L.need_col[t]) || !quant_use_tc() ||
         !quant_tc_supported(R, C, C, src[t], L.kk_row[t] > 0, L.kk_col[t] > 0))
@@ -605,50 +644,47 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
     in_tc[t] = true;
     tc_jobs[n_tc++] = QuantTcJob{
         src[t], R, C, C,
-        L.kk_row[t] ? reinterpret_cast<const int32_t*>(w + L.idx_row[t]) : nullptr, L.kk_row[t],
-        L.kk_row[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_row[t]) : nullptr, w + L.q_row[t], w + L.sf_row[t],
+        L.kk_row[t] ? sp.p<const int32_t>(L.idx_row[t]) : nullptr, L.kk_row[t],
+        L.kk_row[t] ? sp.p<__nv_bfloat16>(L.slice_row[t]) : nullptr, sp.p<uint8_t>(L.q_row[t]), sp.p<uint8_t>(L.sf_row[t]),
         nullptr,
-        L.kk_col[t] ? reinterpret_cast<const int32_t*>(w + L.idx_col[t]) : nullptr, L.kk_col[t],
-        L.kk_col[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_col[t]) : nullptr, w + L.q_col[t], w + L.sf_col[t],
+        L.kk_col[t] ? sp.p<const int32_t>(L.idx_col[t]) : nullptr, L.kk_col[t],
+        L.kk_col[t] ? sp.p<__nv_bfloat16>(L.slice_col[t]) : nullptr, sp.p<uint8_t>(L.q_col[t]), sp.p<uint8_t>(L.sf_col[t]),
         nullptr};
-    if ((R % 128) || (C % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_row[t], 0, size_t(sf_bytes(R, C)), cs));
-    if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
+    if ((R % 128) || (C % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_row[t]), 0, size_t(sf_bytes(R, C)), cs));
+    if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_col[t]), 0, size_t(sf_bytes(C, R)), cs));
   }
   if (n_tc) {
     int nl = 0;
-    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, dev.sms, cs, &nl));
+    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, sms, cs, &nl));
     launches += nl;
   }
   for (int t = 0; t < 3; ++t) {
-    if (in_tc[t]) continue;
+    if (!(tensor_phase(t) & phases) || in_tc[t]) continue;
     const int64_t R = L.R[t], C = L.C[t];
-    const int32_t* rz = L.kk_row[t] ? reinterpret_cast<const int32_t*>(w + L.idx_row[t]) : nullptr;
-    const int32_t* cz = L.kk_col[t] ? reinterpret_cast<const int32_t*>(w + L.idx_col[t]) : nullptr;
-    __nv_bfloat16* srow = L.kk_row[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_row[t]) : nullptr;
-    __nv_bfloat16* scol = L.kk_col[t] ? reinterpret_cast<__nv_bfloat16*>(w + L.slice_col[t]) : nullptr;
-    if (L.need_row[t] && ((R % 128) || (C % 256)))
-      ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_row[t], 0, size_t(sf_bytes(R, C)), cs));
-    if (L.need_col[t] && ((C % 128) || (R % 256)))
-      ADAHOP_LAUNCH(cudaMemsetAsync(w + L.sf_col[t], 0, size_t(sf_bytes(C, R)), cs));
+    const int32_t* rz = L.kk_row[t] ? sp.p<const int32_t>(L.idx_row[t]) : nullptr;
+    const int32_t* cz = L.kk_col[t] ? sp.p<const int32_t>(L.idx_col[t]) : nullptr;
+    __nv_bfloat16* srow = L.kk_row[t] ? sp.p<__nv_bfloat16>(L.slice_row[t]) : nullptr;
+    __nv_bfloat16* scol = L.kk_col[t] ? sp.p<__nv_bfloat16>(L.slice_col[t]) : nullptr;
+    uint8_t *qr = sp.p<uint8_t>(L.q_row[t]), *sr = sp.p<uint8_t>(L.sf_row[t]);
+    uint8_t *qc = sp.p<uint8_t>(L.q_col[t]), *sc = sp.p<uint8_t>(L.sf_col[t]);
+    if (L.need_row[t] && ((R % 128) || (C % 256))) ADAHOP_LAUNCH(cudaMemsetAsync(sr, 0, size_t(sf_bytes(R, C)), cs));
+    if (L.need_col[t] && ((C % 128) || (R % 256))) ADAHOP_LAUNCH(cudaMemsetAsync(sc, 0, size_t(sf_bytes(C, R)), cs));
     if (L.need_row[t] && L.need_col[t] && dual_quant_supported(R, C, rz != nullptr, cz != nullptr)) {
-      ADAHOP_LAUNCH(launch_iht_quant_dual(src[t], R, C, C, rz, L.kk_row[t], srow, w + L.q_row[t], w + L.sf_row[t],
-                                          cz, L.kk_col[t], scol, w + L.q_col[t], w + L.sf_col[t], dev.sms, cs));
+      ADAHOP_LAUNCH(launch_iht_quant_dual(src[t], R, C, C, rz, L.kk_row[t], srow, qr, sr, cz, L.kk_col[t], scol, qc, sc,
+                                          sms, cs));
       launches += quant_last_launches();
     } else {
       if (L.need_row[t]) {
-        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], w + L.q_row[t], w + L.sf_row[t],
-                                       nullptr, srow, false, dev.sms, cs));
+        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, R, C, C, 0, rz, L.kk_row[t], qr, sr, nullptr, srow, false, sms, cs));
         launches += quant_last_launches();
       }
       if (L.need_col[t]) {
-        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], w + L.q_col[t], w + L.sf_col[t],
-                                       nullptr, scol, false, dev.sms, cs));
+        ADAHOP_LAUNCH(launch_iht_quant(src[t], false, C, R, C, 1, cz, L.kk_col[t], qc, sc, nullptr, scol, false, sms, cs));
         launches += quant_last_launches();
       }
     }
   }
   stage_mark(2, cs);
-  void* out[3] = {Y, GX, GW};
   const int64_t MNK[3][3] = {{T, d_out, d_in}, {T, d_in, d_out}, {d_out, d_in, T}};
   const int64_t ldc[3] = {d_out, d_in, d_in};
   // raw operand views per path: A_store / B_store as (ptr, kstrided, ld)
@@ -661,50 +697,160 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
   // ---- 3. BF16 outlier GEMMs: split-K partials, written into C by the MXFP4 GEMM epilogue
   OePatch patch[3] = {};
   for (int path = 0; path < 3; ++path) {
-    if (L.mbig[path] == 0) continue;
+    if (!(path_phase(path) & phases) || L.mbig[path] == 0) continue;
     const bool left = s[path] == ADAHOP_OE_LEFT_IHT;
     const int t = left ? kPathA[path] : kPathB[path];
     const bool col = left ? kPathAo[path] : kPathBo[path];
     const int kk = col ? L.kk_col[t] : L.kk_row[t];
-    const int32_t* idx = reinterpret_cast<const int32_t*>(w + (col ? L.idx_col[t] : L.idx_row[t]));
-    const __nv_bfloat16* slice = reinterpret_cast<const __nv_bfloat16*>(w + (col ? L.slice_col[t] : L.slice_row[t]));
+    const int32_t* idx = sp.p<const int32_t>(col ? L.idx_col[t] : L.idx_row[t]);
+    const __nv_bfloat16* slice = sp.p<const __nv_bfloat16>(col ? L.slice_col[t] : L.slice_row[t]);
     Bf16GemmArgs ga{};
     if (!left) { ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path]; }
     else { ga.A = static_cast<const __nv_bfloat16*>(rawB[path]); ga.a_mn = rawBks[path]; ga.lda = rawBld[path]; }
     ga.B = slice; ga.b_mn = 0; ga.ldb = MNK[path][2];
     ga.Mb = L.mbig[path]; ga.Nb = kk; ga.K = MNK[path][2]; ga.mode = 1;
-    ga.part = reinterpret_cast<float*>(w + L.part[path]); ga.splits = L.splits[path]; ga.npad = L.npad[path];
+    ga.part = sp.p<float>(L.part[path]); ga.splits = L.splits[path]; ga.npad = L.npad[path];
     ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
-    float* Dt = reinterpret_cast<float*>(w + L.dt[path]);
+    float* Dt = sp.p<float>(L.dt[path]);
     ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, kk, Dt, cs));
     launches += 2;
     patch[path] = OePatch{Dt, idx, ga.Mb, kk, left ? 2 : 1};
   }
   stage_mark(3, cs);
-  // ---- 4. the three MXFP4 GEMMs (or BF16 for Lv2 CC); the epilogue writes the outlier entries
+  // ---- 4. the MXFP4 GEMMs (or BF16 for Lv2 CC); the epilogue writes the outlier entries
   for (int path = 0; path < 3; ++path) {
+    if (!(path_phase(path) & phases)) continue;
     const int64_t M = MNK[path][0], N = MNK[path][1], K = MNK[path][2];
+    const bool f32 = odt[path] == ADAHOP_DT_F32;
     if (s[path] == ADAHOP_BF16) {
       Bf16GemmArgs ga{};
       ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path];
       ga.B = static_cast<const __nv_bfloat16*>(rawB[path]); ga.b_mn = rawBks[path]; ga.ldb = rawBld[path];
-      ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = out[path]; ga.out_f32 = out_f32; ga.ldc = ldc[path];
+      ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = out[path]; ga.out_f32 = f32; ga.ldc = ldc[path];
       ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
       launches += 1;
       continue;
     }
     const int ta = kPathA[path], tb = kPathB[path];
-    const uint8_t* qa = w + (kPathAo[path] ? L.q_col[ta] : L.q_row[ta]);
-    const uint8_t* qa_sf = w + (kPathAo[path] ? L.sf_col[ta] : L.sf_row[ta]);
-    const uint8_t* qb = w + (kPathBo[path] ? L.q_col[tb] : L.q_row[tb]);
-    const uint8_t* qb_sf = w + (kPathBo[path] ? L.sf_col[tb] : L.sf_row[tb]);
-    Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], out_f32, ldc[path], M, N, K, patch[path]};
-    ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
+    const uint8_t* qa = sp.p<const uint8_t>(kPathAo[path] ? L.q_col[ta] : L.q_row[ta]);
+    const uint8_t* qa_sf = sp.p<const uint8_t>(kPathAo[path] ? L.sf_col[ta] : L.sf_row[ta]);
+    const uint8_t* qb = sp.p<const uint8_t>(kPathBo[path] ? L.q_col[tb] : L.q_row[tb]);
+    const uint8_t* qb_sf = sp.p<const uint8_t>(kPathBo[path] ? L.sf_col[tb] : L.sf_row[tb]);
+    Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], f32, ldc[path], M, N, K, patch[path]};
+    ADAHOP_LAUNCH(run_gemm_mxf4(ma, sms, cs));
     launches += 1;
   }
   stage_mark(4, cs);
   g_launches = launches;
   return ADAHOP_OK;
+}
+
+inline bool valid_dt(adahop_dtype_t d) { return d == ADAHOP_DT_BF16 || d == ADAHOP_DT_F32; }
+
+}  // namespace
+
+extern "C" {
+
+size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                    const adahop_params_t* p) {
+  if (!s || !p || T <= 0 || d_in <= 0 || d_out <= 0) return 0;
+  DevInfo d = dev_info();
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, d.ok ? d.sms : 148, false, &L);
+  return L.ws_total;
+}
+
+adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
+                                    adahop_dtype_t out_dt, adahop_dtype_t gw_dt, int64_t T, int64_t d_in,
+                                    int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p, void* ws,
+                                    size_t ws_bytes, adahop_stream_t stream) {
+  if (!valid_dt(out_dt) || !valid_dt(gw_dt)) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_layer_args(T, d_in, d_out, s, p, {X, W, GY, Y, GX, GW});
+  if (st != ADAHOP_OK) return st;
+  DevInfo dev;
+  st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, dev.sms, false, &L);
+  if (!ws || ws_bytes < L.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  st = check_oe_rows(L, kFwd | kBwd);
+  if (st != ADAHOP_OK) return st;
+  void* const out[3] = {Y, GX, GW};
+  const adahop_dtype_t odt[3] = {out_dt, out_dt, gw_dt};
+  const Spaces sp{{static_cast<uint8_t*>(ws), nullptr}};
+  return run_layer(kFwd | kBwd, X, W, GY, out, odt, T, d_in, d_out, s, p, L, sp, dev.sms,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t adahop_linear_ctx_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                               const adahop_params_t* p) {
+  if (!s || !p || T <= 0 || d_in <= 0 || d_out <= 0) return 0;
+  DevInfo d = dev_info();
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, d.ok ? d.sms : 148, true, &L);
+  return L.ctx_total;
+}
+
+size_t adahop_linear_split_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                           const adahop_params_t* p) {
+  if (!s || !p || T <= 0 || d_in <= 0 || d_out <= 0) return 0;
+  DevInfo d = dev_info();
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, d.ok ? d.sms : 148, true, &L);
+  return L.ws_total;
+}
+
+int32_t adahop_linear_backward_needs_x(const adahop_strategy_t* s, const adahop_params_t* p) {
+  if (!s || !p) return 0;
+  return backward_needs_x(s, p) ? 1 : 0;
+}
+
+adahop_status_t adahop_linear_forward(const void* X, const void* W, void* Y, adahop_dtype_t out_dt, int64_t T,
+                                      int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
+                                      const adahop_params_t* p, void* ctx, size_t ctx_bytes, void* ws,
+                                      size_t ws_bytes, adahop_stream_t stream) {
+  if (!valid_dt(out_dt)) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_layer_args(T, d_in, d_out, s, p, {X, W, Y});
+  if (st != ADAHOP_OK) return st;
+  DevInfo dev;
+  st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, dev.sms, true, &L);
+  if (!ws || ws_bytes < L.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  if (!ctx || ctx_bytes < L.ctx_total || (reinterpret_cast<uintptr_t>(ctx) & 255)) return ADAHOP_E_WORKSPACE;
+  st = check_oe_rows(L, kFwd);
+  if (st != ADAHOP_OK) return st;
+  void* const out[3] = {Y, nullptr, nullptr};
+  const adahop_dtype_t odt[3] = {out_dt, out_dt, out_dt};
+  const Spaces sp{{static_cast<uint8_t*>(ws), static_cast<uint8_t*>(ctx)}};
+  return run_layer(kFwd, X, W, nullptr, out, odt, T, d_in, d_out, s, p, L, sp, dev.sms,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+adahop_status_t adahop_linear_backward(const void* GY, const void* W, const void* X, void* GX, void* GW,
+                                       adahop_dtype_t gx_dt, adahop_dtype_t gw_dt, int64_t T, int64_t d_in,
+                                       int64_t d_out, const adahop_strategy_t* s, const adahop_params_t* p,
+                                       const void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes,
+                                       adahop_stream_t stream) {
+  if (!valid_dt(gx_dt) || !valid_dt(gw_dt)) return ADAHOP_E_INVALID_ARG;
+  adahop_status_t st = check_layer_args(T, d_in, d_out, s, p, {GY, W, GX, GW});
+  if (st != ADAHOP_OK) return st;
+  if (backward_needs_x(s, p) ? (!X || !aligned16(X)) : false) return ADAHOP_E_INVALID_ARG;
+  DevInfo dev;
+  st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  LayerPlan L;
+  plan_layer(T, d_in, d_out, s, p, dev.sms, true, &L);
+  if (!ws || ws_bytes < L.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255)) return ADAHOP_E_WORKSPACE;
+  if (!ctx || ctx_bytes < L.ctx_total || (reinterpret_cast<uintptr_t>(ctx) & 255)) return ADAHOP_E_WORKSPACE;
+  st = check_oe_rows(L, kBwd);
+  if (st != ADAHOP_OK) return st;
+  void* const out[3] = {nullptr, GX, GW};
+  const adahop_dtype_t odt[3] = {gx_dt, gx_dt, gw_dt};
+  const Spaces sp{{static_cast<uint8_t*>(ws), static_cast<uint8_t*>(const_cast<void*>(ctx))}};
+  return run_layer(kBwd, backward_needs_x(s, p) ? X : nullptr, W, GY, out, odt, T, d_in, d_out, s, p, L, sp, dev.sms,
+                   reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t adahop_workspace_bytes(adahop_path_t path, int64_t T, int64_t d_in, int64_t d_out,

@@ -283,13 +283,11 @@ static cudaError_t launch_bn(const Bf16GemmArgs& a, cudaStream_t st) {
                       uint64_t(a.ldb) * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(bf16g::k_gemm_bf16<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ae = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(bf16g::k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+  });
+  if (ae != cudaSuccess) return ae;
   const int splits = a.mode == 1 ? a.splits : 1;
   dim3 grid(unsigned((a.Mb + bf16g::BM - 1) / bf16g::BM),
             unsigned(a.mode == 1 ? 1 : (a.Nb + BN - 1) / BN), unsigned(splits));

@@ -240,13 +240,11 @@ cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st
   if (!make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
                     uint64_t(a.K / 2), 128, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_mxf4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSmemBytes));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ae = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(k_gemm_mxf4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+  });
+  if (ae != cudaSuccess) return ae;
   const int64_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int grid = int(tiles < num_sms ? tiles : num_sms);
   return launch_k(k_gemm_mxf4, dim3(grid), dim3(kThreads), kSmemBytes, st, 1, tma, tmb, a.a_sf, a.b_sf, a.C,

@@ -20,7 +20,7 @@
 #define GEMM_TRACE 0
 #endif
 // Experiment knob (never set in the product build): bit 0 skips the scale-factor tcgen05.cp,
-// bit 1 the MMAs, bit 2 the scale-factor TMA loads, bit 3 the epilogue stores.
+// bit 1 the MMAs, bit 2 the scale-factor TMA loads, bit 3 the epilogue stores, bit 4 the A/B TMA loads.
 #ifndef GEMM_ABLATE
 #define GEMM_ABLATE 0
 #endif
@@ -39,6 +39,14 @@ constexpr int BK = 256;  // fp4 elements per stage
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 
+// TMEM columns (512 per SM). BN = 128: two disjoint 128-column accumulators, scale factors at
+// 256.. in two alternating sets. BN = 256, BUFS = 2: two OVERLAPPING 256-column accumulators,
+// acc0 = [0, 256) and acc1 = [224, 480) (they share columns [224, 256)), one scale-factor set at
+// 480.. (tcgen05.cp and tcgen05.mma issued by one thread execute in issue order, so the copy for
+// k-step ks+1 cannot overwrite scale factors the MMAs of k-step ks still read). The epilogue
+// drains the shared 32 columns first and releases them on `tovl`: the next tile's MMAs start
+// after ~1/8 of the drain instead of after all of it. BN = 256, BUFS = 1: the single-accumulator
+// layout (experiment builds: ADAHOP_GEMM_OVL=0).
 template <int BN, int BUFS>
 struct Cfg {
   static constexpr int kA = 128 * BK / 2;             // 16 KB: this CTA's 128 rows of A
@@ -48,12 +56,16 @@ struct Cfg {
   static constexpr int kStage = kA + kB + kSfa + kSfb;
   static constexpr int kStages = BN == 256 ? 5 : 7;
   static constexpr int kEpiBufs = 1;
-  static constexpr int kAccCols = BN;
-  static constexpr int kSfaCol = 256;                 // after the accumulator buffers
-  static constexpr int kSfbCol = 264;
-  static constexpr int kSfSet = 32;                   // second scale-factor column set
+  static constexpr bool kOverlap = BN == 256 && BUFS == 2;
+  static constexpr int kOvlCols = 32;                 // columns shared by the two accumulators
+  static constexpr int kAccCols = kOverlap ? BN - kOvlCols : BN;   // column stride between accumulators
+  static constexpr int kSfaCol = kOverlap ? 480 : 256;            // after the accumulator buffers
+  static constexpr int kSfbCol = kSfaCol + 8;
+  static constexpr int kSfSets = kOverlap ? 1 : 2;
+  static constexpr int kSfSet = 32;                   // second scale-factor column set (kSfSets == 2)
   static constexpr size_t kSmem = size_t(kStages) * kStage + kEpiWarps * kEpiBufs * kEpiStageBytes + 1024 + 512;
-  static_assert(BUFS * BN <= 256, "accumulators must fit below the scale-factor columns");
+  static_assert(kOverlap || BUFS * BN <= 256, "accumulators must fit below the scale-factor columns");
+  static_assert(kSfbCol + 2 * (BN / 32) * (kSfSets == 2 ? 2 : 1) <= 512 || kSfSets == 2, "TMEM overflow");
 };
 
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
@@ -91,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + G::kStages;
   uint64_t* tfull = bars + 2 * G::kStages;
   uint64_t* tempty = tfull + BUFS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + BUFS);
+  uint64_t* tovl = tempty + BUFS;     // overlapping accumulators: shared columns drained (once per tile)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tovl + 1);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   constexpr int NP = PM * PN, CS = 2 * NP;
@@ -126,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 2 * kEpiWarps);
     }
+    ptx::mbar_init(tovl, 2 * 4);   // the 4 warps (one per lane quadrant) owning the shared columns, both CTAs
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
@@ -153,15 +167,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* ssfa = sb + G::kB;
         uint8_t* ssfb = ssfa + G::kSfa;
         const uint32_t fb = ptx::mapa(&full[stage], leader_rank);
-        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (GEMM_ABLATE & 4) ? 2 * (G::kA + G::kB) : 2 * G::kStage);
-        if (PN == 1) {
+        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], ((GEMM_ABLATE & 4) ? 0 : 2 * (G::kSfa + G::kSfb)) +
+                                                               ((GEMM_ABLATE & 16) ? 0 : 2 * (G::kA + G::kB)));
+        if (GEMM_ABLATE & 16) {
+        } else if (PN == 1) {
           ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + x * 128));
         } else {
           constexpr int sub = 128 / PN;
           ptx::tma_load_2d_2sm_mc(sa + pn * sub * 128, &tm_a, &full[stage], ks * (BK / 2),
                                   int32_t(mb * 256 + x * 128 + pn * sub), mask_a);
         }
-        if (PM == 1) {
+        if (GEMM_ABLATE & 16) {
+        } else if (PM == 1) {
           ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + x * (BN / 2)));
         } else {
           constexpr int sub = (BN / 2) / PM;
@@ -187,6 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t buf = uint32_t(lt % BUFS);
       const uint32_t use = uint32_t(lt / BUFS);
       ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      // the previous tile's accumulator shares columns with this one: wait until they are drained
+      if (G::kOverlap && lt > 0) ptx::mbar_wait(tovl, uint32_t((lt - 1) & 1));
       GT(0, lt);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * G::kAccCols;
@@ -200,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* ssfb = ssfa + G::kSfa;
         // scale factors alternate between two TMEM column sets by k-step parity, so the copies
         // for step ks+1 do not overwrite columns the MMAs of step ks still read
-        const uint32_t sfo = uint32_t(ks & 1) * G::kSfSet;
+        const uint32_t sfo = G::kSfSets == 2 ? uint32_t(ks & 1) * G::kSfSet : 0u;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if ((GEMM_ABLATE & 1) || !issuer) break;
@@ -243,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cols_per_grp = 128 / elt;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
     const uint32_t empty_leader = ptx::mapa(&tempty[0], leader_rank);
+    const uint32_t ovl_leader = ptx::mapa(tovl, leader_rank);
     int64_t lt = 0;
     for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
       int64_t smb, snb;
@@ -255,19 +275,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const int64_t m0 = mb * 256 + x * 128 + q * 32;
       const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
-      if (BUFS == 1 && !out_f32) {
-        // bf16 single accumulator: read both column groups out of TMEM (one through the smem
-        // stage, one in registers), hand the accumulator back, then do the global stores so
-        // that they overlap the next tile's main loop
+      // overlapping accumulators: the shared columns are the last 32 of acc0 (half 1) and the
+      // first 32 of acc1 (half 0); the warps holding them drain those first and release them
+      const bool owns_ovl = G::kOverlap && half == (buf == 0 ? 1u : 0u);
+      if (BN == 256 && !out_f32) {
+        // bf16: read both column groups out of TMEM (one through the smem stage, one in
+        // registers), hand the accumulator back, then do the global stores so that they
+        // overlap the next tile's main loop
         const uint32_t tb0 = tmem_base + ((q * 32) << 16) + buf * G::kAccCols + half * (BN / 2);
         uint32_t w0[32], w1[32];
         {
-          // all four loads in flight before the single wait: the drain time gates the next tile
           uint32_t r0[32], r1[32], r2[32], r3[32];
-          ptx::tmem_ld_32x32b_x32(tb0, r0);
-          ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
-          ptx::tmem_ld_32x32b_x32(tb0 + 64, r2);
-          ptx::tmem_ld_32x32b_x32(tb0 + 96, r3);
+          if (owns_ovl) {
+            // shared 32 columns first: the next tile's MMAs wait for exactly these
+            if (buf == 0) ptx::tmem_ld_32x32b_x32(tb0 + 96, r3);
+            else ptx::tmem_ld_32x32b_x32(tb0, r0);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ovl_leader);
+            if (buf == 0) {
+              ptx::tmem_ld_32x32b_x32(tb0, r0);
+              ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
+              ptx::tmem_ld_32x32b_x32(tb0 + 64, r2);
+            } else {
+              ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
+              ptx::tmem_ld_32x32b_x32(tb0 + 64, r2);
+              ptx::tmem_ld_32x32b_x32(tb0 + 96, r3);
+            }
+          } else {
+            // all four loads in flight before the single wait: the drain time gates the next tile
+            ptx::tmem_ld_32x32b_x32(tb0, r0);
+            ptx::tmem_ld_32x32b_x32(tb0 + 32, r1);
+            ptx::tmem_ld_32x32b_x32(tb0 + 64, r2);
+            ptx::tmem_ld_32x32b_x32(tb0 + 96, r3);
+          }
           ptx::tmem_ld_wait();
           // accumulator is in registers: hand it back to the MMA warp before packing
           ptx::tc_fence_before();
@@ -319,7 +361,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             w[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
           }
         }
-        if (g == (BN / 2) / cols_per_grp - 1) {
+        const int ngrp = (BN / 2) / cols_per_grp;
+        if (owns_ovl && g == (buf == 0 ? ngrp - 1 : 0)) {
+          // this group holds the columns shared with the other accumulator
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(ovl_leader);
+        }
+        if (g == ngrp - 1) {
           // last TMEM read of this warp: hand the accumulator back before the stores
           ptx::tc_fence_before();
           __syncwarp();
@@ -375,15 +424,18 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   if (!make_tmap_2d(&tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
                     uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
-  // resident clusters of this shape (GPC packing decides it for clusters of 4 and 8)
-  static int max_clusters = 0;
-  if (max_clusters == 0) {
+  // resident clusters of this shape (GPC packing decides it for clusters of 4 and 8), per device
+  static std::atomic<uint64_t> attr{0};
+  static PerDeviceInt cached;
+  cudaError_t ae = once_per_device(attr, [&kern] {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
-    if (e != cudaSuccess) return e;
-    if (CS > 8) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
+    if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  });
+  if (ae != cudaSuccess) return ae;
+  const int dev = current_device();   // valid: once_per_device succeeded
+  int max_clusters = cached.v[dev].load(std::memory_order_relaxed);
+  if (max_clusters <= 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(CS * (num_sms / CS)));
     cfg.blockDim = dim3(mxf4x2::kThreads);
@@ -396,9 +448,10 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
     cfg.attrs = &at;
     cfg.numAttrs = 1;
     int n = 0;
-    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
     if (e != cudaSuccess || n <= 0) n = num_sms / CS;
     max_clusters = n;
+    cached.v[dev].store(n, std::memory_order_relaxed);
   }
   const int64_t tiles = ((a.M + 256 * PM - 1) / (256 * PM)) * ((a.N + BN * PN - 1) / (BN * PN));
   const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
@@ -406,24 +459,32 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
                   tsfb, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
 
+#if ADAHOP_EXPERIMENTS
 // ADAHOP_GEMM_CLUSTER = pairs per cluster as PMxPN: 1 (1x1, default), 2 (1x2), 4 (1x4), 22 (2x2)
 static int cluster_shape() {
-  static int v = [] {
-    const char* e = getenv("ADAHOP_GEMM_CLUSTER");
-    return e ? atoi(e) : 1;
-  }();
+  static const int v = knob("ADAHOP_GEMM_CLUSTER", 1);
   return v;
 }
+#endif
 
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st) {
   if (variant != 256) return launch_2sm<128, 2, 1, 1>(a, num_sms, st);
-  switch (cluster_shape()) {
+#if ADAHOP_EXPERIMENTS
+  switch (cluster_shape()) {   // multicast clusters of CTA pairs (measured slower)
     case 2: return launch_2sm<256, 1, 1, 2>(a, num_sms, st);
     case 4: return launch_2sm<256, 1, 1, 4>(a, num_sms, st);
     case 21: return launch_2sm<256, 1, 2, 1>(a, num_sms, st);
     case 22: return launch_2sm<256, 1, 2, 2>(a, num_sms, st);
-    default: return launch_2sm<256, 1, 1, 1>(a, num_sms, st);
+    default: break;
   }
+  if (knob("ADAHOP_GEMM_OVL", -1) >= 0)
+    return knob("ADAHOP_GEMM_OVL", -1) ? launch_2sm<256, 2, 1, 1>(a, num_sms, st) : launch_2sm<256, 1, 1, 1>(a, num_sms, st);
+#endif
+  // Overlapping double accumulators (Cfg) for K >= 4096: 1-3.5 % faster there (the main loop
+  // is operand-feed bound, so the hidden accumulator drain buys little); slower for short K,
+  // where the early MMA start competes with the output stores (profiles/r02c_gemm_overlap_ab.txt)
+  if (a.K >= 4096) return launch_2sm<256, 2, 1, 1>(a, num_sms, st);
+  return launch_2sm<256, 1, 1, 1>(a, num_sms, st);
 }
 
 }  // namespace adahop

@@ -1,7 +1,9 @@
 // kernels.h — host-side launchers of the AdaHOP sm_100a kernels (internal to libadahop).
 #pragma once
 #include "epilogue.cuh"
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -9,8 +11,45 @@
 
 namespace adahop {
 
+// ------------------------------------------------------------------ host-side knobs and caches
+// Experiment knobs: read from the environment only in experiment builds (build.py --define
+// ADAHOP_EXPERIMENTS=1, used by scripts/micro); the product library always uses the defaults.
+#ifndef ADAHOP_EXPERIMENTS
+#define ADAHOP_EXPERIMENTS 0
+#endif
+inline int knob(const char* name, int dflt) {
+#if ADAHOP_EXPERIMENTS
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
+// Per-device one-time setup. cudaFuncSetAttribute (and occupancy queries) apply to the device
+// that is current at the call, so the "done" record is kept per device ordinal (bit d of the
+// mask). Concurrent first calls may both run `fn`, which must be idempotent; the mask itself is
+// atomic, so the library stays thread-safe (include/adahop.h).
+int current_device();
+template <typename Fn>
+inline cudaError_t once_per_device(std::atomic<uint64_t>& done, Fn&& fn) {
+  const int dev = current_device();
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  const uint64_t bit = uint64_t(1) << dev;
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = fn();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+// A per-device cached positive integer (0 = not computed yet).
+struct PerDeviceInt {
+  std::atomic<int> v[64];
+  PerDeviceInt() { for (auto& x : v) x.store(0); }
+};
+
 // Kernel launch with programmatic dependent launch (PDL) on the stream, optionally as 2-CTA
-// clusters. ADAHOP_PDL=0 in the environment launches without the PDL attribute.
+// clusters. (Experiment builds: ADAHOP_PDL=0 launches without the PDL attribute.)
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -55,8 +94,8 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
                                   cudaStream_t st);
 bool dual_quant_supported(int64_t R, int64_t C, bool row_mask, bool col_mask);
 // quant_tc.cu — Hadamard on the tensor cores, quantisation in the epilogue (bf16 sources).
-bool quant_use_tc();
-int quant_last_launches();   // kernels launched by the last launch_iht_quant / launch_iht_quant_dual   // ADAHOP_QUANT_IMPL=scalar selects the butterfly kernels
+bool quant_use_tc();   // experiment builds: ADAHOP_QUANT_SCALAR=1 selects the butterfly kernels
+int quant_last_launches();   // kernels launched by the last launch_iht_quant / launch_iht_quant_dual
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask);
 struct QuantTcJob {
   const __nv_bfloat16* in; int64_t R, C, ld;
@@ -96,6 +135,8 @@ cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, 
                              cudaStream_t st);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);
+cudaError_t launch_classify_sums(double* d_cv, int64_t rows, int64_t cols, double tau, uint8_t* pattern,
+                                 cudaStream_t st);
 cudaError_t launch_classify(const double* rs, int64_t rows, int64_t row_len, const double* cs,
                             int64_t cols, int64_t col_len, double eps, double tau, double* d_cv,
                             uint8_t* pattern, cudaStream_t st);

@@ -645,16 +645,16 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
   const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64 +
                       ((nrow_zero > 0 || ncol_zero > 0) ? 2 * sizeof(SmemMask) : 0);
   if ((nrow_zero > 0 && R > kMaskMaxRows) || (ncol_zero > 0 && C > kMaskMaxRows)) return cudaErrorInvalidValue;
-  static const int occ = [] { const char* e = getenv("ADAHOP_DUAL_OCC"); return e ? atoi(e) : 2; }();
-  static bool attr = false;
-  if (!attr) {
+  static const int occ = knob("ADAHOP_DUAL_OCC", 2);
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ae = once_per_device(attr, [] {
     const int mx = int(size_t(kQStages) * kQTileBytes + 1024 + 64 + 2 * sizeof(SmemMask));
     cudaError_t e = cudaFuncSetAttribute(k_iht_quant_dual<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_iht_quant_dual<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+    return e;
+  });
+  if (ae != cudaSuccess) return ae;
   const int64_t ntiles = ((R + 127) / 128) * ((C + 127) / 128);
   const int64_t cap = int64_t(num_sms) * occ;
   const unsigned grid = unsigned(ntiles < cap ? ntiles : cap);
@@ -751,15 +751,15 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
     }
     if (!ok || R > kMaskMaxRows) return cudaErrorInvalidValue;
     const size_t smem = size_t(kQStages) * kQTileBytes + 1024 + 64 + (nzero > 0 ? sizeof(SmemMask) : 0);
-    static bool attr[2] = {false, false};
-    if (!attr[kstrided]) {
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t ae = once_per_device(attr, [] {
       const int mx = int(size_t(kQStages) * kQTileBytes + 1024 + 64 + sizeof(SmemMask));
-      cudaError_t e = kstrided
-          ? cudaFuncSetAttribute(k_iht_quant_tma<true, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)
-          : cudaFuncSetAttribute(k_iht_quant_tma<false, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      if (e != cudaSuccess) return e;
-      attr[kstrided] = true;
-    }
+      cudaError_t e = cudaFuncSetAttribute(k_iht_quant_tma<true, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_iht_quant_tma<false, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      return e;
+    });
+    if (ae != cudaSuccess) return ae;
     const int64_t cap = int64_t(num_sms) * 2;   // two persistent CTAs per SM
     const unsigned grid = unsigned(ntiles < cap ? ntiles : cap);
     if (kstrided)
@@ -776,13 +776,12 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
         in, R, K, ld, zero_rows, nzero, codes, sf, kch, had_out, slice);
   } else {
     const size_t smem = size_t(64) * 256 * sizeof(T);
-    static bool attr_g = false;
-    if (!attr_g) {
-      cudaError_t e = cudaFuncSetAttribute(k_iht_quant_col_generic<T, kHad, kSw>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      attr_g = true;
-    }
+    static std::atomic<uint64_t> attr_g{0};
+    cudaError_t ae = once_per_device(attr_g, [smem] {
+      return cudaFuncSetAttribute(k_iht_quant_col_generic<T, kHad, kSw>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem));
+    });
+    if (ae != cudaSuccess) return ae;
     dim3 grid(unsigned((R + 255) / 256), unsigned((K + 63) / 64));
     k_iht_quant_col_generic<T, kHad, kSw><<<grid, 256, smem, st>>>(in, R, K, ld, zero_rows, nzero, codes,
                                                                     sf, kch, had_out, slice);
@@ -791,7 +790,7 @@ static cudaError_t launch_quant_t(const T* in, int64_t R, int64_t K, int64_t ld,
 }
 
 bool quant_use_tc() {
-  static const bool tc = [] { const char* e = getenv("ADAHOP_QUANT_IMPL"); return !(e && e[0] == 's'); }();
+  static const bool tc = knob("ADAHOP_QUANT_SCALAR", 0) == 0;   // experiment builds: 1 selects the butterfly kernels
   return tc;
 }
 
@@ -994,9 +993,8 @@ constexpr int kTopkThreads = 1024;
 // d_out = 2048 stored rows) then need one block and no merge (FOID stage 0.133 -> 0.118 ms per
 // Llama-3.2-1B layer step). ADAHOP_FOID_BLOCK_ROWS = 1024 / 2048 for comparison.
 static int foid_block_rows() {
-  static int v = [] {
-    const char* e = getenv("ADAHOP_FOID_BLOCK_ROWS");
-    const int r = e ? atoi(e) : 4096;
+  static const int v = [] {
+    const int r = knob("ADAHOP_FOID_BLOCK_ROWS", 4096);
     return r == 1024 || r == 2048 ? r : 4096;
   }();
   return v;
@@ -1212,13 +1210,11 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
   }
   if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
   else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kTopkMaxCand * 12));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ae = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTopkMaxCand * 12));
+  });
+  if (ae != cudaSuccess) return ae;
   // (the FOID kernels are launched without PDL: early-resident select CTAs measured slower)
   k_foid_select<<<B.sb_off[n], kTopkThreads, size_t(kTopkMaxCand) * 12, st>>>(B);
   return cudaGetLastError();
@@ -1464,8 +1460,24 @@ __global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* _
   }
 }
 
-// Sum of the blocks' CV partials (fixed order) and the single-rank classification (P:535-541,
-// DESIGN R7): same rule as k_classify.
+// App. A decision (DESIGN R7) from the two CV sums: d_cv[0..1] = the sums,
+// d_cv[2..3] = CV_row = sum_row / rows, CV_col = sum_col / cols; Row if CV_col > tau, Column if
+// CV_row > tau, the larger when both, an exact tie -> Row.
+__device__ __forceinline__ void classify_store(double sum_row, double sum_col, int64_t rows, int64_t cols, double tau,
+                                               double* d_cv, uint8_t* pattern) {
+  const double cv_row = sum_row / double(rows), cv_col = sum_col / double(cols);
+  d_cv[0] = sum_row;
+  d_cv[1] = sum_col;
+  d_cv[2] = cv_row;
+  d_cv[3] = cv_col;
+  const bool row_hit = cv_col > tau, col_hit = cv_row > tau;
+  uint8_t p = 0;
+  if (row_hit && (!col_hit || cv_col >= cv_row)) p = 1;
+  else if (col_hit) p = 2;
+  pattern[0] = p;
+}
+
+// Sum of the blocks' CV partials (fixed order) and the single-rank classification.
 __global__ void __launch_bounds__(256) k_classify_partials(const double* __restrict__ cvpart, int nb, int64_t rows,
                                                           int64_t cols, double tau, double* __restrict__ d_cv,
                                                           uint8_t* __restrict__ pattern) {
@@ -1482,16 +1494,7 @@ __global__ void __launch_bounds__(256) k_classify_partials(const double* __restr
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    d_cv[0] = red[0][0];
-    d_cv[1] = red[1][0];
-    const double cv_row = red[0][0] / double(rows), cv_col = red[1][0] / double(cols);
-    const bool row_hit = cv_col > tau, col_hit = cv_row > tau;
-    uint8_t p = 0;
-    if (row_hit && (!col_hit || cv_col >= cv_row)) p = 1;
-    else if (col_hit) p = 2;
-    pattern[0] = p;
-  }
+  if (threadIdx.x == 0) classify_store(red[0][0], red[1][0], rows, cols, tau, d_cv, pattern);
 }
 
 size_t calib_cvpart_bytes(int64_t R, int64_t C) {
@@ -1563,16 +1566,17 @@ __global__ void __launch_bounds__(1024) k_classify(const double* __restrict__ rs
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    d_cv[0] = red[0][0];
-    d_cv[1] = red[1][0];
-    const double cv_row = red[0][0] / double(rows), cv_col = red[1][0] / double(cols);
-    const bool row_hit = cv_col > tau, col_hit = cv_row > tau;
-    uint8_t p = 0;
-    if (row_hit && (!col_hit || cv_col >= cv_row)) p = 1;
-    else if (col_hit) p = 2;
-    pattern[0] = p;
-  }
+  if (threadIdx.x == 0) classify_store(red[0][0], red[1][0], rows, cols, tau, d_cv, pattern);
+}
+// Multi-rank decision: d_cv[0] = the row-CV sum over ALL ranks' rows (all-reduced by the caller),
+// d_cv[1] = the column-CV sum from the merged column statistics; rows = the global row count.
+__global__ void k_classify_sums(double* d_cv, int64_t rows, int64_t cols, double tau, uint8_t* pattern) {
+  if (threadIdx.x == 0) classify_store(d_cv[0], d_cv[1], rows, cols, tau, d_cv, pattern);
+}
+cudaError_t launch_classify_sums(double* d_cv, int64_t rows, int64_t cols, double tau, uint8_t* pattern,
+                                 cudaStream_t st) {
+  k_classify_sums<<<1, 32, 0, st>>>(d_cv, rows, cols, tau, pattern);
+  return cudaGetLastError();
 }
 cudaError_t launch_classify(const double* rs, int64_t rows, int64_t row_len, const double* cs,
                             int64_t cols, int64_t col_len, double eps, double tau, double* d_cv,

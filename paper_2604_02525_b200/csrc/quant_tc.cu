@@ -488,13 +488,12 @@ bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool r
 template <bool kRow, bool kCol, bool kHad>
 static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaStream_t st) {
   const size_t smem = quant_tc_smem(masks);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(quant_tc_smem(true)));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ae = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(quant_tc_smem(true)));
+  });
+  if (ae != cudaSuccess) return ae;
   const unsigned grid = unsigned(J.ntiles < num_sms ? J.ntiles : num_sms);
   return launch_k(qtc::k_quant_tc<kRow, kCol, kHad>, dim3(grid), dim3(qtc::kThreads), smem, st, 1, J);
 }
@@ -560,17 +559,11 @@ static cudaError_t launch_oe_gather(const __nv_bfloat16* T, int64_t R, int64_t C
 // staged tiles instead of the separate k_oe_gather launches — measured slower (quant stage 0.59
 // vs 0.54 ms per Llama-3.2-1B layer step: the stage release waits for the copies)
 static bool gather_fused() {
-  static int v = [] {
-    const char* e = getenv("ADAHOP_GATHER_FUSED");
-    return e ? atoi(e) : 0;
-  }();
+  static const int v = knob("ADAHOP_GATHER_FUSED", 0);
   return v != 0;
 }
 static bool gather_after_quant() {
-  static int v = [] {
-    const char* e = getenv("ADAHOP_GATHER_AFTER");
-    return e ? atoi(e) : 0;
-  }();
+  static const int v = knob("ADAHOP_GATHER_AFTER", 0);
   return v != 0;
 }
 

@@ -65,23 +65,48 @@ class CalibrationStep:
     cv_col: float
 
 
-def calibrate_sharded(t_local: torch.Tensor, rows_global: int, stats_fn: Callable, classify_fn: Callable,
-                      classify_cv_fn: Callable, group=None) -> CalibrationStep:
-    """One calibration step of one token-sharded tensor (rows = tokens).
+@dataclass
+class CalibrationOps:
+    """The three library calls of one calibration step (include/adahop.h):
+    stats(t) -> (row_stats [rows, 4], col_stats [cols, 4])           adahop_stats
+    classify(row_stats, col_stats, row_len, col_count) -> (cv[4], pat) adahop_classify
+    classify_sums(cv, rows_global, cols) -> pat                        adahop_classify_sums
+    The CPU tests inject host implementations; the product uses the C ABI (``default_ops``)."""
+    stats: Callable
+    classify: Callable
+    classify_sums: Callable
 
-    stats_fn(t) -> (row_stats [rows_local,4], col_stats [cols,4]) (adahop_stats);
-    classify_fn(row_stats, col_stats, row_len, col_count) -> (cv_sums[2], pattern) (adahop_classify);
-    classify_cv_fn(cv_row, cv_col) -> pattern (adahop_classify_cv)."""
-    rows_local, cols = t_local.shape
-    row_stats, col_stats = stats_fn(t_local)
+
+def default_ops() -> CalibrationOps:
+    from . import adahop as ah
+    return CalibrationOps(ah.stats, ah.classify, ah.classify_sums)
+
+
+PAT_NAME = {0: "N", 1: "R", 2: "C"}
+
+
+def calibrate_sharded(t_local: torch.Tensor, rows_global: int, ops: Optional[CalibrationOps] = None,
+                      group=None) -> CalibrationStep:
+    """One calibration step of one token-sharded tensor (rows = tokens), App. A.
+
+    Every arithmetic step runs in the library; this function only moves data between ranks:
+      1. adahop_stats on the local rows;
+      2. all-reduce the column statistics (SUM of the moments, MAX of |x|);
+      3. adahop_classify with col_count = rows_global: cv[0] = local row-CV sum,
+         cv[1] = column-CV sum over the merged statistics;
+      4. all-reduce cv[0] (SUM over ranks);
+      5. adahop_classify_sums(rows_global): CV_row, CV_col and the pattern, identical on all ranks."""
+    ops = ops or default_ops()
+    _, cols = t_local.shape
+    row_stats, col_stats = ops.stats(t_local)
     merge_col_stats(col_stats, group)
-    cv, _ = classify_fn(row_stats, col_stats, cols, rows_global)
-    cv = cv.clone()
+    cv, _ = ops.classify(row_stats, col_stats, cols, rows_global)
     row_sum = cv[:1].clone()
     merge_row_cv_sum(row_sum, group)
-    cv_row = float(row_sum.item()) / rows_global
-    cv_col = float(cv[1].item()) / cols
-    return CalibrationStep(classify_cv_fn(cv_row, cv_col), cv_row, cv_col)
+    cv[:1].copy_(row_sum)
+    pat = ops.classify_sums(cv, rows_global, cols)
+    vals = cv.cpu().tolist()
+    return CalibrationStep(PAT_NAME[int(pat.reshape(-1)[0].item())], vals[2], vals[3])
 
 
 class DataParallelLinear:

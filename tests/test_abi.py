@@ -30,7 +30,7 @@ def test_every_declared_symbol_is_exported_and_bound():
 
 
 def test_abi_version_and_defaults():
-    assert _lib.lib.adahop_abi_version() == 1
+    assert _lib.lib.adahop_abi_version() == 2
     p = _lib.Params(0, 0, 0, 0, 0.0, 0.0)
     _lib.lib.adahop_default_params(C.byref(p))
     assert (p.had_block, p.oe_k, p.foid_probe, p.level) == (32, 64, 64, 1)
@@ -47,9 +47,26 @@ def test_majority_vote_and_classify_cv_match_oracle():
     for seq in (["R"] * 30, ["R"] * 16 + ["N"] * 14, ["R"] * 15 + ["C"] * 15, ["C"] * 3 + ["N"] * 3,
                 ["N"] * 5 + ["C"] * 4 + ["R"] * 4):
         assert ah.majority_vote(seq) == O.majority_vote(seq)
-    for cr, cc in ((1.2, 1.3), (3.5, 1.2), (1.2, 3.5), (3.0, 3.0), (3.0, 4.0), (4.0, 3.0), (2.0, 2.0)):
-        want = "R" if (cc > 2 and (cr <= 2 or cc >= cr)) else ("C" if cr > 2 else "N")
-        assert ah.classify_cv(cr, cc) == want
+    # an empty or invalid record is an input error on both sides (oracle: ValueError)
+    for bad in ([], ["R", "X"]):
+        with pytest.raises(ValueError):
+            ah.majority_vote(bad)
+    assert _lib.lib.adahop_majority_vote(None, 3) == -1
+    arr = (C.c_int32 * 2)(1, 7)
+    assert _lib.lib.adahop_majority_vote(arr, 2) == -1
+    # the library's decision on the oracle's CVs == the oracle's decision, on the closed-form
+    # matrices of test_oracle_pins (both above tau each way, exact tie, one side only, neither)
+    import numpy as np
+    ident = np.eye(16)
+    t = np.eye(16)
+    t[0, 1:4] = 1.0
+    wide = np.zeros((4, 64))
+    wide[np.arange(4), np.arange(4) * 16] = 1.0
+    for m in (ident, t, t.T, wide, wide.T, np.tile(np.eye(4), (4, 1)), np.full((8, 8), 2.0)):
+        assert ah.classify_cv(*O.cv_row_col(m)) == O.classify(m)
+    # threshold boundary: strictly greater than tau
+    assert ah.classify_cv(2.0, 2.0) == "N"
+    assert ah.classify_cv(2.0000001, 2.0) == "C"
 
 
 def test_status_strings():
@@ -73,6 +90,9 @@ def test_host_validation_without_device():
     # had_block != 32 -> unsupported
     q = _lib.Params(had_block=16)
     assert f.adahop_gemm(ptr, 0, 64, ptr, 0, 64, ptr, 1, 64, 64, 64, 64, 0, C.byref(q), ptr, 4096, None) == 3
+    # the multi-rank decision entry point validates before touching the device
+    assert f.adahop_classify_sums(None, 64, 64, C.byref(p), None, None) == 1
+    assert f.adahop_classify_sums(ptr, 0, 64, C.byref(p), ptr, None) == 2
     # wgrad needs T % 32 == 0
     assert f.adahop_linear_wgrad(ptr, ptr, ptr, 1, 48, 64, 64, 0, C.byref(p), ptr, 4096, None) == 2
 

@@ -3,51 +3,15 @@ token sharding, the wgrad all-reduce and the calibration merge. The per-shard co
 CPU oracle (injected), so the DP result must equal the sum of per-shard oracle results
  and calibration must equal the single-process classification of the whole
 tensor."""
-import os
-import socket
-
 import numpy as np
 import pytest
 import torch
-import torch.distributed as dist
-import torch.multiprocessing as mp
 
 import oracle as O
 import synth
+from _mp import spawn
 
 dist_mod = pytest.importorskip("paper_2604_02525_b200.dist")
-
-
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def _run(rank, world, port, fn, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        q.put((rank, fn(rank, world)))
-    finally:
-        dist.destroy_process_group()
-
-
-def spawn(fn, world=2):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, fn, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    out = dict(q.get(timeout=300) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    return out
 
 
 def test_token_shard_covers_and_aligns():
@@ -112,6 +76,7 @@ def _np_stats(t):
 
 
 def _np_classify(rs, cs, row_len, col_count, eps=1e-8):
+    # host stand-in for adahop_classify (App. A): CV sums, then the single-rank decision
     rs = rs.numpy()
     cs = cs.numpy()
 
@@ -120,21 +85,26 @@ def _np_classify(rs, cs, row_len, col_count, eps=1e-8):
         var = np.maximum(st[:, 1] / n - mu * mu, 0)
         return np.sum(np.sqrt(var) / (st[:, 2] / n + eps))
 
-    return torch.tensor([cv(rs, row_len), cv(cs, col_count)], dtype=torch.float64), None
+    out = torch.tensor([cv(rs, row_len), cv(cs, col_count), 0.0, 0.0], dtype=torch.float64)
+    return out, _np_classify_sums(out, rs.shape[0], cs.shape[0])
 
 
-def _classify_cv(cv_row, cv_col):
-    if cv_col > 2.0 and (cv_row <= 2.0 or cv_col >= cv_row):
-        return "R"
-    return "C" if cv_row > 2.0 else "N"
+def _np_classify_sums(cv, rows, cols, tau=2.0):
+    # host stand-in for adahop_classify_sums (DESIGN R7)
+    cv[2] = cv[0] / rows
+    cv[3] = cv[1] / cols
+    cr, cc = float(cv[2]), float(cv[3])
+    p = 1 if (cc > tau and (cr <= tau or cc >= cr)) else (2 if cr > tau else 0)
+    return torch.tensor([p], dtype=torch.uint8)
 
 
 def _dp_calib(rank, world):
     res = {}
+    ops = dist_mod.CalibrationOps(_np_stats, _np_classify, _np_classify_sums)
     for p in "RCN":
         t, _ = synth.operand(512, 256, p, "GY", case_id=903)
         a, b = dist_mod.token_shard(512, world, rank)
-        step = dist_mod.calibrate_sharded(torch.from_numpy(t[a:b]), 512, _np_stats, _np_classify, _classify_cv)
+        step = dist_mod.calibrate_sharded(torch.from_numpy(t[a:b]), 512, ops)
         res[p] = (step.pattern, step.cv_row, step.cv_col)
     return res
 

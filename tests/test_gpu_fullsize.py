@@ -58,15 +58,16 @@ def sampled_check(path, strategy, got, x, w, gy, k, rng, n=2000):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("model,linear,k", [
-    ("llama32_1b", "gate", 64),     # configs[1]: X = C, G_Y = C -> fwd CN (IHT), dgrad CN (IHT), wgrad RC (OE-R)
-    ("llama32_1b", "k", 64),        # X = C, G_Y = R -> dgrad RN (OE-L), wgrad CC (OE-R, Lv1)
-    ("llama3_8b", "k", 0),          # configs[3] k sweep on the 8B kv projection
-    ("llama3_8b", "k", 16),
-    ("llama3_8b", "k", 64),
-    ("instella_3b", "down", 64),    # configs[2]: K = 6912 fwd, N = 6912 dgrad / wgrad
+@pytest.mark.parametrize("model,linear,k,level", [
+    ("llama32_1b", "gate", 64, 1),  # configs[1]: X = C, G_Y = C -> fwd CN (IHT), dgrad CN (IHT), wgrad RC (OE-R)
+    ("llama32_1b", "k", 64, 1),     # X = C, G_Y = R -> dgrad RN (OE-L), wgrad CC (OE-R, Lv1)
+    ("llama3_8b", "k", 0, 1),       # configs[3] k sweep on the 8B kv projection
+    ("llama3_8b", "k", 16, 1),
+    ("llama3_8b", "k", 64, 1),
+    ("llama3_8b", "k", 64, 2),      # AdaHOP-Lv2: the CC wgrad runs in BF16, full size
+    ("instella_3b", "down", 64, 1),  # configs[2]: K = 6912 fwd, N = 6912 dgrad / wgrad
 ])
-def test_linear_layer_full_size_sampled(model, linear, k):
+def test_linear_layer_full_size_sampled(model, linear, k, level):
     spec = {"llama32_1b": synth.LLAMA32_1B, "llama3_8b": synth.LLAMA3_8B, "instella_3b": synth.INSTELLA_3B}[model]
     _, d_in, d_out = next(t for t in spec["linears"] if t[0] == linear)
     px, pg = synth.LLAMA32_1B_LAYER_PATTERNS[linear]
@@ -74,8 +75,10 @@ def test_linear_layer_full_size_sampled(model, linear, k):
     x, _ = synth.operand(T, d_in, px, "X", case_id=501)
     w, _ = synth.operand(d_out, d_in, "N", "W", case_id=502)
     gy, _ = synth.operand(T, d_out, pg, "GY", case_id=503)
-    strats = tuple(ah.strategy_for_pair(*fed_pair(p, px, "N", pg), 1) for p in ("fwd", "dgrad", "wgrad"))
-    p = ah.Params(oe_k=k)
+    strats = tuple(ah.strategy_for_pair(*fed_pair(p, px, "N", pg), level) for p in ("fwd", "dgrad", "wgrad"))
+    if level == 2:
+        assert strats[2] == "BF16"
+    p = ah.Params(oe_k=k, level=level)
     xd, wd, gd = dev_bf16(x), dev_bf16(w), dev_bf16(gy)
     outs32 = ah.linear_layer(xd, wd, gd, strats, p, out_dtype=torch.float32)
     outs16 = ah.linear_layer(xd, wd, gd, strats, p, out_dtype=torch.bfloat16)

@@ -152,6 +152,69 @@ def test_iht_quant_extreme_magnitudes():
     np.testing.assert_array_equal(codes.cpu().numpy()[finite], O.pack_codes(oc)[finite])
 
 
+def _extreme_bf16_rows(R, K, seed):
+    # bf16 rows whose per-row scales sweep the whole bf16 exponent range (2^-133 ... 2^120), plus
+    # zero rows, a row holding only the smallest bf16 subnormal, and rows with one near-max
+    # element per 32-block (Hadamard outputs ~2^125.5: scale exponent e = 123, the quantiser's
+    # e > 120 fallback); the low rows take its e < -100 fallback
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((R, K)).astype(np.float64)
+    ex = np.round(np.linspace(-133, 118, R))
+    x *= np.exp2(ex)[:, None]
+    x[3] = 0.0
+    x[4] = 0.0
+    x[4, 7] = 2.0 ** -133
+    # (rows 5 and 6 put theirs in different columns, so that no 32-block of either orientation
+    # holds two of them: the transform of finite inputs must stay finite, include/adahop.h)
+    for r, c0 in ((5, 0), (6, 16)):
+        x[r] = 0.0
+        x[r, c0::32] = 3.3e38 * np.where(rng.standard_normal(K // 32) > 0, 1.0, -1.0)
+    return O.round_bf16(x.astype(np.float32))
+
+
+@pytest.mark.parametrize("k_strided", [False, True])
+def test_quant_tc_bf16_extreme_magnitudes_production_path(k_strided):
+    # The tensor-core quantiser on bf16 inputs (the production path of every bf16 operand): the
+    # fp32 Hadamard dump (debug variant) fixes the quantiser's input; the PRODUCTION variant (no
+    # dump: fused c * 2^-e multiply, fallbacks for e > 120 / e < -100) must give the oracle's
+    # codes and scales of that input bit for bit (SURVEY c19 protocol (a)).
+    R, K = 256, 512
+    x = _extreme_bf16_rows(R, K, 21)
+    t = dev_bf16(x.T.copy() if k_strided else x)
+    _, _, had = ah.debug_iht_quant(t, k_strided=k_strided, want_had=True)
+    codes, scales, _ = ah.debug_iht_quant(t, k_strided=k_strided, want_had=False)
+    torch.cuda.synchronize()
+    had = had.cpu().numpy()
+    assert np.isfinite(had).all()
+    oc, osc = O.quantize_mxfp4(had)
+    np.testing.assert_array_equal(scales.cpu().numpy(), osc)
+    np.testing.assert_array_equal(codes.cpu().numpy(), O.pack_codes(oc))
+    assert osc.max() >= 127 + 121 and osc[osc != 127].min() <= 127 - 101   # both fallbacks exercised
+    # the Hadamard output itself: within 1e-6 of the exact transform, per row (rows of normal
+    # fp32 magnitude; subnormal outputs carry fewer significant bits by construction)
+    ref = O.iht_dense(x)
+    big = np.abs(ref).max(1) >= 2.0 ** -100
+    err = np.linalg.norm(had - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+    assert np.all(err[big] <= TOL_HAD)
+
+
+def test_quant_dual_bf16_extreme_magnitudes_production_path():
+    # the dual-orientation production launch (row + column layouts of one tensor in one pass) at
+    # the same magnitudes, against the oracle quantiser of each orientation's Hadamard dump
+    R, C = 256, 512
+    x = _extreme_bf16_rows(R, C, 22)
+    t = dev_bf16(x)
+    qr, sr, qc, sc = ah.debug_quant_dual(t)
+    _, _, had_r = ah.debug_iht_quant(t, want_had=True)
+    _, _, had_c = ah.debug_iht_quant(t, k_strided=True, want_had=True)
+    torch.cuda.synchronize()
+    for had, q, sc_ in ((had_r, qr, sr), (had_c, qc, sc)):
+        assert torch.isfinite(had).all()
+        oc, osc = O.quantize_mxfp4(had.cpu().numpy())
+        np.testing.assert_array_equal(sc_.cpu().numpy(), osc)
+        np.testing.assert_array_equal(q.cpu().numpy(), O.pack_codes(oc))
+
+
 # ======================================================================= FOID
 @pytest.mark.parametrize("k_strided", [False, True])
 @pytest.mark.parametrize("R,K,k,probe", [(5000, 128, 64, 64), (300, 96, 8, 64), (2048, 64, 256, 64),

@@ -265,6 +265,38 @@ def test_classify_planted_patterns_and_duality():
             assert O.classify(t * 37.0) == p                      # scale invariance S:261
 
 
+def test_classify_both_above_tau_closed_forms():
+    # The both-above-tau branch of App. A's rule (reading R7: larger CV wins, exact
+    # tie -> Row), pinned on 0/1 matrices whose CVs have closed forms. A row (or
+    # column) of length n with r ones has mean r/n and population std sqrt(r/n (1 - r/n)), so
+    # std / mean|x| = sqrt(n/r - 1) (eps = 1e-8 moves it by < 1e-5). All sums are exact dyadic
+    # fractions, so the tie below is exact in fp64 (the tolerances cover eps).
+    s3, s7, s15 = math.sqrt(3), math.sqrt(7), math.sqrt(15)
+    # identity: every row and column has one 1 of 16 -> CV_row = CV_col = sqrt(15) > tau: tie -> R
+    ident = np.eye(16)
+    cr, cc = O.cv_row_col(ident)
+    assert cr == cc and abs(cr - s15) < 1e-5
+    assert O.classify(ident) == "R"
+    # identity + row 0 also holding ones at columns 1..3: row 0 has r = 4 (sqrt 3), rows 1..15
+    # r = 1 (sqrt 15); columns 1..3 have r = 2 (sqrt 7), the other 13 r = 1 (sqrt 15)
+    t = np.eye(16)
+    t[0, 1:4] = 1.0
+    cr, cc = O.cv_row_col(t)
+    want_r, want_c = (s3 + 15 * s15) / 16, (13 * s15 + 3 * s7) / 16     # 3.7392, 3.6429
+    assert abs(cr - want_r) < 1e-5 and abs(cc - want_c) < 1e-5
+    assert cr > cc > O.TAU
+    assert O.classify(t) == "C"          # both above tau, CV_row larger -> Column-wise
+    assert O.classify(t.T) == "R"        # transposed: CV_col larger -> Row-wise
+    # only one direction above tau: 16 x 4 with a single 1 per row (rows: sqrt(3) < tau;
+    # columns: 4 ones of 16 -> sqrt(3) too) -> None; 4 x 64 diagonal-ish: rows sqrt(63) -> C
+    assert O.classify(np.tile(np.eye(4), (4, 1))) == "N"
+    wide = np.zeros((4, 64))
+    wide[np.arange(4), np.arange(4) * 16] = 1.0
+    cr, cc = O.cv_row_col(wide)
+    assert abs(cr - math.sqrt(63)) < 1e-5 and abs(cc - math.sqrt(3) * 4 / 64) < 1e-5
+    assert O.classify(wide) == "C"
+
+
 def test_majority_vote_examples():
     # SPEC S:257-259
     assert O.majority_vote(["R"] * 30) == "R"
