@@ -31,8 +31,9 @@
  *  - Shape rules: K % 32 == 0 (else ADAHOP_E_SHAPE; no padding);
  *    had_block must be 32 (else ADAHOP_E_UNSUPPORTED); oe_k > rows/cols of the
  *    extracted operand clamps; oe_k == 0 means "no OE"; oe_k <= 256; the OE operand has at
- *    most 16384 stored rows (ADAHOP_E_UNSUPPORTED beyond: the FOID select and the OE
- *    masks are sized for it).
+ *    most 65536 stored rows (ADAHOP_E_UNSUPPORTED beyond: the FOID select merges the
+ *    k-best of 16 blocks of 4096 rows) — e.g. up to 65536 tokens per GPU for an OE on the
+ *    token dimension (dgrad OE-Left on G_Y, fwd OE-Left on X).
  *    Leading dimensions must keep every row 16-byte aligned.
  */
 #ifndef ADAHOP_H_
@@ -100,6 +101,16 @@ const char* adahop_status_string(adahop_status_t s);
  * CC -> OE-Right (level 1) or BF16 (level 2). Pure host function. */
 adahop_strategy_t adahop_strategy_for_pair(adahop_pattern_t left, adahop_pattern_t right,
                                            int32_t level);
+
+/* Strategies of the three matmuls of one linear from its tensors' calibrated patterns (host, pure;
+ * §5.1 step 3). Patterns are detected on the tensors as stored — X [T x d_in],
+ * W [d_out x d_in], G_Y [T x d_out] — and the fed operand pairs are
+ *   fwd (X, W^T), dgrad (G_Y, W), wgrad (G_Y^T, X), with pattern(T^T) = swap(R <-> C)
+ * (R8, pinned by Table 1's cross-path identities). Writes out[0..2] = the strategies of
+ * {fwd, dgrad, wgrad} and, when fed_pairs is not NULL, fed_pairs[2 p], fed_pairs[2 p + 1] = the
+ * fed (left, right) patterns of path p. Returns 0, or -1 for an invalid pattern / level. */
+int32_t adahop_layer_strategies(adahop_pattern_t pat_x, adahop_pattern_t pat_w, adahop_pattern_t pat_gy,
+                                int32_t level, adahop_strategy_t* out, adahop_pattern_t* fed_pairs);
 
 /* Majority vote over per-step patterns; ties resolve R > C > N (R9).
  * `per_step` is a host array of n >= 1 pattern codes (0, 1, 2). Returns ADAHOP_PAT_INVALID for

@@ -41,6 +41,7 @@ SIGNATURES = {
     "adahop_strategy_for_pair": (I32, [I32, I32, I32]),
     "adahop_majority_vote": (I32, [C.POINTER(I32), I32]),
     "adahop_classify_cv": (I32, [F64, F64, PP]),
+    "adahop_layer_strategies": (I32, [I32, I32, I32, I32, C.POINTER(I32), C.POINTER(I32)]),
     "adahop_stats_workspace_bytes": (SZ, [I64, I64]),
     "adahop_stats": (I32, [P, I32, I64, I64, I64, P, P, P, SZ, P]),
     "adahop_classify": (I32, [P, I64, P, I64, I64, PP, P, P, P]),

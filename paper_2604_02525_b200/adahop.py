@@ -27,7 +27,7 @@ __all__ = [
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
     "calibrate_workspace_bytes", "classify_sums", "LinearContext", "linear_forward", "linear_backward",
-    "split_workspace_bytes",
+    "split_workspace_bytes", "linear_ctx_bytes", "layer_strategies",
 ]
 
 
@@ -54,6 +54,17 @@ def _ptr(t) -> C.c_void_p:
 # ------------------------------------------------------------------------- host helpers
 def strategy_for_pair(left: str, right: str, level: int = 1) -> str:
     return STRATEGY_NAME[lib.adahop_strategy_for_pair(PAT[left], PAT[right], level)]
+
+
+def layer_strategies(pat_x: str, pat_w: str, pat_gy: str, level: int = 1):
+    """(strategies (fwd, dgrad, wgrad), fed pairs ('XY' strings)) of one linear from the calibrated
+    patterns of X, W, G_Y as stored (adahop_layer_strategies)."""
+    out = (C.c_int32 * 3)()
+    fed = (C.c_int32 * 6)()
+    if lib.adahop_layer_strategies(PAT[pat_x], PAT[pat_w], PAT[pat_gy], level, out, fed) != 0:
+        raise ValueError(f"invalid patterns / level {(pat_x, pat_w, pat_gy, level)}")
+    return (tuple(STRATEGY_NAME[v] for v in out),
+            tuple(PAT_NAME[fed[2 * i]] + PAT_NAME[fed[2 * i + 1]] for i in range(3)))
 
 
 def majority_vote(patterns) -> str:
@@ -433,6 +444,12 @@ class LinearContext:
     def saved_bytes(self) -> int:
         """Device bytes kept alive between forward and backward for this linear."""
         return self.buf.numel() + (self.x.numel() * self.x.element_size() if self.x is not None else 0)
+
+
+def linear_ctx_bytes(T, d_in, d_out, strategies, params=None) -> int:
+    """Bytes of the context adahop_linear_forward saves for adahop_linear_backward."""
+    p = params or Params()
+    return lib.adahop_linear_ctx_bytes(T, d_in, d_out, _strats(strategies), C.byref(p))
 
 
 def split_workspace_bytes(T, d_in, d_out, strategies, params=None) -> int:

@@ -251,6 +251,25 @@ adahop_pattern_t adahop_majority_vote(const int32_t* per_step, int32_t n) {
   return ADAHOP_PAT_NONE;
 }
 
+int32_t adahop_layer_strategies(adahop_pattern_t pat_x, adahop_pattern_t pat_w, adahop_pattern_t pat_gy,
+                                int32_t level, adahop_strategy_t* out, adahop_pattern_t* fed_pairs) {
+  auto ok = [](adahop_pattern_t q) { return q == ADAHOP_PAT_NONE || q == ADAHOP_PAT_ROW || q == ADAHOP_PAT_COL; };
+  if (!out || !ok(pat_x) || !ok(pat_w) || !ok(pat_gy) || (level != 1 && level != 2)) return -1;
+  auto tr = [](adahop_pattern_t q) {   // pattern of the transpose (R8)
+    return q == ADAHOP_PAT_ROW ? ADAHOP_PAT_COL : (q == ADAHOP_PAT_COL ? ADAHOP_PAT_ROW : ADAHOP_PAT_NONE);
+  };
+  // fed pairs: fwd (X, W^T), dgrad (G_Y, W), wgrad (G_Y^T, X)
+  const adahop_pattern_t fed[3][2] = {{pat_x, tr(pat_w)}, {pat_gy, pat_w}, {tr(pat_gy), pat_x}};
+  for (int path = 0; path < 3; ++path) {
+    out[path] = adahop_strategy_for_pair(fed[path][0], fed[path][1], level);
+    if (fed_pairs) {
+      fed_pairs[2 * path] = fed[path][0];
+      fed_pairs[2 * path + 1] = fed[path][1];
+    }
+  }
+  return 0;
+}
+
 adahop_pattern_t adahop_classify_cv(double cv_row, double cv_col, const adahop_params_t* p) {
   const double tau = p ? p->tau : 2.0;
   const bool row_hit = cv_col > tau, col_hit = cv_row > tau;

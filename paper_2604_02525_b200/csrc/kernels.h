@@ -112,8 +112,9 @@ cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64
 cudaError_t launch_sf_convert(const uint8_t* src, int64_t R, int64_t K, uint8_t* dst,
                               bool to_canonical, cudaStream_t st);
 // FOID: probe keys + top-k -> idx_sorted[min(k,R)] (ascending). `keys` points to a scratch
-// buffer of foid_ws_bytes(R) bytes whose first R doubles receive the keys. R <= kFoidMaxRows.
-constexpr int64_t kFoidMaxRows = 16384;
+// buffer of foid_ws_bytes(R) bytes whose first R doubles receive the keys. R <= kFoidMaxRows:
+// 16 select blocks of 4096 rows whose k <= 256 survivors the last block merges in 4096 slots.
+constexpr int64_t kFoidMaxRows = 65536;
 size_t foid_ws_bytes(int64_t R);
 cudaError_t launch_foid(const void* in, bool in_f32, int64_t R, int64_t K, int64_t ld,
                         int kstrided, int k, int probe, double* keys, int32_t* idx_sorted,

@@ -1204,6 +1204,9 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
   for (int i = 0; i < n; ++i) {
     const FoidJob& J = jobs[i];
     if (J.R > kFoidMaxRows || J.R <= 0 || J.k <= 0 || J.k > 256) return cudaErrorInvalidValue;
+    // the merge keeps every block's k survivors in 4096 shared-memory slots
+    if ((J.R + B.rows_per_block - 1) / B.rows_per_block * J.k > 4096 && J.R > B.rows_per_block)
+      return cudaErrorInvalidValue;
     B.j[i] = FoidJobDev{J.in, J.R, J.ld, J.kstrided, int(std::min<int64_t>(J.probe, J.K)), J.k, J.scratch, J.idx};
     B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
     B.sb_off[i + 1] = B.sb_off[i] + int((J.R + B.rows_per_block - 1) / B.rows_per_block);

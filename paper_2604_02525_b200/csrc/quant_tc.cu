@@ -54,17 +54,13 @@ constexpr int kThreads = 128 + kEpiGroups * 128;   // warps 0..3 control, 4..19 
 constexpr int kHBytes = 32 * 32 * 2;  // H_32 in the canonical no-swizzle K-major layout
 constexpr int kStg = 128 * 64;        // one tile's codes of one orientation: 128 stored rows x 64 bytes
 
-constexpr int kMaskMaxRows = 32768;
+// The OE rows / columns of one (job, orientation): the sorted index list (k <= 256) staged in
+// shared memory; membership is a binary search, so the operand's row count is not limited.
 struct Mask {
-  uint32_t bits[kMaskMaxRows / 32];
   int32_t idx[256];
 };
-__device__ __forceinline__ void mask_build(Mask* m, const int32_t* __restrict__ idx, int n, int64_t rows) {
-  const int words = int((rows + 31) / 32);
-  for (int i = threadIdx.x; i < words; i += blockDim.x) m->bits[i] = 0u;
+__device__ __forceinline__ void mask_build(Mask* m, const int32_t* __restrict__ idx, int n, int64_t) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicOr(&m->bits[idx[i] >> 5], 1u << (idx[i] & 31));
   __syncthreads();
 }
 // first position in the sorted list idx[0, n) whose value is >= v
@@ -76,7 +72,10 @@ __device__ __forceinline__ int lower_bound_idx(const int32_t* idx, int n, int v)
   }
   return lo;
 }
-__device__ __forceinline__ bool mask_hit(const Mask* m, int64_t r) { return (m->bits[r >> 5] >> (r & 31)) & 1u; }
+__device__ __forceinline__ bool mask_hit(const Mask* m, int n, int64_t r) {
+  const int p = lower_bound_idx(m->idx, n, int(r));
+  return p < n && m->idx[p] == r;
+}
 __device__ __forceinline__ int mask_slot(const Mask* m, int n, int64_t r) {
   int lo = 0, hi = n - 1;
   while (lo <= hi) {
@@ -415,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       uint8_t* sst = sfstg + (oi * 2 + buf) * 512;
       const int64_t srow = (col_side ? int64_t(ct) * 128 : int64_t(rt) * 128) + row;
       const int64_t kb0 = (col_side ? int64_t(rt) * 4 : int64_t(ct) * 4) + blk0;   // first K-block of this group
-      const bool extracted = srow < rows_total && o.nzero > 0 && mask_hit(m, srow);
+      const bool extracted = srow < rows_total && o.nzero > 0 && mask_hit(m, o.nzero, srow);
       ptx::mbar_wait(&stgfree[buf], (use & 1) ^ 1);   // the store warp has read this staging buffer
       ptx::mbar_wait(&tfull[buf], use & 1);
       if (warp == 4 && lane == 0) QTC_T(3, lt);
@@ -481,8 +480,8 @@ size_t quant_tc_smem(bool masks) {
 }
 
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask) {
-  return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-         (!row_mask || R <= qtc::kMaskMaxRows) && (!col_mask || C <= qtc::kMaskMaxRows);
+  (void)R; (void)C; (void)row_mask; (void)col_mask;   // OE masks are index lists: no row limit
+  return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
 }
 
 template <bool kRow, bool kCol, bool kHad>

@@ -1,0 +1,155 @@
+"""Calibration-driven plan (§5.1): run the calibration pass on every linear's X, W and
+G_Y for a number of training steps (30 in the paper), vote each tensor's pattern over the
+steps, and freeze the strategy of each of the linear's three matmuls (tab:strategy_summary,
+P:305-326). The frozen plan is what the hot path consumes: "requires no runtime pattern
+detection".
+
+Every decision is the library's: adahop_calibrate (stats + App. A classification, per tensor and
+step, device-resident and graph-capturable), adahop_majority_vote, adahop_layer_strategies (fed
+orientation + strategy table). This module only records the per-step pattern codes, reads them back
+once, and persists the result (JSON) — SURVEY §5's checkpoint of the calibration outcome.
+"""
+from __future__ import annotations
+
+import json
+from collections import Counter
+from dataclasses import asdict, dataclass, field
+
+import torch
+
+from . import adahop as ah
+
+TENSORS = ("X", "W", "G_Y")
+PATHS = ("fwd", "dgrad", "wgrad")
+
+
+@dataclass
+class LinearPlan:
+    name: str
+    d_in: int
+    d_out: int
+    patterns: dict                       # tensor -> voted pattern ('R' | 'C' | 'N')
+    strategies: tuple                    # (fwd, dgrad, wgrad)
+    fed_pairs: tuple                     # fed (left, right) patterns per path, e.g. ('CN', 'CN', 'RC')
+    votes: dict = field(default_factory=dict)   # tensor -> {pattern: steps}
+
+
+@dataclass
+class Plan:
+    level: int
+    steps: int
+    linears: list
+
+    def strategies(self, name: str) -> tuple:
+        return next(lp.strategies for lp in self.linears if lp.name == name)
+
+    def census(self) -> dict:
+        """Fed-pair counts per path (the form of tab:pattern_distribution)."""
+        out = {p: Counter() for p in PATHS}
+        for lp in self.linears:
+            for p, pair in zip(PATHS, lp.fed_pairs):
+                out[p][pair] += 1
+        return {p: dict(sorted(c.items())) for p, c in out.items()}
+
+    def to_json(self) -> str:
+        return json.dumps({"level": self.level, "steps": self.steps,
+                           "linears": [dict(asdict(lp), strategies=list(lp.strategies),
+                                            fed_pairs=list(lp.fed_pairs)) for lp in self.linears]}, indent=1)
+
+    @staticmethod
+    def from_json(text: str) -> "Plan":
+        d = json.loads(text)
+        lins = [LinearPlan(e["name"], e["d_in"], e["d_out"], e["patterns"], tuple(e["strategies"]),
+                           tuple(e["fed_pairs"]), e.get("votes", {})) for e in d["linears"]]
+        return Plan(d["level"], d["steps"], lins)
+
+    def save(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(self.to_json())
+
+    @staticmethod
+    def load(path: str) -> "Plan":
+        with open(path) as f:
+            return Plan.from_json(f.read())
+
+
+def plan_from_patterns(linears, per_step: dict, level: int = 1) -> Plan:
+    """linears: [(name, d_in, d_out)]; per_step[(name, tensor)] = the per-step pattern letters.
+    Votes each record (adahop_majority_vote) and maps the voted patterns to the three strategies
+    (adahop_layer_strategies)."""
+    out = []
+    steps = 0
+    for name, d_in, d_out in linears:
+        pats, votes = {}, {}
+        for t in TENSORS:
+            rec = list(per_step[(name, t)])
+            steps = max(steps, len(rec))
+            pats[t] = ah.majority_vote(rec)
+            votes[t] = dict(Counter(rec))
+        strategies, fed = ah.layer_strategies(pats["X"], pats["W"], pats["G_Y"], level)
+        out.append(LinearPlan(name, d_in, d_out, pats, strategies, fed, votes))
+    return Plan(level, steps, out)
+
+
+class Calibrator:
+    """Records one pattern code per (step, linear, tensor) on the device.
+
+    record() issues adahop_calibrate for X, W and G_Y of one linear (no host synchronisation, so a
+    whole calibration step can be captured in a CUDA graph); plan() reads the record back once and
+    votes. Token-sharded data parallelism uses paper_2604_02525_b200.dist.calibrate_sharded per
+    tensor instead (its classification needs the merged statistics of all ranks)."""
+
+    def __init__(self, linears, steps: int = 30, params=None, device=None):
+        self.linears = list(linears)
+        self.index = {name: i for i, (name, _, _) in enumerate(self.linears)}
+        self.steps = steps
+        self.params = params or ah.Params()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        n = len(self.linears)
+        self.pat = torch.full((steps, n, 3), 255, dtype=torch.uint8, device=dev)
+        self.cv = torch.zeros((steps, n, 3, 4), dtype=torch.float64, device=dev)
+        self.ws = None
+        self.device = dev
+
+    def workspace_bytes(self, T: int) -> int:
+        return max(max(ah.calibrate_workspace_bytes(T, d_in), ah.calibrate_workspace_bytes(d_out, d_in),
+                       ah.calibrate_workspace_bytes(T, d_out)) for _, d_in, d_out in self.linears)
+
+    def record(self, step: int, name: str, x: torch.Tensor, w: torch.Tensor, gy: torch.Tensor) -> None:
+        i = self.index[name]
+        need = max(ah.calibrate_workspace_bytes(*t.shape) for t in (x, w, gy))
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        for j, t in enumerate((x, w, gy)):
+            ah.calibrate_async(t, self.ws, self.cv[step, i, j], self.pat[step, i, j:j + 1], self.params)
+
+    def record_sharded(self, step: int, name: str, x_local: torch.Tensor, w: torch.Tensor, gy_local: torch.Tensor,
+                       rows_global: int, group=None) -> None:
+        """Token-sharded variant: X and G_Y hold this rank's token rows; their patterns are decided
+        on the statistics merged over all ranks (dist.calibrate_sharded), W (replicated) locally."""
+        from . import dist as ahd
+        i = self.index[name]
+        codes = {"N": 0, "R": 1, "C": 2}
+        for j, t in enumerate((x_local, None, gy_local)):
+            if t is None:
+                need = ah.calibrate_workspace_bytes(*w.shape)
+                if self.ws is None or self.ws.numel() < need:
+                    self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+                ah.calibrate_async(w, self.ws, self.cv[step, i, j], self.pat[step, i, j:j + 1], self.params)
+                continue
+            st = ahd.calibrate_sharded(t, rows_global, group=group)
+            self.pat[step, i, j] = codes[st.pattern]
+
+    def per_step_patterns(self) -> dict:
+        codes = self.pat.cpu().tolist()
+        out = {}
+        for name, i in self.index.items():
+            for j, t in enumerate(TENSORS):
+                rec = [codes[s][i][j] for s in range(self.steps)]
+                if any(c > 2 for c in rec):
+                    raise RuntimeError(f"calibration record of {name}.{t} is incomplete")
+                out[(name, t)] = [ah.PAT_NAME[c] for c in rec]
+        return out
+
+    def plan(self, level: int = 1) -> Plan:
+        return plan_from_patterns(self.linears, self.per_step_patterns(), level)

@@ -84,20 +84,44 @@ def operand(rows: int, cols: int, pattern: str, kind: str = "X", case_id: int = 
 
 
 def operand_torch(rows: int, cols: int, pattern: str, kind: str, seed: int, device,
-                  scale: float = PLANT_SCALE):
-    """Full-size bench operand generated on the device (bf16), same recipe."""
+                  scale: float = PLANT_SCALE, plant_seed: int | None = None, out=None):
+    """Full-size bench operand generated on the device (bf16), same recipe. With plant_seed the
+    planted rows / columns come from their own generator, so that successive steps (different
+    `seed`) keep the same outlier channels — the persistence calibration relies on.
+    `out` (bf16, rows x cols) receives the result in place."""
     import torch
     g = torch.Generator(device=device)
     g.manual_seed(42 + int(seed))
     a = torch.randn((rows, cols), generator=g, device=device, dtype=torch.float32)
     a.mul_(SIGMA[kind])
+    gp = g
+    if plant_seed is not None:
+        gp = torch.Generator(device=device)
+        gp.manual_seed(42 + int(plant_seed))
     if pattern == "R":
-        idx = torch.randperm(rows, generator=g, device=device)[: n_planted(rows)]
+        idx = torch.randperm(rows, generator=gp, device=device)[: n_planted(rows)]
         a[idx, :] *= scale
     elif pattern == "C":
-        idx = torch.randperm(cols, generator=g, device=device)[: n_planted(cols)]
+        idx = torch.randperm(cols, generator=gp, device=device)[: n_planted(cols)]
         a[:, idx] *= scale
+    if out is not None:
+        return out.copy_(a)
     return a.to(torch.bfloat16)
+
+
+# Config 5 (SURVEY §8d): per-tensor patterns of the 16 x 7 Llama-3.2-1B linears that reproduce the
+# model's Table-1 census exactly (P:190-195): 15 linears (X = N, G_Y = C), 69 (C, C), 20 (C, N),
+# 8 (C, R) placed on k / v projections (P:295); W = N everywhere.
+def llama32_1b_census_patterns():
+    """[(layer, linear, pattern_x, pattern_w, pattern_gy)] for the 112 linears."""
+    names = [n for n, _, _ in LLAMA32_1B["linears"]]
+    slots = [(layer, n) for layer in range(LLAMA32_1B["layers"]) for n in names]
+    kv = [s for s in slots if s[1] in ("k", "v")][:8]
+    rest = [s for s in slots if s not in kv]
+    cls = {s: ("C", "R") for s in kv}
+    for i, s in enumerate(rest):
+        cls[s] = ("N", "C") if i < 15 else (("C", "C") if i < 15 + 69 else ("C", "N"))
+    return [(layer, n, cls[(layer, n)][0], "N", cls[(layer, n)][1]) for layer, n in slots]
 
 
 # --------------------------------------------------------------------------------------

@@ -232,10 +232,54 @@ def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
 
 
 def test_foid_row_limit_is_reported():
-    x = torch.zeros((16385, 64), dtype=torch.bfloat16, device=DEV)
-    with pytest.raises(ah.AdahopError if hasattr(ah, "AdahopError") else Exception) as e:
+    x = torch.zeros((65537, 64), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(ah.AdahopError) as e:
         ah.debug_foid(x, k=8)
     assert "unsupported" in str(e.value)
+
+
+@pytest.mark.parametrize("k_strided", [False, True])
+@pytest.mark.parametrize("k", [64, 256])
+def test_foid_65536_rows_bitexact(k, k_strided):
+    # 65536 stored rows (e.g. 64k tokens per GPU for an OE on the token dimension): 16 select
+    # blocks whose survivors the last block merges (PAPER P:760 FOID, DESIGN R5 keys and ties)
+    R, K = 65536, 64
+    x, planted = synth.operand(R, K, "R", "X", case_id=R + k, count=12)
+    x[70000 % R] = x[123]                          # an exact key tie across select blocks
+    xin = x.T.copy() if k_strided else x
+    idx, keys = ah.debug_foid(dev_bf16(xin), k=k, k_strided=k_strided)
+    np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), O.foid_keys(x).view(np.uint64))
+    np.testing.assert_array_equal(idx.cpu().numpy(), O.foid_indices(x, k))
+    assert set(planted.rows) <= set(idx.cpu().numpy().tolist())
+
+
+def test_oe_left_on_65536_tokens_layer_sampled():
+    # dgrad OE-Left (RN: G_Y row-wise) with the extracted rows chosen among 65536 tokens: FOID over
+    # 65536 rows, the row mask of the dual quantiser beyond the old 32768-row bitmap, the outlier
+    # GEMM and the fused scatter; sampled against the oracle (all extracted rows included)
+    T, d_in, d_out = 65536, 256, 512
+    x, _ = synth.operand(T, d_in, "C", "X", case_id=961)
+    w, _ = synth.operand(d_out, d_in, "N", "W", case_id=962)
+    gy, planted = synth.operand(T, d_out, "R", "GY", case_id=963)
+    strats = ("IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT")
+    p = ah.Params(oe_k=64)
+    y, gx, gw = ah.linear_layer(dev_bf16(x), dev_bf16(w), dev_bf16(gy), strats, p, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    idx = O.foid_indices(gy, 64)
+    assert set(planted.rows) <= set(idx.tolist())
+    rows = np.concatenate([rng.integers(0, T, 1500), idx])
+    cols = rng.integers(0, d_in, rows.size)
+    a_store, b_store = O.path_operands("dgrad", x=x, w=w, gy=gy)
+    ref = O.sampled_entries(np.ascontiguousarray(a_store), np.ascontiguousarray(b_store), "OE_LEFT_IHT", rows, cols)
+    assert rel_fro(gx.cpu().numpy()[rows, cols], ref) <= TOL_OUT
+    # the wgrad (K = 65536 tokens) and fwd of the same call
+    for path, got, s in (("fwd", y, "IHT"), ("wgrad", gw, "OE_RIGHT_IHT")):
+        a_store, b_store = O.path_operands(path, x=x, w=w, gy=gy)
+        r_ = rng.integers(0, got.shape[0], 1500)
+        c_ = rng.integers(0, got.shape[1], 1500)
+        ref = O.sampled_entries(np.ascontiguousarray(a_store), np.ascontiguousarray(b_store), s, r_, c_)
+        assert rel_fro(got.cpu().numpy()[r_, c_], ref) <= TOL_OUT, path
 
 
 # ======================================================================= MXFP4 GEMM

@@ -1,0 +1,104 @@
+"""GPU parity of the split layer API (adahop_linear_forward / adahop_linear_backward):
+the forward quantises X and W once in both orientations and saves the FP4 column layouts with the
+OE indices and BF16 outlier slices ("both the quantized residual and the BF16 outlier tensor
+are saved to the context for backpropagation"); the backward consumes them. Results must equal
+adahop_linear_layer bitwise and the oracle within the north-star tolerance; the context must be
+smaller than the BF16 activation it replaces."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2604_02525_b200 as ah  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TOL_OUT = 1e-3
+
+
+def dev_bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, torch.bfloat16)
+
+
+def rel_fro(got, ref):
+    ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / np.linalg.norm(ref))
+
+
+# (fwd, dgrad, wgrad) strategies, (X, W, G_Y) patterns; includes the two wgrad strategies whose BF16
+# part needs all of X in the backward (OE-Left, Lv2 BF16) and OE on W's columns (dgrad OE-Right)
+CASES = [
+    (("IHT", "IHT", "OE_RIGHT_IHT"), ("C", "N", "C"), 1),
+    (("IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT"), ("C", "N", "R"), 1),
+    (("IHT", "IHT", "OE_LEFT_IHT"), ("N", "N", "C"), 1),
+    (("OE_LEFT_IHT", "OE_RIGHT_IHT", "IHT"), ("R", "C", "N"), 1),
+    (("OE_RIGHT_IHT", "IHT", "BF16"), ("C", "N", "R"), 2),
+]
+
+
+@pytest.mark.parametrize("shape", [(640, 384, 256), (2048, 1024, 512)])
+@pytest.mark.parametrize("strats,pats,level", CASES)
+def test_split_equals_layer_and_oracle(strats, pats, level, shape):
+    T, d_in, d_out = shape
+    px, pw, pg = pats
+    x, _ = synth.operand(T, d_in, px, "X", case_id=801)
+    w, _ = synth.operand(d_out, d_in, pw, "W", case_id=802)
+    gy, _ = synth.operand(T, d_out, pg, "GY", case_id=803)
+    p = ah.Params(oe_k=16, level=level)
+    xd, wd, gd = dev_bf16(x), dev_bf16(w), dev_bf16(gy)
+    y_l, gx_l, gw_l = ah.linear_layer(xd, wd, gd, strats, p, out_dtype=torch.float32)
+    y, ctx = ah.linear_forward(xd, wd, strats, p, out_dtype=torch.float32)
+    gx, gw = ah.linear_backward(gd, wd, ctx, gx_dtype=torch.float32, gw_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert ctx.needs_x == (strats[2] == "BF16" or strats[2] == "OE_LEFT_IHT")
+    for a, b in ((y, y_l), (gx, gx_l), (gw, gw_l)):
+        np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+    for path, got, s in (("fwd", y, strats[0]), ("dgrad", gx, strats[1]), ("wgrad", gw, strats[2])):
+        assert rel_fro(got.cpu().numpy(), O.linear(path, s, x=x, w=w, gy=gy, k=16)) <= TOL_OUT, (path, s)
+
+
+def test_split_backward_reads_only_the_context():
+    # X is released (and its memory overwritten) between forward and backward when the wgrad
+    # strategy does not need it: the backward result must not change
+    T, d_in, d_out = 1024, 512, 256
+    x, _ = synth.operand(T, d_in, "C", "X", case_id=811)
+    w, _ = synth.operand(d_out, d_in, "N", "W", case_id=812)
+    gy, _ = synth.operand(T, d_out, "C", "GY", case_id=813)
+    strats = ("IHT", "IHT", "OE_RIGHT_IHT")
+    p = ah.Params(oe_k=16)
+    xd, wd, gd = dev_bf16(x), dev_bf16(w), dev_bf16(gy)
+    _, ctx = ah.linear_forward(xd, wd, strats, p)
+    assert not ctx.needs_x and ctx.x is None
+    gx0, gw0 = ah.linear_backward(gd, wd, ctx)
+    xd.fill_(7.0)                     # the activation is gone
+    gx1, gw1 = ah.linear_backward(gd, wd, ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(gx0, gx1) and torch.equal(gw0, gw1)
+    ref = O.linear("wgrad", "OE_RIGHT_IHT", x=x, gy=gy, k=16)
+    assert rel_fro(gw0.cpu().numpy(), ref) <= TOL_OUT
+
+
+@pytest.mark.parametrize("model,linear", [("llama32_1b", "gate"), ("llama3_8b", "q")])
+def test_context_memory_vs_bf16_activation(model, linear):
+    # the saved activation state per linear: FP4 codes + E8M0 scales of X's
+    # column layout, the OE slice of X and W's FP4 column layout, against the BF16 X a BF16
+    # linear keeps for its wgrad
+    spec = {"llama32_1b": synth.LLAMA32_1B, "llama3_8b": synth.LLAMA3_8B}[model]
+    _, d_in, d_out = next(t for t in spec["linears"] if t[0] == linear)
+    T = 16384
+    strats = ("IHT", "IHT", "OE_RIGHT_IHT")
+    p = ah.Params()
+    n = ah.linear_ctx_bytes(T, d_in, d_out, strats, p)
+    x_bf16 = T * d_in * 2
+    fp4_x = T * d_in // 2 + T * d_in // 32
+    fp4_w = d_in * d_out // 2 + d_in * d_out // 32
+    slice_x = 64 * T * 2
+    assert fp4_x + fp4_w + slice_x <= n <= fp4_x + fp4_w + slice_x + 8 * 4096
+    # the activation part (FP4 X + its BF16 outlier columns) vs the BF16 X: > 3x smaller
+    assert x_bf16 / (n - fp4_w) > 3.0
