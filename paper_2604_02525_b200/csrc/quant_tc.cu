@@ -54,13 +54,21 @@ constexpr int kThreads = 128 + kEpiGroups * 128;   // warps 0..3 control, 4..19 
 constexpr int kHBytes = 32 * 32 * 2;  // H_32 in the canonical no-swizzle K-major layout
 constexpr int kStg = 128 * 64;        // one tile's codes of one orientation: 128 stored rows x 64 bytes
 
-// The OE rows / columns of one (job, orientation): the sorted index list (k <= 256) staged in
-// shared memory; membership is a binary search, so the operand's row count is not limited.
+// The OE rows / columns of one (job, orientation): the sorted index list (k <= 256) and a
+// membership bitmap over the operand's stored rows, both staged in shared memory (the bitmap is
+// sized per launch: ceil(rows / 32) words; a per-row binary search instead made the quant stage
+// 9 % slower, profiles/r02k_mask_ab.txt).
+constexpr int64_t kMaskMaxRows = kFoidMaxRows;   // the OE index sets come from FOID
 struct Mask {
   int32_t idx[256];
 };
-__device__ __forceinline__ void mask_build(Mask* m, const int32_t* __restrict__ idx, int n, int64_t) {
+__device__ __forceinline__ void mask_build(Mask* m, uint32_t* bits, const int32_t* __restrict__ idx, int n,
+                                           int64_t rows) {
+  const int words = int((rows + 31) / 32);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) bits[i] = 0u;
   for (int i = threadIdx.x; i < n; i += blockDim.x) m->idx[i] = idx[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicOr(&bits[idx[i] >> 5], 1u << (idx[i] & 31));
   __syncthreads();
 }
 // first position in the sorted list idx[0, n) whose value is >= v
@@ -71,10 +79,6 @@ __device__ __forceinline__ int lower_bound_idx(const int32_t* idx, int n, int v)
     if (idx[mid] < v) lo = mid + 1; else hi = mid;
   }
   return lo;
-}
-__device__ __forceinline__ bool mask_hit(const Mask* m, int n, int64_t r) {
-  const int p = lower_bound_idx(m->idx, n, int(r));
-  return p < n && m->idx[p] == r;
 }
 __device__ __forceinline__ int mask_slot(const Mask* m, int n, int64_t r) {
   int lo = 0, hi = n - 1;
@@ -89,6 +93,7 @@ __device__ __forceinline__ int mask_slot(const Mask* m, int n, int64_t r) {
 
 struct Out {
   uint8_t* q; uint8_t* sf; const int32_t* zero; int nzero; __nv_bfloat16* slice; float* had;
+  int bits_off;   // first word of this mask's bitmap in the shared bitmap region
 };
 
 // kind::f16 instruction descriptor: D f32, A/B bf16, M = 128, N = 32, A major selectable.
@@ -195,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   uint64_t* stgfree = staged + 2;      // [2] store warp -> epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stgfree + 2);
   Mask* masks = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [job][row, col]
+  uint32_t* mbits = reinterpret_cast<uint32_t*>(masks + 2 * kMaxJobs);               // bitmaps (Out::bits_off)
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const int ntiles = J.ntiles;
   constexpr int kEpiWarps = kEpiGroups * 4;
@@ -229,8 +235,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   ptx::griddep_launch();
   ptx::griddep_wait();   // the prologue above overlapped the previous kernel's tail
   for (int jb = 0; jb < J.n; ++jb) {
-    if (kRow && J.j[jb].orow.nzero > 0) mask_build(&masks[2 * jb], J.j[jb].orow.zero, J.j[jb].orow.nzero, J.j[jb].R);
-    if (kCol && J.j[jb].ocol.nzero > 0) mask_build(&masks[2 * jb + 1], J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
+    if (kRow && J.j[jb].orow.nzero > 0)
+      mask_build(&masks[2 * jb], mbits + J.j[jb].orow.bits_off, J.j[jb].orow.zero, J.j[jb].orow.nzero, J.j[jb].R);
+    if (kCol && J.j[jb].ocol.nzero > 0)
+      mask_build(&masks[2 * jb + 1], mbits + J.j[jb].ocol.bits_off, J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
   }
   ptx::fence_proxy_async();  // H written by threads, read by the tensor core
   ptx::tc_fence_before();
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       uint8_t* sst = sfstg + (oi * 2 + buf) * 512;
       const int64_t srow = (col_side ? int64_t(ct) * 128 : int64_t(rt) * 128) + row;
       const int64_t kb0 = (col_side ? int64_t(rt) * 4 : int64_t(ct) * 4) + blk0;   // first K-block of this group
-      const bool extracted = srow < rows_total && o.nzero > 0 && mask_hit(m, o.nzero, srow);
+      const bool extracted = srow < rows_total && o.nzero > 0 && ((mbits[o.bits_off + (srow >> 5)] >> (srow & 31)) & 1u);
       ptx::mbar_wait(&stgfree[buf], (use & 1) ^ 1);   // the store warp has read this staging buffer
       ptx::mbar_wait(&tfull[buf], use & 1);
       if (warp == 4 && lane == 0) QTC_T(3, lt);
@@ -474,23 +482,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 
 }  // namespace qtc
 
-size_t quant_tc_smem(bool masks) {
+// bitmap_words: the total size of the launch's OE membership bitmaps (0 without masks)
+size_t quant_tc_smem(bool masks, int64_t bitmap_words) {
   return size_t(qtc::kStages) * qtc::kTile + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
-         (masks ? 2 * qtc::kMaxJobs * sizeof(qtc::Mask) : 0);
+         (masks ? 2 * qtc::kMaxJobs * sizeof(qtc::Mask) + size_t(bitmap_words) * 4 : 0);
 }
+// every (job, orientation) of a launch may carry a mask over up to kMaskMaxRows stored rows
+static size_t quant_tc_smem_max() { return quant_tc_smem(true, 2 * qtc::kMaxJobs * (qtc::kMaskMaxRows / 32)); }
 
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask) {
-  (void)R; (void)C; (void)row_mask; (void)col_mask;   // OE masks are index lists: no row limit
-  return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+         (!row_mask || R <= qtc::kMaskMaxRows) && (!col_mask || C <= qtc::kMaskMaxRows);
 }
 
 template <bool kRow, bool kCol, bool kHad>
-static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int num_sms, cudaStream_t st) {
-  const size_t smem = quant_tc_smem(masks);
+static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int64_t bitmap_words, int num_sms, cudaStream_t st) {
+  const size_t smem = quant_tc_smem(masks, bitmap_words);
   static std::atomic<uint64_t> attr{0};
   cudaError_t ae = once_per_device(attr, [] {
     return cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(quant_tc_smem(true)));
+                                int(quant_tc_smem_max()));
   });
   if (ae != cudaSuccess) return ae;
   const unsigned grid = unsigned(J.ntiles < num_sms ? J.ntiles : num_sms);
@@ -606,6 +617,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
   const bool row = jobs[0].q_row != nullptr, col = jobs[0].q_col != nullptr;
   const bool had = jobs[0].had_row != nullptr || jobs[0].had_col != nullptr;
   bool masks = false;
+  int64_t words = 0;   // bitmap words of the launch's masks
   int tiles = 0;
   for (int i = 0; i < n; ++i) {
     const QuantTcJob& q = jobs[i];
@@ -630,19 +642,29 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     tiles += jj.ctiles * int((q.R + 127) / 128);
     jj.kch_row = sf_kchunks(q.C);
     jj.kch_col = sf_kchunks(q.R);
-    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, fused ? q.slice_row : nullptr, q.had_row};
-    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, fused ? q.slice_col : nullptr, q.had_col};
-    masks |= (row && q.nrow_zero > 0) || (col && q.ncol_zero > 0);
+    jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, fused ? q.slice_row : nullptr, q.had_row, 0};
+    jj.ocol = qtc::Out{q.q_col, q.sf_col, q.col_zero, col ? q.ncol_zero : 0, fused ? q.slice_col : nullptr, q.had_col, 0};
+    if (jj.orow.nzero > 0) {
+      if (q.R > qtc::kMaskMaxRows) return cudaErrorInvalidValue;
+      jj.orow.bits_off = int(words);
+      words += (q.R + 31) / 32;
+    }
+    if (jj.ocol.nzero > 0) {
+      if (q.C > qtc::kMaskMaxRows) return cudaErrorInvalidValue;
+      jj.ocol.bits_off = int(words);
+      words += (q.C + 31) / 32;
+    }
+    masks |= jj.orow.nzero > 0 || jj.ocol.nzero > 0;
   }
   J.ntiles = tiles;
   if (launches) ++*launches;
   cudaError_t e = cudaSuccess;
-  if (row && col) e = had ? launch_tc<true, true, true>(J, masks, num_sms, st)
-                          : launch_tc<true, true, false>(J, masks, num_sms, st);
-  else if (row) e = had ? launch_tc<true, false, true>(J, masks, num_sms, st)
-                        : launch_tc<true, false, false>(J, masks, num_sms, st);
-  else if (col) e = had ? launch_tc<false, true, true>(J, masks, num_sms, st)
-                        : launch_tc<false, true, false>(J, masks, num_sms, st);
+  if (row && col) e = had ? launch_tc<true, true, true>(J, masks, words, num_sms, st)
+                          : launch_tc<true, true, false>(J, masks, words, num_sms, st);
+  else if (row) e = had ? launch_tc<true, false, true>(J, masks, words, num_sms, st)
+                        : launch_tc<true, false, false>(J, masks, words, num_sms, st);
+  else if (col) e = had ? launch_tc<false, true, true>(J, masks, words, num_sms, st)
+                        : launch_tc<false, true, false>(J, masks, words, num_sms, st);
   if (e != cudaSuccess) return e;
   return after ? gathers() : cudaSuccess;
 }
