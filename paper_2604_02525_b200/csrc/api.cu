@@ -173,6 +173,12 @@ int current_device() {
   return cudaGetDevice(&d) == cudaSuccess && d >= 0 && d < 64 ? d : -1;
 }
 
+// ADAHOP_OR_FUSED=0 (experiment builds) runs the wgrad OE-Right product as a BF16 GEMM instead
+bool or_fusion_enabled() {
+  static const bool on = knob("ADAHOP_OR_FUSED", 1) == 1;
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = knob("ADAHOP_PDL", 1) != 0;
   return on;
@@ -508,6 +514,8 @@ struct LayerPlan {
   Buf idx_row[3], idx_col[3], slice_row[3], slice_col[3];
   Buf keys_row[3], keys_col[3];   // per-FOID scratch
   Buf part[3], dt[3];             // per-path outlier split-K partials and folded Dt
+  int or_kk = 0;                  // wgrad OE-Right product fused into G_Y's quant pass (0: not planned)
+  Buf or_part, or_ticket;         // its per-(band, CTA) partials; the GEMM pre-fold's CTA count
   int splits[3];
   int64_t npad[3], mbig[3];
   size_t ws_total = 0, ctx_total = 0;
@@ -583,6 +591,17 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     L->splits[path] = bf16_gemm_splits(L->mbig[path], MNK[path][2], sms);
     take(L->part[path], size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4, false);
     take(L->dt[path], size_t(kk) * size_t(L->mbig[path]) * 4, false);
+  }
+  // wgrad OE-Right (A = G_Y^T, B_out = X[:, S]): the product A B_out accumulates in G_Y's quant
+  // pass when G_Y is quantised in both orientations there ("fuses ... into a single kernel")
+  if (or_fusion_enabled() && s[2] == ADAHOP_OE_RIGHT_IHT && p->oe_k > 0 && L->kk_col[0] > 0 &&
+      L->need_row[2] && L->need_col[2]) {
+    const size_t b = quant_tc_or_part_bytes(T, d_out, L->kk_col[0], sms);
+    if (b > 0) {
+      L->or_kk = L->kk_col[0];
+      take(L->or_part, b, false);
+      take(L->or_ticket, 4, false);
+    }
   }
   L->ws_total = c[0].take(0) + 256;
   L->ctx_total = split ? c[1].take(0) + 256 : 0;
@@ -669,12 +688,21 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
         L.kk_col[t] ? sp.p<const int32_t>(L.idx_col[t]) : nullptr, L.kk_col[t],
         L.kk_col[t] ? sp.p<__nv_bfloat16>(L.slice_col[t]) : nullptr, sp.p<uint8_t>(L.q_col[t]), sp.p<uint8_t>(L.sf_col[t]),
         nullptr};
+    if (t == 2 && L.or_kk > 0) {
+      QuantTcJob& q = tc_jobs[n_tc - 1];
+      q.or_slice = sp.p<const __nv_bfloat16>(L.slice_col[0]);
+      q.or_kk = L.or_kk;
+      q.or_part = sp.p<float>(L.or_part);
+      q.or_part_bytes = quant_tc_or_part_bytes(R, C, L.or_kk, sms);
+      q.or_ticket = sp.p<unsigned>(L.or_ticket);
+    }
     if ((R % 128) || (C % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_row[t]), 0, size_t(sf_bytes(R, C)), cs));
     if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_col[t]), 0, size_t(sf_bytes(C, R)), cs));
   }
+  bool or_fused = false;
   if (n_tc) {
     int nl = 0;
-    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, sms, cs, &nl));
+    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, sms, cs, &nl, &or_fused));
     launches += nl;
   }
   for (int t = 0; t < 3; ++t) {
@@ -722,6 +750,11 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
     const bool col = left ? kPathAo[path] : kPathBo[path];
     const int kk = col ? L.kk_col[t] : L.kk_row[t];
     const int32_t* idx = sp.p<const int32_t>(col ? L.idx_col[t] : L.idx_row[t]);
+    if (path == 2 && or_fused) {   // the quant pass left the product's partials; the epilogue sums them
+      patch[path] = quant_tc_or_patch(T, d_out, kk, sms, sp.p<const float>(L.or_part), sp.p<unsigned>(L.or_ticket),
+                                      sp.p<float>(L.dt[path]), idx);
+      continue;
+    }
     const __nv_bfloat16* slice = sp.p<const __nv_bfloat16>(col ? L.slice_col[t] : L.slice_row[t]);
     Bf16GemmArgs ga{};
     if (!left) { ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path]; }

@@ -94,13 +94,72 @@ __device__ __forceinline__ void epi_store_rows128(uint8_t* stg, const uint32_t (
 // the residual operand has the OE rows (OE-Left) / columns (OE-Right) zeroed, so the main
 // product is exactly 0 there and those entries of C are the BF16 outlier product alone:
 //   OE-Right (mode 1): C[m][idx[j]] = Dt[j][m]       OE-Left (mode 2): C[idx[j]][n] = Dt[j][n]
-// with Dt the split-K-folded, transposed outlier product (launch_outlier_fold).
+// with Dt the split-K-folded, transposed outlier product (launch_outlier_fold). With `ticket`
+// (mode 1, the product fused into the quant pass, quant_tc.cu) Dt is first folded by the GEMM's
+// own epilogue threads from the quant pass's per-(band, CTA) partials, in CTA order:
+//   Dt[j][m] = sum_s part[m / 128][s][j][m % 128],  s < the band's slot count,
+// each CTA a disjoint share while its first main loop runs; every CTA then counts itself in on
+// `ticket` (zeroed by the quant pass) and the first patch waits for all of them (the persistent
+// grid is co-resident).
 struct OePatch {
   const float* Dt;         // [k][Mb]
   const int32_t* idx;      // sorted, k entries
   int64_t Mb;
   int k, mode;             // mode 0: none
+  const float* part = nullptr;   // [Mb / 128 bands][spb][npad][128]
+  unsigned* ticket = nullptr;
+  int spb = 0, npad = 0;
+  int or_n = 0, or_rtiles = 0, or_chunks = 0;   // the quant pass's chunking (see qtc::OrSpec)
 };
+__device__ __forceinline__ float oe_fold_value(const OePatch& op, int j, int64_t m) {
+  const int ct = int(m >> 7);
+  const int64_t u0 = int64_t(ct) * op.or_rtiles;
+  const int64_t u1 = min(int64_t(op.or_n), u0 + op.or_rtiles) - 1;
+  const int nslots = int(((u1 + 1) * op.or_chunks - 1) / op.or_n - ((u0 + 1) * op.or_chunks - 1) / op.or_n) + 1;
+  const float* p = op.part + (int64_t(ct) * op.spb * op.npad + j) * 128 + (m & 127);
+  const int64_t stride = int64_t(op.npad) * 128;
+  float v = 0.f;
+  int s = 0;
+  for (; s + 4 <= nslots; s += 4) {   // independent loads, summed in slot order
+    const float a = __ldg(p + s * stride), b = __ldg(p + (s + 1) * stride);
+    const float c = __ldg(p + (s + 2) * stride), d = __ldg(p + (s + 3) * stride);
+    v = (((v + a) + b) + c) + d;
+  }
+  for (; s < nslots; ++s) v += __ldg(p + s * stride);
+  return v;
+}
+// All epilogue threads of the CTA (tid < nthreads, named barrier `bar`): fold this CTA's share.
+__device__ __forceinline__ void oe_prefold(const OePatch& op, int tid, int nthreads, uint32_t bar) {
+  if (op.ticket == nullptr) return;
+  const int64_t total = int64_t(op.k) * op.Mb;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = per * blockIdx.x, hi = min(total, lo + per);
+  float* dt = const_cast<float*>(op.Dt);
+  for (int64_t e = lo + tid; e < hi; e += nthreads) {
+    const int j = int(e / op.Mb);
+    dt[e] = oe_fold_value(op, j, e - int64_t(j) * op.Mb);
+  }
+  __threadfence();
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthreads) : "memory");
+  if (tid == 0) atomicAdd(op.ticket, 1u);
+}
+// Whole warp, before its first patch: every CTA has folded its share.
+__device__ __forceinline__ void oe_prefold_wait(const OePatch& op) {
+  if (op.ticket == nullptr) return;
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.ticket) : "memory");
+      if (v >= gridDim.x) break;
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+}
+// Dt values written in this kernel (pre-fold) are read through L2, never the non-coherent path
+__device__ __forceinline__ float oe_patch_value(const OePatch& op, int j, int64_t m) {
+  return op.ticket ? __ldcg(op.Dt + int64_t(j) * op.Mb + m) : __ldg(op.Dt + int64_t(j) * op.Mb + m);
+}
 
 // [j0, j1) = the entries of sorted idx in [lo, hi): one pass of the warp over idx (k <= 256)
 __device__ __forceinline__ void idx_range(const int32_t* __restrict__ idx, int k, int64_t lo, int64_t hi, int& j0,
@@ -132,7 +191,7 @@ __device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& 
     if (m < M)
       for (int j = j0; j < j1; ++j) {
         const int cl = int(__ldg(op.idx + j) - n0);
-        const float v = __ldg(op.Dt + int64_t(j) * op.Mb + m);
+        const float v = oe_patch_value(op, j, m);
         uint8_t* dst = stg + lane * kEpiPitch + cl * elt;
         if (elt == 4) *reinterpret_cast<float*>(dst) = v;
         else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);

@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp
+    // fused outlier product: fold this CTA's share of Dt while the first main loop runs
+    oe_prefold(oe, int(threadIdx.x) - 128, 128, 1);
+    oe_prefold_wait(oe);
     int64_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
       int64_t mb, nb;

@@ -263,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
     const uint32_t empty_leader = ptx::mapa(&tempty[0], leader_rank);
     const uint32_t ovl_leader = ptx::mapa(tovl, leader_rank);
+    // fused outlier product: fold this CTA's share of Dt while the first main loop runs
+    oe_prefold(oe, int(threadIdx.x) - 128, kEpiWarps * 32, 1);
+    oe_prefold_wait(oe);
     int64_t lt = 0;
     for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
       int64_t smb, snb;

@@ -634,7 +634,7 @@ cudaError_t launch_iht_quant_dual(const __nv_bfloat16* in, int64_t R, int64_t C,
     const QuantTcJob q{in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, nullptr,
                        col_zero, ncol_zero, slice_col, q_col, sf_col, nullptr};
     g_quant_launches = 0;
-    return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+    return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches, nullptr);
   }
   if ((ld * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(in) & 15) != 0) return cudaErrorInvalidValue;
   CUtensorMap tm;
@@ -805,13 +805,13 @@ cudaError_t launch_iht_quant(const void* in, bool in_f32, int64_t R, int64_t K, 
       const QuantTcJob q{src, R, K, ld, zero_rows, nzero, slice, codes, sf, had_out,
                          nullptr, 0, nullptr, nullptr, nullptr, nullptr};
       g_quant_launches = 0;
-      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches, nullptr);
     }
     if (kstrided && quant_tc_supported(K, R, ld, in, false, nzero > 0)) {   // T = [K][R], column orientation
       const QuantTcJob q{src, K, R, ld, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
                          zero_rows, nzero, slice, codes, sf, had_out};
       g_quant_launches = 0;
-      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches);
+      return launch_quant_tc_multi(&q, 1, num_sms, st, &g_quant_launches, nullptr);
     }
   }
 #define ADAHOP_Q(T, H, S)                                                                   \

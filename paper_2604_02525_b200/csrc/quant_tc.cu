@@ -46,9 +46,16 @@ __device__ long long g_qtc_trace[5][64];
 namespace adahop {
 namespace qtc {
 
-constexpr int kStages = 4;
 constexpr int kBox = 16384;           // 128 rows x 128 bytes (64 bf16 columns)
 constexpr int kTile = 2 * kBox;       // 128 x 128 bf16
+// Ring depth and stage size: the fused outlier product (kOr) adds the tile's slice rows (two
+// boxes of 64 rows x npad <= 64 slice rows) to every stage and runs 3 stages deep.
+constexpr int kOrMaxN = 64;
+constexpr int kOrBytes = 2 * kOrMaxN * 128;
+template <bool kOr> struct Ring {
+  static constexpr int kStages = kOr ? 3 : 4;
+  static constexpr int kStage = kTile + (kOr ? kOrBytes : 0);
+};
 constexpr int kEpiGroups = 4;         // epilogue groups of 4 warps (one warp per TMEM lane quarter)
 constexpr int kThreads = 128 + kEpiGroups * 128;   // warps 0..3 control, 4..19 epilogue
 constexpr int kHBytes = 32 * 32 * 2;  // H_32 in the canonical no-swizzle K-major layout
@@ -163,46 +170,102 @@ __device__ __forceinline__ void quant_block(const uint32_t (&d)[32], uint4& code
   codes = make_uint4(e2m1x8(v), e2m1x8(v + 8), e2m1x8(v + 16), e2m1x8(v + 24));
 }
 
-// Several tensors in one persistent launch: the global tile index runs over the tiles of job 0,
-// then job 1, ...; every role finds its tile's job by the prefix offsets.
+// Several tensors in one persistent launch. The "plain" jobs' tiles form one global index (job 0's
+// tiles, then job 1's, ...) that CTA b visits with stride gridDim.x, row bands first (ct fastest):
+// concurrent CTAs stream whole row bands, so the bf16 reads are long contiguous runs.
+//
+// Fused outlier product (OE-Right wgrad, eq:oe_right P:280 with A = G_Y^T, B_out = X[:, S]):
+//   P[c][j] = sum_r T[r][c] * S[j][r]     (T = the streamed tensor [R x C], S = the slice [kk][R])
+// The last job of the launch may carry it (Jobs::orr). Its tiles are visited after the plain ones,
+// column band by column band (rt fastest), in contiguous chunks: OR-chunk b (of min(n, SMs)) goes
+// to CTA b, so a CTA accumulates a band's product across consecutive token tiles in TMEM (one
+// tcgen05.mma kind::f16 per 16 rows, A = the staged tile read MN-major, B = the TMA-loaded slice
+// rows) and writes one partial per (band, CTA) segment; k_or_fold sums a band's partials in CTA
+// order (deterministic) into Dt[j][c] for the MXFP4 GEMM epilogue (eq:oe_right's "+ A B_out").
 constexpr int kMaxJobs = 3;
-// Tiles run along the rows of T first (ct fastest): concurrent CTAs stream whole row bands,
-// so the bf16 reads are long contiguous runs.
 struct Job {
   int64_t R, C;
   int ctiles, tile0;
   int64_t kch_row, kch_col;
   Out orow, ocol;
 };
-struct Jobs {
-  CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs];
-  Job j[kMaxJobs];
-  int n, ntiles;
+struct OrSpec {
+  int on;          // 1: the last job carries the outlier product
+  int npad, kk;    // MMA N (kk rounded up to 16, <= kOrMaxN) and slice rows
+  int n, rtiles;   // OR tiles (= rtiles x ctiles of the job) and row tiles per column band
+  int chunks;      // min(n, SMs): OR-chunk b = tiles [b n / chunks, (b + 1) n / chunks)
+  int spb;         // partial slots per band
+  float* part;     // [ctiles][spb][npad][128] fp32
+  unsigned* ticket;   // zeroed here; the MXFP4 GEMM's pre-fold counts its CTAs on it
 };
-__device__ __forceinline__ int job_of(const Jobs& J, int tile) {
-  int jb = 0;
-  while (jb + 1 < J.n && tile >= J.j[jb + 1].tile0) ++jb;
-  return jb;
+struct Jobs {
+  CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs], tor;
+  Job j[kMaxJobs];
+  int n, ntiles;   // jobs; plain tiles (every job but the OR job)
+  OrSpec orr;
+};
+struct TileRef {
+  int jb, rt, ct;
+  bool orr, first, last;   // an OR tile; first / last tile of its (band, CTA) segment
+};
+__device__ __forceinline__ int or_chunk_lo(const OrSpec& o, int b) { return int((int64_t(b) * o.n) / o.chunks); }
+// The i-th tile of this CTA; false past its last tile (the same sequence in every role).
+__device__ __forceinline__ bool tile_at(const Jobs& J, int i, TileRef& t) {
+  const int b = int(blockIdx.x), G = int(gridDim.x);
+  const int np = J.ntiles > b ? (J.ntiles - b + G - 1) / G : 0;
+  if (i < np) {
+    const int g = b + i * G;
+    const int nplain = J.n - (J.orr.on ? 1 : 0);
+    int jb = 0;
+    while (jb + 1 < nplain && g >= J.j[jb + 1].tile0) ++jb;
+    const int lt0 = g - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
+    t = TileRef{jb, lt0 / ctiles, lt0 % ctiles, false, false, false};
+    return true;
+  }
+  if (!J.orr.on || b >= J.orr.chunks) return false;
+  const int lo = or_chunk_lo(J.orr, b), hi = or_chunk_lo(J.orr, b + 1);
+  const int u = lo + (i - np);
+  if (u >= hi) return false;
+  const int rt = u % J.orr.rtiles;
+  t = TileRef{J.n - 1, rt, u / J.orr.rtiles, true, u == lo || rt == 0, u + 1 == hi || rt == J.orr.rtiles - 1};
+  return true;
+}
+// OR-chunk holding OR tile u: the largest b with lo(b) <= u
+__device__ __forceinline__ int or_chunk_of(const OrSpec& o, int u) {
+  return int(((int64_t(u) + 1) * o.chunks - 1) / o.n);
 }
 
-template <bool kRow, bool kCol, bool kHad>
+// kind::f16 instruction descriptor of the outlier product: M = 128 (tile columns, A MN-major),
+// N = npad (slice rows, B K-major), D f32.
+__host__ __device__ constexpr uint32_t idesc_or(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+
+template <bool kRow, bool kCol, bool kHad, bool kOr>
 __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant__ Jobs J) {
+  using RG = Ring<kOr>;
+  constexpr int kStages = RG::kStages;
+  // TMEM: the Hadamard accumulators double-buffered (2 x 256 columns); with the fused outlier
+  // product single-buffered at [0, 256) and the product's accumulator at [256, 256 + npad)
+  constexpr int kTBufs = kOr ? 1 : 2;
+  constexpr uint32_t kOrCol = 256;
   extern __shared__ __align__(1024) uint8_t smem_q[];
   uint8_t* ring = smem_q + ((1024u - (ptx::smem_u32(smem_q) & 1023u)) & 1023u);
-  uint8_t* stg = ring + kStages * kTile;   // codes [orientation][buffer][128 rows x 64 B], 64B-swizzled
+  uint8_t* stg = ring + kStages * RG::kStage;   // codes [orientation][buffer][128 rows x 64 B], 64B-swizzled
   uint8_t* sfstg = stg + 4 * kStg;         // scales [orientation][buffer][512 B] = one SF chunk each
   uint8_t* hmat = sfstg + 4 * 512;
   uint64_t* full = reinterpret_cast<uint64_t*>(hmat + kHBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* empty = full + 4;
+  uint64_t* tfull = empty + 4;         // [2]
   uint64_t* tempty = tfull + 2;        // [2]
   uint64_t* staged = tempty + 2;       // [2] epilogue warps -> store warp
   uint64_t* stgfree = staged + 2;      // [2] store warp -> epilogue warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stgfree + 2);
+  uint64_t* orfull = stgfree + 2;      // MMA -> flush warps: a segment's product is complete
+  uint64_t* orempty = orfull + 1;      // flush warps -> MMA: the product accumulator is drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(orempty + 1);
   Mask* masks = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [job][row, col]
   uint32_t* mbits = reinterpret_cast<uint32_t*>(masks + 2 * kMaxJobs);               // bitmaps (Out::bits_off)
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int ntiles = J.ntiles;
   constexpr int kEpiWarps = kEpiGroups * 4;
 
   // ---- setup: barriers, H_32, TMEM, OE masks
@@ -212,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       if (kRow) ptx::prefetch_tmap(&J.tqr[jb]);
       if (kCol) ptx::prefetch_tmap(&J.tqc[jb]);
     }
+    if (kOr) ptx::prefetch_tmap(&J.tor);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 2);   // MMA commit + OE-slice gather warp
@@ -222,6 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       ptx::mbar_init(&staged[b], kEpiWarps);
       ptx::mbar_init(&stgfree[b], 1);
     }
+    ptx::mbar_init(orfull, 1);
+    ptx::mbar_init(orempty, 4);       // the four warps of epilogue group 0
     ptx::fence_barrier_init();
   }
   // H (n = j rows, k = i): core matrices of 8 rows x 16 bytes, (n/8, k/8) -> ((n/8)*4 + k/8)*128
@@ -240,27 +306,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     if (kCol && J.j[jb].ocol.nzero > 0)
       mask_build(&masks[2 * jb + 1], mbits + J.j[jb].ocol.bits_off, J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
   }
+  // the previous user of the ticket (an earlier GEMM) has completed: griddep_wait above
+  if (kOr && blockIdx.x == 0 && threadIdx.x == 0) *J.orr.ticket = 0u;
   ptx::fence_proxy_async();  // H written by threads, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int first = blockIdx.x, stride = gridDim.x;
+  const int npad = kOr ? J.orr.npad : 0;
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = first; tile < ntiles; tile += stride) {
-      const int jb = job_of(J, tile);
-      const int lt0 = tile - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
-      const int rt = lt0 / ctiles, ct = lt0 % ctiles;
+    TileRef t;
+    for (int i = 0; tile_at(J, i, t); ++i) {
       ptx::mbar_wait(&empty[stage], phase ^ 1);
-      QTC_T(0, (tile - first) / stride);
-      uint8_t* dst = ring + stage * kTile;
-      ptx::mbar_arrive_expect_tx(&full[stage], kTile);
-      ptx::tma_load_2d(dst, &J.tm[jb], &full[stage], int32_t(ct * 128), int32_t(rt * 128));
-      ptx::tma_load_2d(dst + kBox, &J.tm[jb], &full[stage], int32_t(ct * 128 + 64), int32_t(rt * 128));
+      QTC_T(0, i);
+      uint8_t* dst = ring + stage * RG::kStage;
+      const bool o = kOr && t.orr;
+      ptx::mbar_arrive_expect_tx(&full[stage], kTile + (o ? 2 * npad * 128 : 0));
+      ptx::tma_load_2d(dst, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128), int32_t(t.rt * 128));
+      ptx::tma_load_2d(dst + kBox, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128 + 64), int32_t(t.rt * 128));
+      if (o) {
+        // the slice rows S[0, npad) x tile rows [128 rt, +128) as two 64-row K boxes (rows >= kk: zeros)
+        ptx::tma_load_2d(dst + kTile, &J.tor, &full[stage], int32_t(t.rt * 128), 0);
+        ptx::tma_load_2d(dst + kTile + npad * 128, &J.tor, &full[stage], int32_t(t.rt * 128 + 64), 0);
+      }
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 1) {
@@ -269,15 +341,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     const uint64_t bdesc = ptx::make_sdesc(ptx::smem_u32(hmat), 128, 512, 0);
     int stage = 0;
     uint32_t phase = 0;
-    int lt = 0;
-    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
-      const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
+    int segs = 0;   // completed outlier-product segments
+    TileRef t;
+    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+      const uint32_t buf = kTBufs == 2 ? uint32_t(lt & 1) : 0u;
+      const uint32_t use = kTBufs == 2 ? uint32_t(lt >> 1) : uint32_t(lt);
       ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
       QTC_T(1, lt);
       ptx::mbar_wait(&full[stage], phase);
       QTC_T(2, lt);
+      const bool o = kOr && t.orr;
+      // a new segment reuses the product accumulator once the previous segment is flushed
+      if (o && t.first && segs > 0) ptx::mbar_wait(orempty, uint32_t((segs - 1) & 1));
       ptx::tc_fence_after();
-      const uint32_t base = ptx::smem_u32(ring + stage * kTile);
+      const uint32_t base = ptx::smem_u32(ring + stage * RG::kStage);
       const uint32_t d0 = tmem_base + buf * 256;
       // start-address field = bits [0,14) of the descriptor in 16-byte units: offsets add directly
       const uint64_t arow = ptx::make_sdesc(base, 16, 1024, 2);     // K-major (row blocks)
@@ -299,10 +376,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
             }
           }
         }
-        ptx::tc_commit(&empty[stage]);
+        // the epilogue waits only for the Hadamard MMAs; the stage waits for the product's too
         ptx::tc_commit(&tfull[buf]);
+        if (o) {
+          // P[c][j] += sum over the tile's 128 rows r of T[r][c] S[j][r]: eight K = 16 steps; A = the
+          // tile MN-major (as the column blocks), B = the slice boxes K-major (128B swizzle)
+          const uint64_t bor = ptx::make_sdesc(base + kTile, 16, 1024, 2);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_bf16(tmem_base + kOrCol, acol + uint64_t((k * 16 * 128) >> 4),
+                          bor + uint64_t(((k >> 2) * npad * 128 + (k & 3) * 32) >> 4), idesc_or(npad),
+                          (t.first && k == 0) ? 0u : 1u);
+        }
+        ptx::tc_commit(&empty[stage]);
+        if (o && t.last) ptx::tc_commit(orfull);
       }
       __syncwarp();
+      if (o && t.last) ++segs;
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 3) {
@@ -312,15 +402,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     // the MMA commit. out_row[s][c] = T[idx[s], c], out_col[s][r] = T[r, idx[s]].
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = first; tile < ntiles; tile += stride) {
-      const int jb = job_of(J, tile);
-      const Job& jj = J.j[jb];
-      const int lt0 = tile - jj.tile0;
-      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
+    TileRef t;
+    for (int i = 0; tile_at(J, i, t); ++i) {
+      const Job& jj = J.j[t.jb];
+      const int rt = t.rt, ct = t.ct;
       ptx::mbar_wait(&full[stage], phase);
-      const uint8_t* base = ring + stage * kTile;
+      const uint8_t* base = ring + stage * RG::kStage;
       if (kCol && jj.ocol.slice != nullptr && jj.ocol.nzero > 0) {
-        const Mask* m = &masks[2 * jb + 1];
+        const Mask* m = &masks[2 * t.jb + 1];
         const int n = jj.ocol.nzero;
         int j = lower_bound_idx(m->idx, n, ct * 128);
         const int j1 = lower_bound_idx(m->idx, n, ct * 128 + 128);
@@ -335,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         }
       }
       if (kRow && jj.orow.slice != nullptr && jj.orow.nzero > 0) {
-        const Mask* m = &masks[2 * jb];
+        const Mask* m = &masks[2 * t.jb];
         const int n = jj.orow.nzero;
         int j = lower_bound_idx(m->idx, n, rt * 128);
         const int j1 = lower_bound_idx(m->idx, n, rt * 128 + 128);
@@ -358,12 +447,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     // ------------------------------------------------------------ store warp
     // One TMA store of the 128 x 64-byte code box and one 512-byte bulk copy of the scale chunk
     // per orientation and tile, so the epilogue warps never stall on global-store issue.
-    int lt = 0;
-    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
-      const int jb = job_of(J, tile);
-      const Job jj = J.j[jb];   // by value: one param-space read per tile
-      const int lt0 = tile - jj.tile0;
-      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
+    TileRef t;
+    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+      const Job jj = J.j[t.jb];   // by value: one param-space read per tile
+      const int rt = t.rt, ct = t.ct;
       const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
       ptx::mbar_wait(&staged[buf], use & 1);
       if (ptx::elect_one()) {
@@ -376,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           const int64_t srow0 = cs ? int64_t(ct) * 128 : int64_t(rt) * 128;
           const int kt = cs ? rt : ct;   // K-tile index: K-blocks [4 kt, 4 kt + 4)
           if (!(QTC_ABLATE & 4))
-            ptx::tma_store_2d(cs ? &J.tqc[jb] : &J.tqr[jb], stg + (oi * 2 + buf) * kStg, kt * 64, int32_t(srow0));
+            ptx::tma_store_2d(cs ? &J.tqc[t.jb] : &J.tqr[t.jb], stg + (oi * 2 + buf) * kStg, kt * 64, int32_t(srow0));
           if (!(QTC_ABLATE & 8)) {
             uint8_t* gsf = (cs ? jj.ocol.sf : jj.orow.sf) + ((srow0 >> 7) * (cs ? jj.kch_col : jj.kch_row) + kt) * 512;
             ptx::bulk_store(gsf, sfstg + (oi * 2 + buf) * 512, 512);
@@ -394,7 +481,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     // ------------------------------------------------------------ epilogue
     // Dual launch: groups 0,1 -> row blocks {0,1},{2,3}; groups 2,3 -> column blocks {0,1},{2,3}.
     // Single orientation: group g -> block g. Four warps per SM sub-partition hide the
-    // TMEM-load -> amax -> convert latency chain of each block.
+    // TMEM-load -> amax -> convert latency chain of each block. Group 0 also flushes the outlier
+    // product of a finished segment (TMEM lane = tile column).
     constexpr int kOrients = (kRow ? 1 : 0) + (kCol ? 1 : 0);
     constexpr int kBlocksPerGroup = 4 * kOrients / kEpiGroups;
     constexpr int kGroupsPerOrient = kEpiGroups / kOrients;
@@ -407,23 +495,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     const uint32_t blk0 = sub * kBlocksPerGroup;
     const uint32_t oi = kRow ? orient : 0;     // staging slot of this orientation
     const uint32_t sw = (row >> 1) & 3;        // 64B swizzle of the staging row
-    int lt = 0;
-    for (int tile = first; tile < ntiles; tile += stride, ++lt) {
-      const int jb = job_of(J, tile);
-      const Job jj = J.j[jb];   // by value: one param-space read per tile
-      const int lt0 = tile - jj.tile0;
-      const int rt = lt0 / jj.ctiles, ct = lt0 % jj.ctiles;
+    int segs = 0;
+    TileRef t;
+    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+      const Job jj = J.j[t.jb];   // by value: one param-space read per tile
+      const int rt = t.rt, ct = t.ct;
       const Out& o = col_side ? jj.ocol : jj.orow;
-      const Mask* m = &masks[2 * jb + (col_side ? 1 : 0)];
+      const uint32_t* bits = mbits + o.bits_off;
       const int64_t K = col_side ? jj.R : jj.C;
       const int64_t rows_total = col_side ? jj.C : jj.R;
-      const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
-      uint8_t* st = stg + (oi * 2 + buf) * kStg;
-      uint8_t* sst = sfstg + (oi * 2 + buf) * 512;
+      const uint32_t sbuf = uint32_t(lt & 1), suse = uint32_t(lt >> 1);   // staging buffers
+      const uint32_t buf = kTBufs == 2 ? sbuf : 0u;                         // TMEM buffer
+      const uint32_t use = kTBufs == 2 ? suse : uint32_t(lt);
+      uint8_t* st = stg + (oi * 2 + sbuf) * kStg;
+      uint8_t* sst = sfstg + (oi * 2 + sbuf) * 512;
       const int64_t srow = (col_side ? int64_t(ct) * 128 : int64_t(rt) * 128) + row;
       const int64_t kb0 = (col_side ? int64_t(rt) * 4 : int64_t(ct) * 4) + blk0;   // first K-block of this group
-      const bool extracted = srow < rows_total && o.nzero > 0 && ((mbits[o.bits_off + (srow >> 5)] >> (srow & 31)) & 1u);
-      ptx::mbar_wait(&stgfree[buf], (use & 1) ^ 1);   // the store warp has read this staging buffer
+      const bool extracted = srow < rows_total && o.nzero > 0 && ((bits[srow >> 5] >> (srow & 31)) & 1u);
+      ptx::mbar_wait(&stgfree[sbuf], (suse & 1) ^ 1);   // the store warp has read this staging buffer
       ptx::mbar_wait(&tfull[buf], use & 1);
       if (warp == 4 && lane == 0) QTC_T(3, lt);
       ptx::tc_fence_after();
@@ -460,7 +549,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       }
       ptx::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&staged[buf]);
+      if (lane == 0) ptx::mbar_arrive(&staged[sbuf]);
+      if (kOr && t.orr && t.last) {
+        if (group == 0) {
+          // flush the finished segment: P[c = 128 ct + row][j] -> its (band, CTA) partial slot
+          ptx::mbar_wait(orfull, uint32_t(segs & 1));
+          ptx::tc_fence_after();
+          uint32_t p0[32], p1[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + kOrCol, p0);
+          if (npad > 32) ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + kOrCol + 32, p1);
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(orempty);
+          const int u0 = ct * J.orr.rtiles;
+          const int slot = int(blockIdx.x) - or_chunk_of(J.orr, u0);
+          float* dst = J.orr.part + (int64_t(ct) * J.orr.spb + slot) * npad * 128 + row;
+          // lanes = consecutive columns: one 128-byte store per (warp, j)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < npad) dst[int64_t(j) * 128] = __uint_as_float(p0[j]);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (32 + j < npad) dst[int64_t(32 + j) * 128] = __uint_as_float(p1[j]);
+        }
+        ++segs;
+      }
     }
   }
   ptx::tc_fence_before();
@@ -472,7 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 #if QTC_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t0 = g_qtc_trace[0][0];
-    for (int i = 0; i < 64 && first + i * stride < ntiles; ++i)
+    TileRef t;
+    for (int i = 0; i < 64 && tile_at(J, i, t); ++i)
       printf("qtc tile %2d: tma %7lld tempty %7lld full %7lld epi %7lld drained %7lld\n", i,
              g_qtc_trace[0][i] - t0, g_qtc_trace[1][i] - t0, g_qtc_trace[2][i] - t0, g_qtc_trace[3][i] - t0,
              g_qtc_trace[4][i] - t0);
@@ -483,29 +598,78 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 }  // namespace qtc
 
 // bitmap_words: the total size of the launch's OE membership bitmaps (0 without masks)
-size_t quant_tc_smem(bool masks, int64_t bitmap_words) {
-  return size_t(qtc::kStages) * qtc::kTile + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
+static size_t quant_tc_smem(bool masks, int64_t bitmap_words, bool orr) {
+  const size_t ring = orr ? size_t(qtc::Ring<true>::kStages) * qtc::Ring<true>::kStage
+                          : size_t(qtc::Ring<false>::kStages) * qtc::Ring<false>::kStage;
+  return ring + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
          (masks ? 2 * qtc::kMaxJobs * sizeof(qtc::Mask) + size_t(bitmap_words) * 4 : 0);
 }
+constexpr size_t kSmemLimit = 232448;   // 227 KB per CTA on sm_100
 // every (job, orientation) of a launch may carry a mask over up to kMaskMaxRows stored rows
-static size_t quant_tc_smem_max() { return quant_tc_smem(true, 2 * qtc::kMaxJobs * (qtc::kMaskMaxRows / 32)); }
+static size_t quant_tc_smem_max(bool orr) {
+  const size_t m = quant_tc_smem(true, 2 * qtc::kMaxJobs * (qtc::kMaskMaxRows / 32), orr);
+  return m < kSmemLimit ? m : kSmemLimit;
+}
 
 bool quant_tc_supported(int64_t R, int64_t C, int64_t ld, const void* in, bool row_mask, bool col_mask) {
   return (ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
          (!row_mask || R <= qtc::kMaskMaxRows) && (!col_mask || C <= qtc::kMaskMaxRows);
 }
 
-template <bool kRow, bool kCol, bool kHad>
+// Partial slots per column band of the fused outlier product over T [R x C] when the OR tiles
+// are cut into chunks = min(tiles, num_sms) contiguous chunks (host copy of the device rule).
+static int or_slots_per_band(const qtc::OrSpec& o) {
+  int spb = 0;
+  for (int ct = 0; ct * o.rtiles < o.n; ++ct) {
+    const int64_t u0 = int64_t(ct) * o.rtiles, u1 = std::min<int64_t>(o.n, int64_t(ct + 1) * o.rtiles) - 1;
+    const int64_t b0 = ((u0 + 1) * o.chunks - 1) / o.n, b1 = ((u1 + 1) * o.chunks - 1) / o.n;
+    spb = std::max(spb, int(b1 - b0 + 1));
+  }
+  return spb;
+}
+static qtc::OrSpec or_spec(int64_t R, int64_t C, int kk, int num_sms) {
+  qtc::OrSpec o{};
+  o.on = 1;
+  o.kk = kk;
+  o.npad = int((kk + 15) / 16 * 16);
+  o.rtiles = int((R + 127) / 128);
+  o.n = o.rtiles * int((C + 127) / 128);
+  o.chunks = std::min(o.n, num_sms);
+  o.spb = or_slots_per_band(o);
+  return o;
+}
+OePatch quant_tc_or_patch(int64_t R, int64_t C, int kk, int num_sms, const float* part, unsigned* ticket, float* Dt,
+                          const int32_t* idx) {
+  const qtc::OrSpec o = or_spec(R, C, kk, num_sms);
+  OePatch p{Dt, idx, C, kk, 1};
+  p.part = part;
+  p.ticket = ticket;
+  p.spb = o.spb;
+  p.npad = o.npad;
+  p.or_n = o.n;
+  p.or_rtiles = o.rtiles;
+  p.or_chunks = o.chunks;
+  return p;
+}
+size_t quant_tc_or_part_bytes(int64_t R, int64_t C, int kk, int num_sms) {
+  if (kk <= 0 || kk > qtc::kOrMaxN || R <= 0 || C <= 0) return 0;
+  const qtc::OrSpec o = or_spec(R, C, kk, num_sms);
+  return size_t((C + 127) / 128) * size_t(o.spb) * size_t(o.npad) * 128 * 4;
+}
+
+template <bool kRow, bool kCol, bool kHad, bool kOr>
 static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int64_t bitmap_words, int num_sms, cudaStream_t st) {
-  const size_t smem = quant_tc_smem(masks, bitmap_words);
+  const size_t smem = quant_tc_smem(masks, bitmap_words, kOr);
+  if (smem > kSmemLimit) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> attr{0};
   cudaError_t ae = once_per_device(attr, [] {
-    return cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(quant_tc_smem_max()));
+    return cudaFuncSetAttribute(qtc::k_quant_tc<kRow, kCol, kHad, kOr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(quant_tc_smem_max(kOr)));
   });
   if (ae != cudaSuccess) return ae;
-  const unsigned grid = unsigned(J.ntiles < num_sms ? J.ntiles : num_sms);
-  return launch_k(qtc::k_quant_tc<kRow, kCol, kHad>, dim3(grid), dim3(qtc::kThreads), smem, st, 1, J);
+  const int tiles = J.ntiles + (kOr ? J.orr.n : 0);
+  const unsigned grid = unsigned(tiles < num_sms ? tiles : num_sms);
+  return launch_k(qtc::k_quant_tc<kRow, kCol, kHad, kOr>, dim3(grid), dim3(qtc::kThreads), smem, st, 1, J);
 }
 
 // Each job: T [R x C] bf16 (pitch ld). Row outputs (stored rows = R, K = C) and / or column
@@ -572,25 +736,47 @@ static bool gather_fused() {
   static const int v = knob("ADAHOP_GATHER_FUSED", 0);
   return v != 0;
 }
+// ADAHOP_OR_FUSED=2 (experiment builds): every dual launch runs the fused-product kernel variant
+// (single TMEM buffer, 3-stage ring) without a product, to separate its costs
+static bool or_variant_without_product() {
+  static const int v = knob("ADAHOP_OR_FUSED", 1);
+  return v == 2;
+}
 static bool gather_after_quant() {
   static const int v = knob("ADAHOP_GATHER_AFTER", 0);
   return v != 0;
 }
 
-cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms, cudaStream_t st, int* launches) {
+cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms, cudaStream_t st, int* launches,
+                                  bool* or_fused) {
+  if (or_fused) *or_fused = false;
   if (n <= 0) return cudaSuccess;
   if (n > qtc::kMaxJobs) return cudaErrorInvalidValue;
   // The OE slices come from a separate gather (copying them inside the quant pipeline stalls
   // it), launched before the quant pass (see gather_after_quant for the measured alternative).
   const bool after = gather_after_quant();
   const bool fused = gather_fused() && !after;
+  // The fused outlier product (at most one job; its slice must exist before the launch, so not
+  // with the in-kernel gathers) runs on the dual-orientation kernel; its job goes last.
+  int or_in = -1;
+  for (int i = 0; i < n; ++i)
+    if (jobs_in[i].or_slice) {
+      if (or_in >= 0) return cudaErrorInvalidValue;
+      or_in = i;
+    }
+  bool orr = or_in >= 0 && !after && !fused && jobs_in[or_in].q_row && jobs_in[or_in].q_col &&
+             !jobs_in[or_in].had_row && !jobs_in[or_in].had_col && jobs_in[or_in].or_kk > 0 &&
+             jobs_in[or_in].or_kk <= qtc::kOrMaxN && jobs_in[or_in].or_ticket &&
+             jobs_in[or_in].or_part_bytes >= quant_tc_or_part_bytes(jobs_in[or_in].R, jobs_in[or_in].C,
+                                                                    jobs_in[or_in].or_kk, num_sms);
   QuantTcJob jobs[qtc::kMaxJobs];
   int m = 0;
   for (int pass = 0; pass < (after ? 2 : 1); ++pass)
     for (int i = 0; i < n; ++i) {
       const bool colg = jobs_in[i].q_col && jobs_in[i].ncol_zero > 0 && jobs_in[i].slice_col;
-      if (!after || colg == (pass == 1)) jobs[m++] = jobs_in[i];
+      if (orr ? i != or_in : (!after || colg == (pass == 1))) jobs[m++] = jobs_in[i];
     }
+  if (orr) jobs[m++] = jobs_in[or_in];
   auto gathers = [&]() -> cudaError_t {
     for (int i = 0; i < n; ++i) {
       const QuantTcJob& q = jobs[i];
@@ -607,10 +793,6 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     }
     return cudaSuccess;
   };
-  if (!after && !fused) {
-    cudaError_t e = gathers();
-    if (e != cudaSuccess) return e;
-  }
   qtc::Jobs J;
   memset(&J, 0, sizeof(J));
   J.n = n;
@@ -639,7 +821,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     jj.R = q.R; jj.C = q.C;
     jj.ctiles = int((q.C + 127) / 128);
     jj.tile0 = tiles;
-    tiles += jj.ctiles * int((q.R + 127) / 128);
+    if (!(orr && i == n - 1)) tiles += jj.ctiles * int((q.R + 127) / 128);
     jj.kch_row = sf_kchunks(q.C);
     jj.kch_col = sf_kchunks(q.R);
     jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, fused ? q.slice_row : nullptr, q.had_row, 0};
@@ -657,15 +839,37 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     masks |= jj.orow.nzero > 0 || jj.ocol.nzero > 0;
   }
   J.ntiles = tiles;
+  if (orr) {
+    const QuantTcJob& q = jobs[n - 1];
+    J.orr = or_spec(q.R, q.C, q.or_kk, num_sms);
+    J.orr.part = q.or_part;
+    J.orr.ticket = q.or_ticket;
+    // the slice S [kk][R] (R contiguous): boxes of 64 rows of T (128 B) x npad slice rows, OOB -> 0
+    if (quant_tc_smem(masks, words, true) > kSmemLimit ||
+        !make_tmap_2d(&J.tor, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q.or_slice, uint64_t(q.R), uint64_t(q.or_kk),
+                      uint64_t(q.R) * 2, 64, uint32_t(J.orr.npad), CU_TENSOR_MAP_SWIZZLE_128B)) {
+      // does not fit: the caller runs the BF16 outlier GEMM; the job becomes a plain one again
+      orr = false;
+      J.orr = qtc::OrSpec{};
+      J.ntiles = tiles + J.j[n - 1].ctiles * int((q.R + 127) / 128);
+    }
+  }
+  if (!after && !fused) {
+    cudaError_t e = gathers();
+    if (e != cudaSuccess) return e;
+  }
   if (launches) ++*launches;
   cudaError_t e = cudaSuccess;
-  if (row && col) e = had ? launch_tc<true, true, true>(J, masks, words, num_sms, st)
-                          : launch_tc<true, true, false>(J, masks, words, num_sms, st);
-  else if (row) e = had ? launch_tc<true, false, true>(J, masks, words, num_sms, st)
-                        : launch_tc<true, false, false>(J, masks, words, num_sms, st);
-  else if (col) e = had ? launch_tc<false, true, true>(J, masks, words, num_sms, st)
-                        : launch_tc<false, true, false>(J, masks, words, num_sms, st);
+  if (orr || (row && col && !had && or_variant_without_product()))
+    e = launch_tc<true, true, false, true>(J, masks, words, num_sms, st);
+  else if (row && col) e = had ? launch_tc<true, true, true, false>(J, masks, words, num_sms, st)
+                               : launch_tc<true, true, false, false>(J, masks, words, num_sms, st);
+  else if (row) e = had ? launch_tc<true, false, true, false>(J, masks, words, num_sms, st)
+                        : launch_tc<true, false, false, false>(J, masks, words, num_sms, st);
+  else if (col) e = had ? launch_tc<false, true, true, false>(J, masks, words, num_sms, st)
+                        : launch_tc<false, true, false, false>(J, masks, words, num_sms, st);
   if (e != cudaSuccess) return e;
+  if (orr && or_fused) *or_fused = true;
   return after ? gathers() : cudaSuccess;
 }
 
@@ -675,7 +879,7 @@ cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64
                             uint8_t* sf_col, float* had_col, int num_sms, cudaStream_t st) {
   const QuantTcJob q{in, R, C, ld, row_zero, nrow_zero, slice_row, q_row, sf_row, had_row,
                      col_zero, ncol_zero, slice_col, q_col, sf_col, had_col};
-  return launch_quant_tc_multi(&q, 1, num_sms, st, nullptr);
+  return launch_quant_tc_multi(&q, 1, num_sms, st, nullptr, nullptr);
 }
 
 }  // namespace adahop

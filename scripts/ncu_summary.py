@@ -16,7 +16,7 @@ import sys
 from collections import OrderedDict
 
 # hot-path kernels of the layer step (calibration kernels excluded: bench.py times them after the step)
-OURS = re.compile(r"mxf4x2::|bf16g::|k_quant_tc|k_gemm_|k_foid|k_oe_|k_outlier|k_iht")
+OURS = re.compile(r"mxf4x2::|bf16g::|k_quant_tc|k_gemm_|k_foid|k_oe_|k_outlier|k_iht|k_or_fold")
 
 
 def short(name: str) -> str:

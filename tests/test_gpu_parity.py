@@ -466,8 +466,18 @@ def test_linear_layer_matches_paths_and_oracle(strats, shape):
     gx1 = ah.linear_dgrad(gd, wd, strats[1], p, out_dtype=torch.float32)
     gw1 = ah.linear_wgrad(gd, xd, strats[2], p, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    for a, b in ((y, y1), (gx, gx1), (gw, gw1)):
+    for a, b in ((y, y1), (gx, gx1)):
         np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+    # wgrad: the MXFP4 part is bitwise equal; with OE-Right the layer call accumulates the outlier
+    # product A B_out in G_Y's quant pass and the per-path call in a split-K BF16 GEMM, two fp32
+    # summation orders of the same product, so the extracted columns agree to rounding
+    a, b = gw.cpu().numpy(), gw1.cpu().numpy()
+    diff = a.view(np.uint32) != b.view(np.uint32)
+    if strats[2] == "OE_RIGHT_IHT":
+        assert len(np.unique(np.nonzero(diff)[1])) <= 16   # at most the k = 16 extracted columns
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    else:
+        assert not diff.any()
     for path, got, s in (("fwd", y, strats[0]), ("dgrad", gx, strats[1]), ("wgrad", gw, strats[2])):
         ref = O.linear(path, s, x=x, w=w, gy=gy, k=16)
         assert rel_fro(got.cpu().numpy(), ref) <= TOL_OUT, (path, s)
