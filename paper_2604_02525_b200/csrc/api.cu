@@ -175,7 +175,8 @@ int current_device() {
 
 // ADAHOP_OR_FUSED=0 (experiment builds) runs the wgrad OE-Right product as a BF16 GEMM instead
 bool or_fusion_enabled() {
-  static const bool on = knob("ADAHOP_OR_FUSED", 1) == 1;
+  static const int v = knob("ADAHOP_OR_FUSED", 1);
+  static const bool on = v == 1 || v == 3;
   return on;
 }
 

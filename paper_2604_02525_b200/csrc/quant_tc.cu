@@ -197,6 +197,7 @@ struct OrSpec {
   int spb;         // partial slots per band
   float* part;     // [ctiles][spb][npad][128] fp32
   unsigned* ticket;   // zeroed here; the MXFP4 GEMM's pre-fold counts its CTAs on it
+  int dry;            // experiment builds (ADAHOP_OR_FUSED=3): the OR tile order without the product
 };
 struct Jobs {
   CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs], tor;
@@ -209,27 +210,35 @@ struct TileRef {
   bool orr, first, last;   // an OR tile; first / last tile of its (band, CTA) segment
 };
 __device__ __forceinline__ int or_chunk_lo(const OrSpec& o, int b) { return int((int64_t(b) * o.n) / o.chunks); }
-// The i-th tile of this CTA; false past its last tile (the same sequence in every role).
-__device__ __forceinline__ bool tile_at(const Jobs& J, int i, TileRef& t) {
-  const int b = int(blockIdx.x), G = int(gridDim.x);
-  const int np = J.ntiles > b ? (J.ntiles - b + G - 1) / G : 0;
-  if (i < np) {
-    const int g = b + i * G;
-    const int nplain = J.n - (J.orr.on ? 1 : 0);
-    int jb = 0;
-    while (jb + 1 < nplain && g >= J.j[jb + 1].tile0) ++jb;
-    const int lt0 = g - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
-    t = TileRef{jb, lt0 / ctiles, lt0 % ctiles, false, false, false};
+// This CTA's tile sequence (the same in every role): plain tiles b, b + G, ... then its OR chunk.
+struct TileCursor {
+  int g, u, uend;   // next plain tile; next / end OR tile
+  int lo;           // first OR tile of the chunk
+  __device__ __forceinline__ explicit TileCursor(const Jobs& J) {
+    g = int(blockIdx.x);
+    u = uend = lo = 0;
+    if (J.orr.on && int(blockIdx.x) < J.orr.chunks) {
+      lo = u = or_chunk_lo(J.orr, int(blockIdx.x));
+      uend = or_chunk_lo(J.orr, int(blockIdx.x) + 1);
+    }
+  }
+  __device__ __forceinline__ bool next(const Jobs& J, TileRef& t) {
+    if (g < J.ntiles) {
+      const int nplain = J.n - (J.orr.on ? 1 : 0);
+      int jb = 0;
+      while (jb + 1 < nplain && g >= J.j[jb + 1].tile0) ++jb;
+      const int lt0 = g - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
+      t = TileRef{jb, lt0 / ctiles, lt0 % ctiles, false, false, false};
+      g += int(gridDim.x);
+      return true;
+    }
+    if (u >= uend) return false;
+    const int rt = u % J.orr.rtiles;
+    t = TileRef{J.n - 1, rt, u / J.orr.rtiles, true, u == lo || rt == 0, u + 1 == uend || rt == J.orr.rtiles - 1};
+    ++u;
     return true;
   }
-  if (!J.orr.on || b >= J.orr.chunks) return false;
-  const int lo = or_chunk_lo(J.orr, b), hi = or_chunk_lo(J.orr, b + 1);
-  const int u = lo + (i - np);
-  if (u >= hi) return false;
-  const int rt = u % J.orr.rtiles;
-  t = TileRef{J.n - 1, rt, u / J.orr.rtiles, true, u == lo || rt == 0, u + 1 == hi || rt == J.orr.rtiles - 1};
-  return true;
-}
+};
 // OR-chunk holding OR tile u: the largest b with lo(b) <= u
 __device__ __forceinline__ int or_chunk_of(const OrSpec& o, int u) {
   return int(((int64_t(u) + 1) * o.chunks - 1) / o.n);
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       mask_build(&masks[2 * jb + 1], mbits + J.j[jb].ocol.bits_off, J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
   }
   // the previous user of the ticket (an earlier GEMM) has completed: griddep_wait above
-  if (kOr && blockIdx.x == 0 && threadIdx.x == 0) *J.orr.ticket = 0u;
+  if (kOr && J.orr.on && blockIdx.x == 0 && threadIdx.x == 0) *J.orr.ticket = 0u;
   ptx::fence_proxy_async();  // H written by threads, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
@@ -320,11 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     int stage = 0;
     uint32_t phase = 0;
     TileRef t;
-    for (int i = 0; tile_at(J, i, t); ++i) {
+    TileCursor cur(J);
+    for (int i = 0; cur.next(J, t); ++i) {
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       QTC_T(0, i);
       uint8_t* dst = ring + stage * RG::kStage;
-      const bool o = kOr && t.orr;
+      const bool o = kOr && t.orr && !J.orr.dry;
       ptx::mbar_arrive_expect_tx(&full[stage], kTile + (o ? 2 * npad * 128 : 0));
       ptx::tma_load_2d(dst, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128), int32_t(t.rt * 128));
       ptx::tma_load_2d(dst + kBox, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128 + 64), int32_t(t.rt * 128));
@@ -343,14 +353,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     uint32_t phase = 0;
     int segs = 0;   // completed outlier-product segments
     TileRef t;
-    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+    TileCursor cur(J);
+    for (int lt = 0; cur.next(J, t); ++lt) {
       const uint32_t buf = kTBufs == 2 ? uint32_t(lt & 1) : 0u;
       const uint32_t use = kTBufs == 2 ? uint32_t(lt >> 1) : uint32_t(lt);
       ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
       QTC_T(1, lt);
       ptx::mbar_wait(&full[stage], phase);
       QTC_T(2, lt);
-      const bool o = kOr && t.orr;
+      const bool o = kOr && t.orr && !J.orr.dry;
       // a new segment reuses the product accumulator once the previous segment is flushed
       if (o && t.first && segs > 0) ptx::mbar_wait(orempty, uint32_t((segs - 1) & 1));
       ptx::tc_fence_after();
@@ -403,7 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     int stage = 0;
     uint32_t phase = 0;
     TileRef t;
-    for (int i = 0; tile_at(J, i, t); ++i) {
+    TileCursor cur(J);
+    for (int i = 0; cur.next(J, t); ++i) {
       const Job& jj = J.j[t.jb];
       const int rt = t.rt, ct = t.ct;
       ptx::mbar_wait(&full[stage], phase);
@@ -448,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     // One TMA store of the 128 x 64-byte code box and one 512-byte bulk copy of the scale chunk
     // per orientation and tile, so the epilogue warps never stall on global-store issue.
     TileRef t;
-    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+    TileCursor cur(J);
+    for (int lt = 0; cur.next(J, t); ++lt) {
       const Job jj = J.j[t.jb];   // by value: one param-space read per tile
       const int rt = t.rt, ct = t.ct;
       const uint32_t buf = uint32_t(lt & 1), use = uint32_t(lt >> 1);
@@ -497,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     const uint32_t sw = (row >> 1) & 3;        // 64B swizzle of the staging row
     int segs = 0;
     TileRef t;
-    for (int lt = 0; tile_at(J, lt, t); ++lt) {
+    TileCursor cur(J);
+    for (int lt = 0; cur.next(J, t); ++lt) {
       const Job jj = J.j[t.jb];   // by value: one param-space read per tile
       const int rt = t.rt, ct = t.ct;
       const Out& o = col_side ? jj.ocol : jj.orow;
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       ptx::fence_proxy_async();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&staged[sbuf]);
-      if (kOr && t.orr && t.last) {
+      if (kOr && t.orr && t.last && !J.orr.dry) {
         if (group == 0) {
           // flush the finished segment: P[c = 128 ct + row][j] -> its (band, CTA) partial slot
           ptx::mbar_wait(orfull, uint32_t(segs & 1));
@@ -587,7 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t0 = g_qtc_trace[0][0];
     TileRef t;
-    for (int i = 0; i < 64 && tile_at(J, i, t); ++i)
+    TileCursor cur(J);
+    for (int i = 0; i < 64 && cur.next(J, t); ++i)
       printf("qtc tile %2d: tma %7lld tempty %7lld full %7lld epi %7lld drained %7lld\n", i,
              g_qtc_trace[0][i] - t0, g_qtc_trace[1][i] - t0, g_qtc_trace[2][i] - t0, g_qtc_trace[3][i] - t0,
              g_qtc_trace[4][i] - t0);
@@ -844,6 +859,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     J.orr = or_spec(q.R, q.C, q.or_kk, num_sms);
     J.orr.part = q.or_part;
     J.orr.ticket = q.or_ticket;
+    J.orr.dry = knob("ADAHOP_OR_FUSED", 1) == 3 ? 1 : 0;
     // the slice S [kk][R] (R contiguous): boxes of 64 rows of T (128 B) x npad slice rows, OOB -> 0
     if (quant_tc_smem(masks, words, true) > kSmemLimit ||
         !make_tmap_2d(&J.tor, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q.or_slice, uint64_t(q.R), uint64_t(q.or_kk),
