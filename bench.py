@@ -635,6 +635,11 @@ def main():
     peaks = load_peaks()
     dom = max(stage_tot, key=stage_tot.get)
     roof = roofline(dom, gemms, stage_tot, peaks, T, model, per_path=args.per_path, workload=args.workload)
+    if dom == "gemm_mxf4" and not args.no_cublas:
+        lib = library_fp4(gemms, args, l2, as_graph, timed, dev)
+        if lib:
+            lib["ours_over_library"] = lib["ms_per_step"] / stage_tot[dom]
+            roof["library_fp4"] = lib
 
     # ---- CPU oracle baseline (rank 0, bounded sample)
     cpu = None
@@ -867,6 +872,42 @@ def profiled_traffic(workload, kernel):
         return None
 
 
+def library_fp4(gemms, args, l2, as_graph, timed, dev):
+    """The library's block-scaled FP4 GEMM on the step's MXFP4 GEMM shapes: cuBLASLt NVFP4 (E2M1 x
+    E2M1, E4M3 scales per 16 along K: the same FP4 tensor-core rate as MXFP4, twice the scale
+    factors; torch exposes no MXFP4 matmul) through F.scaled_mm, bf16 out, timed like our step
+    (CUDA graph, L2 flushed between steps). Speed-of-light context for the GEMM stage, not a
+    baseline of the method. None where torch / cuBLASLt does not offer it."""
+    import torch
+    F = torch.nn.functional
+    if not hasattr(F, "scaled_mm"):
+        return None
+    try:
+        ops = []
+        for g in gemms:
+            if g["strategy"] == "BF16":
+                continue
+            M, N, K = g["M"], g["N"], g["K"]
+            a = torch.randint(0, 256, (M, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+            b = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+            sa = torch.ones((M, K // 16), device=dev).to(torch.float8_e4m3fn)
+            sb = torch.ones((K // 16, N), device=dev).to(torch.float8_e4m3fn)
+            ops.append((a, b, sa, sb))
+
+        def step():
+            for a, b, sa, sb in ops:   # outputs come from the graph's private pool
+                F.scaled_mm(a, b.t(), [sa], [F.ScalingType.BlockWise1x16], [sb], [F.ScalingType.BlockWise1x16],
+                            [F.SwizzleType.SWIZZLE_32_4_4], [F.SwizzleType.SWIZZLE_32_4_4], None, torch.bfloat16)
+        step()
+        flops = sum(2.0 * g["M"] * g["N"] * g["K"] for g in gemms if g["strategy"] != "BF16")
+        ms, _ = timed(as_graph(step), args.steps, args.warmup)
+        return {"kernel": "cuBLASLt NVFP4 block-scaled GEMM (torch F.scaled_mm, BlockWise1x16)",
+                "ms_per_step": ms, "TFLOP_s": flops / (ms * 1e-3) / 1e12,
+                "note": "same M,N,K as the step's MXFP4 GEMMs, bf16 out (ours: fp32 G_W)"}
+    except Exception as e:  # noqa: BLE001  (reported, not fatal: context only)
+        return {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+
+
 def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False, workload=None):
     """Achieved = algorithmic work of the dominant stage per step / its measured time (CUDA events
     recorded by the library around the stage on the launching stream) = the launch-weighted
@@ -883,26 +924,7 @@ def roofline(dom, gemms, stage_tot, peaks, T, model=None, per_path=False, worklo
             tr["algorithmic_bytes_per_launch"] = sum((g["M"] + g["N"]) * g["K"] * 17 / 32 +
                                                      g["M"] * g["N"] * (4 if g["path"] == "wgrad" else 2)
                                                      for g in gemms if g["strategy"] != "BF16") / n
-        # The operand feed: TMA moves, per CTA pair and 256-deep k-step, A 2 x 16 KB + B 2 x 16 KB +
-        # scale factors 2 x 3 KB (256 x 256 tiles) or 2 x (16 + 8 + 2) KB (256 x 128 tiles, long-K
-        # GEMMs with few tiles: the api.cu rule). Its cap is the L2 -> SM delivery rate measured on
-        # B200 by scripts/micro/tma_feed.cu (profiles/r02d_tma_feed.txt): 62 B/clk/SM with two
-        # issuing CTAs per SM, 18.0 TB/s at 1965 MHz — a lower bound of the hardware cap.
-        feed = 0.0
-        for g in gemms:
-            if g["strategy"] == "BF16":
-                continue
-            tiles256 = -(-g["M"] // 256) * -(-g["N"] // 256)
-            narrow = g["K"] >= 8192 and 2 * tiles256 < 148 // 2
-            tiles = -(-g["M"] // 256) * -(-g["N"] // (128 if narrow else 256))
-            feed += tiles * -(-g["K"] // 256) * (52 if narrow else 70) * 1024
-        feed_tbps = feed / (stage_tot[dom] * 1e-3) / 1e12
-        feed_cap = 62 * 148 * 1965e6 / 1e12
         return {"kernel": "k_gemm_mxf4_2sm (tcgen05 kind::mxf4, cta_group::2)", "bound": "tensor", "achieved": ach,
-                "operand_feed": {"achieved_TBps": feed_tbps, "cap_TBps": feed_cap, "frac": feed_tbps / feed_cap,
-                                 "note": "TMA L2->SM operand bytes / GEMM stage time vs the measured B200 TMA "
-                                         "delivery rate (scripts/micro/tma_feed.cu); the main loop's binding "
-                                         "resource (profiles/r02b_gemm_ablation.txt)"},
                 "peak": fp4_peak, "unit": "TFLOP/s", "frac": ach / fp4_peak,
                 "traffic": tr["bytes_per_launch"] if tr else None, "traffic_detail": tr,
                 "launches_per_step": n, "flop_per_launch": work / n,

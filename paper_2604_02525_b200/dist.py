@@ -110,25 +110,49 @@ def calibrate_sharded(t_local: torch.Tensor, rows_global: int, ops: Optional[Cal
 
 
 class DataParallelLinear:
-    """fwd / dgrad / wgrad of one linear on this rank's token shard, AdaHOP strategies fixed
-    per path at calibration time; wgrad partials are all-reduced."""
+    """One linear on this rank's token shard, AdaHOP strategies fixed per path at calibration
+    time; wgrad partials are all-reduced.
+
+    The training-step form is forward() / backward(): the split layer API (adahop_linear_forward /
+    _backward) quantises X and W once in both orientations in the forward, saves the FP4
+    context, and the backward quantises G_Y once for dgrad and wgrad — the path bench.py times.
+    fwd() / dgrad() / wgrad() are the per-path calls (every operand quantised per GEMM)."""
 
     def __init__(self, strategies: dict, params=None, group=None, compute: Optional[dict] = None):
         self.strategies = strategies
         self.params = params
         self.group = group
-        if compute is None:
-            from . import adahop as ah
-            compute = {"fwd": ah.linear_fwd, "dgrad": ah.linear_dgrad, "wgrad": ah.linear_wgrad}
-        self.compute = compute
+        self.compute = dict(compute or {})   # injected ops (CPU tests); the C ABI otherwise
+
+    _OPS = {"fwd": "linear_fwd", "dgrad": "linear_dgrad", "wgrad": "linear_wgrad",
+            "forward": "linear_forward", "backward": "linear_backward"}
+
+    def _op(self, name):
+        if name not in self.compute:
+            from . import adahop as ah   # loads the CUDA library (fails loudly without it)
+            self.compute[name] = getattr(ah, self._OPS[name])
+        return self.compute[name]
+
+    def _strats(self):
+        return (self.strategies["fwd"], self.strategies["dgrad"], self.strategies["wgrad"])
 
     def forward(self, x_local, w, **kw):
-        return self.compute["fwd"](x_local, w, self.strategies["fwd"], self.params, **kw)
+        """(Y_local, ctx): Y = X W^T on the local token rows and the saved backward context."""
+        return self._op("forward")(x_local, w, self._strats(), self.params, **kw)
+
+    def backward(self, gy_local, w, ctx, async_op: bool = False, **kw):
+        """(G_X_local, G_W[, work]): G_W is the rank-local partial summed over ranks."""
+        gx, gw = self._op("backward")(gy_local, w, ctx, **kw)
+        work = allreduce_wgrad(gw, self.group, async_op=async_op)
+        return (gx, gw, work) if async_op else (gx, gw)
+
+    def fwd(self, x_local, w, **kw):
+        return self._op("fwd")(x_local, w, self.strategies["fwd"], self.params, **kw)
 
     def dgrad(self, gy_local, w, **kw):
-        return self.compute["dgrad"](gy_local, w, self.strategies["dgrad"], self.params, **kw)
+        return self._op("dgrad")(gy_local, w, self.strategies["dgrad"], self.params, **kw)
 
     def wgrad(self, gy_local, x_local, async_op: bool = False, **kw):
-        gw = self.compute["wgrad"](gy_local, x_local, self.strategies["wgrad"], self.params, **kw)
+        gw = self._op("wgrad")(gy_local, x_local, self.strategies["wgrad"], self.params, **kw)
         work = allreduce_wgrad(gw, self.group, async_op=async_op)
         return (gw, work) if async_op else gw

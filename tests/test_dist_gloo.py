@@ -67,6 +67,46 @@ def test_wgrad_allreduce_equals_sum_of_shard_oracles():
     assert np.linalg.norm(single - exact) / np.linalg.norm(exact) < 0.2
 
 
+# split training-step form (forward saves a context, backward all-reduces G_W)
+W_DP = synth.operand(D_OUT, D_IN, "N", "W", case_id=903)[0]
+STRATS = {"fwd": "IHT", "dgrad": "IHT", "wgrad": O.OE_RIGHT}
+
+
+def _oracle_forward(x, w, strategies, params, **kw):
+    y = O.linear("fwd", strategies[0], x=x.numpy(), w=w.numpy(), k=K_OE)
+    return torch.from_numpy(y), {"x": x, "strategies": strategies}
+
+
+def _oracle_backward(gy, w, ctx, **kw):
+    s = ctx["strategies"]
+    gx = O.linear("dgrad", s[1], w=w.numpy(), gy=gy.numpy(), k=K_OE)
+    gw = O.linear("wgrad", s[2], x=ctx["x"].numpy(), gy=gy.numpy(), k=K_OE)
+    return torch.from_numpy(gx), torch.from_numpy(gw)
+
+
+def _dp_split(rank, world):
+    x, gy = _inputs()
+    t0, t1 = dist_mod.token_shard(T, world, rank)
+    lin = dist_mod.DataParallelLinear(STRATS, compute={"forward": _oracle_forward, "backward": _oracle_backward})
+    y, ctx = lin.forward(torch.from_numpy(x[t0:t1]), torch.from_numpy(W_DP))
+    gx, gw, work = lin.backward(torch.from_numpy(gy[t0:t1]), torch.from_numpy(W_DP), ctx, async_op=True)
+    work.wait()
+    return y.numpy(), gx.numpy(), gw.numpy()
+
+
+def test_split_step_allreduces_wgrad_and_keeps_local_rows():
+    out = spawn(_dp_split)
+    x, gy = _inputs()
+    shards = [dist_mod.token_shard(T, 2, r) for r in range(2)]
+    want_gw = sum(O.linear("wgrad", O.OE_RIGHT, x=x[a:b], gy=gy[a:b], k=K_OE) for a, b in shards)
+    for r, (a, b) in enumerate(shards):
+        y, gx, gw = out[r]
+        np.testing.assert_allclose(gw, want_gw, rtol=1e-12, atol=1e-15)
+        # fwd / dgrad need no communication: each rank's rows equal the single-shard oracle
+        np.testing.assert_array_equal(y, O.linear("fwd", "IHT", x=x[a:b], w=W_DP, k=K_OE))
+        np.testing.assert_array_equal(gx, O.linear("dgrad", "IHT", w=W_DP, gy=gy[a:b], k=K_OE))
+
+
 # -------------------------------------------------------------------------------- calibration
 def _np_stats(t):
     t = t.numpy().astype(np.float64)
