@@ -638,7 +638,6 @@ def main():
     if dom == "gemm_mxf4" and not args.no_cublas:
         lib = library_fp4(gemms, args, l2, as_graph, timed, dev)
         if lib:
-            lib["ours_over_library"] = lib["ms_per_step"] / stage_tot[dom]
             roof["library_fp4"] = lib
 
     # ---- CPU oracle baseline (rank 0, bounded sample)
@@ -873,37 +872,52 @@ def profiled_traffic(workload, kernel):
 
 
 def library_fp4(gemms, args, l2, as_graph, timed, dev):
-    """The library's block-scaled FP4 GEMM on the step's MXFP4 GEMM shapes: cuBLASLt NVFP4 (E2M1 x
-    E2M1, E4M3 scales per 16 along K: the same FP4 tensor-core rate as MXFP4, twice the scale
-    factors; torch exposes no MXFP4 matmul) through F.scaled_mm, bf16 out, timed like our step
-    (CUDA graph, L2 flushed between steps). Speed-of-light context for the GEMM stage, not a
-    baseline of the method. None where torch / cuBLASLt does not offer it."""
+    """The library's block-scaled FP4 GEMM next to ours on the step's MXFP4 GEMM shapes: cuBLASLt
+    NVFP4 (E2M1 x E2M1, E4M3 scales per 16 along K — the same FP4 tensor-core rate as MXFP4, twice
+    the scale factors; torch exposes no MXFP4 matmul) through F.scaled_mm, and k_gemm_mxf4_2sm alone
+    (adahop_debug_gemm_mxf4_tcsf: one launch per GEMM, scales already in the tcgen05 layout), both
+    with the step's output dtypes (bf16 Y / G_X, fp32 G_W), both timed like the step (CUDA graph,
+    L2 flushed between steps). Speed-of-light context for the GEMM stage, not a baseline of the
+    method. None where torch / cuBLASLt does not offer it."""
     import torch
+    import paper_2604_02525_b200 as ah
     F = torch.nn.functional
     if not hasattr(F, "scaled_mm"):
         return None
     try:
-        ops = []
+        lib_ops, our_ops = [], []
         for g in gemms:
             if g["strategy"] == "BF16":
                 continue
             M, N, K = g["M"], g["N"], g["K"]
-            a = torch.randint(0, 256, (M, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
-            b = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+            odt = torch.float32 if g["path"] == "wgrad" else torch.bfloat16
+            ca = torch.randint(0, 256, (M, K // 2), dtype=torch.uint8, device=dev)
+            cb = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device=dev)
             sa = torch.ones((M, K // 16), device=dev).to(torch.float8_e4m3fn)
             sb = torch.ones((K // 16, N), device=dev).to(torch.float8_e4m3fn)
-            ops.append((a, b, sa, sb))
+            lib_ops.append((ca.view(torch.float4_e2m1fn_x2), cb.view(torch.float4_e2m1fn_x2), sa, sb, odt))
+            ea = torch.full((ah.debug_sf_bytes(M, K),), 127, dtype=torch.uint8, device=dev)
+            eb = torch.full((ah.debug_sf_bytes(N, K),), 127, dtype=torch.uint8, device=dev)
+            our_ops.append((ca, ea, cb, eb, torch.empty((M, N), dtype=odt, device=dev)))
 
-        def step():
-            for a, b, sa, sb in ops:   # outputs come from the graph's private pool
+        def step_lib():
+            for a, b, sa, sb, odt in lib_ops:   # outputs come from the graph's private pool
                 F.scaled_mm(a, b.t(), [sa], [F.ScalingType.BlockWise1x16], [sb], [F.ScalingType.BlockWise1x16],
-                            [F.SwizzleType.SWIZZLE_32_4_4], [F.SwizzleType.SWIZZLE_32_4_4], None, torch.bfloat16)
-        step()
+                            [F.SwizzleType.SWIZZLE_32_4_4], [F.SwizzleType.SWIZZLE_32_4_4], None, odt)
+
+        def step_ours():
+            for ca, ea, cb, eb, out in our_ops:
+                ah.debug_gemm_mxf4_tcsf(ca, ea, cb, eb, out)
+        step_lib()
+        step_ours()
         flops = sum(2.0 * g["M"] * g["N"] * g["K"] for g in gemms if g["strategy"] != "BF16")
-        ms, _ = timed(as_graph(step), args.steps, args.warmup)
+        ms_lib, _ = timed(as_graph(step_lib), args.steps, args.warmup)
+        ms_ours, _ = timed(as_graph(step_ours), args.steps, args.warmup)
         return {"kernel": "cuBLASLt NVFP4 block-scaled GEMM (torch F.scaled_mm, BlockWise1x16)",
-                "ms_per_step": ms, "TFLOP_s": flops / (ms * 1e-3) / 1e12,
-                "note": "same M,N,K as the step's MXFP4 GEMMs, bf16 out (ours: fp32 G_W)"}
+                "ms_per_step": ms_lib, "TFLOP_s": flops / (ms_lib * 1e-3) / 1e12,
+                "ours_gemm_only_ms_per_step": ms_ours, "ours_gemm_only_TFLOP_s": flops / (ms_ours * 1e-3) / 1e12,
+                "ours_over_library": ms_lib / ms_ours,
+                "note": "the step's MXFP4 GEMM shapes and output dtypes; ours = k_gemm_mxf4_2sm alone (no outlier patch)"}
     except Exception as e:  # noqa: BLE001  (reported, not fatal: context only)
         return {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
 

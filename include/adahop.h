@@ -207,7 +207,12 @@ adahop_status_t adahop_linear_wgrad(const void* GY, const void* X, void* GW, ada
  * wgrad A) — the quantised copies the paper keeps for backward. Requires T, d_in,
  * d_out multiples of 32. Outputs Y [T x d_out] and G_X [T x d_in] contiguous in out_dt,
  * G_W [d_out x d_in] contiguous in gw_dt (fp32 for the data-parallel all-reduce).
- * G_W is this rank's partial under token sharding (the caller all-reduces it). */
+ * G_W is this rank's partial under token sharding (the caller all-reduces it).
+ * With a wgrad OE-Right strategy (s[2], eq:oe_right P:280) and oe_k <= 64 the outlier product
+ * A B_out = G_Y^T X[:, S] is accumulated inside G_Y's quantisation pass (transform,
+ * quantisation and the outlier path in one kernel) instead of a separate BF16 GEMM; its fp32
+ * partials are summed in a fixed order, so results are deterministic (run to run and graph vs
+ * eager) and equal to the BF16-GEMM form to fp32 rounding of the outlier columns. */
 size_t adahop_layer_workspace_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
                                     const adahop_params_t* p);
 adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY, void* Y, void* GX, void* GW,
@@ -293,6 +298,14 @@ adahop_status_t adahop_debug_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_
                                        adahop_stream_t stream);
 size_t adahop_debug_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
+/* The same GEMM kernel alone (one launch, no scale conversion): a_sf / b_sf are already in the
+ * tcgen05 block-scaled layout the quantiser writes (adahop_debug_sf_bytes(rows, K) bytes each,
+ * see DESIGN.md §5). Used to time the GEMM kernel by itself (bench.py's library comparison). */
+size_t adahop_debug_sf_bytes(int64_t rows, int64_t K);
+adahop_status_t adahop_debug_gemm_mxf4_tcsf(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes,
+                                            const uint8_t* b_sf, void* C, adahop_dtype_t out_dt, int64_t ldc,
+                                            int64_t M, int64_t N, int64_t K, adahop_stream_t stream);
+
 /* E2M1 element conversion used by the quantiser (hardware cvt.rn.satfinite.e2m1x2) and
  * its software statement (nearest of {0,.5,1,1.5,2,3,4,6}, ties to even mantissa,
  * saturating, sign = signbit): one code per input (device arrays of n). */
@@ -311,8 +324,9 @@ int32_t adahop_last_launch_count(void);
 
 /* Optional stage timing (tab:latency breakdown): `events` is a host array of 5
  * cudaEvent_t (or NULL to disable) used by the following hot-path calls on this thread:
- * [0] start, [1] after FOID, [2] after IHT+quant of both operands (with the OE-slice gathers),
- * [3] after the BF16 outlier GEMM + split-K fold, [4] after the MXFP4 GEMM whose epilogue writes
+ * [0] start, [1] after FOID, [2] after IHT+quant of both operands (with the OE-slice gathers and,
+ * in the layer / backward calls, the fused wgrad OE-Right outlier product), [3] after the
+ * remaining BF16 outlier GEMMs + split-K folds, [4] after the MXFP4 GEMMs, whose epilogues write
  * the outlier entries (the fused scatter) — or after the Lv2 BF16 GEMM. */
 void adahop_set_stage_events(void* events);
 

@@ -67,6 +67,8 @@ SIGNATURES = {
     "adahop_debug_foid": (I32, [P, I32, I64, I64, I64, I32, I32, I32, P, P, P, SZ, P]),
     "adahop_debug_gemm_mxf4": (I32, [P, P, P, P, P, I32, I64, I64, I64, I64, P, SZ, P]),
     "adahop_debug_gemm_workspace_bytes": (SZ, [I64, I64, I64]),
+    "adahop_debug_sf_bytes": (SZ, [I64, I64]),
+    "adahop_debug_gemm_mxf4_tcsf": (I32, [P, P, P, P, P, I32, I64, I64, I64, I64, P]),
     "adahop_debug_e2m1": (I32, [P, I64, P, P, P]),
     "adahop_debug_e2m1_exhaustive": (I32, [C.c_uint64, C.c_uint64, P, P, P]),
     "adahop_last_launch_count": (I32, []),

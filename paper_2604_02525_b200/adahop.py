@@ -341,6 +341,23 @@ def debug_gemm_mxf4(a_codes, a_scales, b_codes, b_scales, out_dtype=torch.float3
     return out
 
 
+def debug_sf_bytes(rows: int, K: int) -> int:
+    return int(lib.adahop_debug_sf_bytes(rows, K))
+
+
+def debug_gemm_mxf4_tcsf(a_codes, a_sf, b_codes, b_sf, out):
+    """The MXFP4 GEMM kernel alone: scales already in the tcgen05 layout (debug_sf_bytes each)."""
+    M, Kh = a_codes.shape
+    N = b_codes.shape[0]
+    for t in (a_codes, b_codes, a_sf, b_sf, out):
+        assert t.is_cuda and t.is_contiguous()
+    assert out.shape == (M, N) and a_sf.numel() >= debug_sf_bytes(M, 2 * Kh) and b_sf.numel() >= debug_sf_bytes(N, 2 * Kh)
+    check("adahop_debug_gemm_mxf4_tcsf",
+          lib.adahop_debug_gemm_mxf4_tcsf(_ptr(a_codes), _ptr(a_sf), _ptr(b_codes), _ptr(b_sf), _ptr(out), _dt(out),
+                                          out.stride(0), M, N, 2 * Kh, _stream()))
+    return out
+
+
 def debug_e2m1(v: torch.Tensor):
     """(hardware codes, software-rule codes) of fp32 values through the quantiser's conversion."""
     v = v.contiguous().float()

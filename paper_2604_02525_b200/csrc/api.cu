@@ -1072,6 +1072,28 @@ adahop_status_t adahop_debug_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_
   return ADAHOP_OK;
 }
 
+size_t adahop_debug_sf_bytes(int64_t rows, int64_t K) {
+  if (rows <= 0 || K <= 0 || K % 32) return 0;
+  return size_t(sf_bytes(rows, K));
+}
+
+adahop_status_t adahop_debug_gemm_mxf4_tcsf(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes,
+                                            const uint8_t* b_sf, void* C, adahop_dtype_t out_dt, int64_t ldc,
+                                            int64_t M, int64_t N, int64_t K, adahop_stream_t stream) {
+  if (!a_codes || !a_sf || !b_codes || !b_sf || !C) return ADAHOP_E_INVALID_ARG;
+  if (M <= 0 || N <= 0 || K <= 0 || K % 32) return ADAHOP_E_SHAPE;
+  if (ldc < N || !aligned16(a_codes) || !aligned16(b_codes) || !aligned16(C) || !aligned16(a_sf) || !aligned16(b_sf))
+    return ADAHOP_E_INVALID_ARG;
+  DevInfo dev;
+  adahop_status_t st = check_device(&dev);
+  if (st != ADAHOP_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  Mxf4GemmArgs ma{a_codes, a_sf, b_codes, b_sf, C, out_dt == ADAHOP_DT_F32, ldc, M, N, K};
+  ADAHOP_LAUNCH(run_gemm_mxf4(ma, dev.sms, cs));
+  g_launches = 1;
+  return ADAHOP_OK;
+}
+
 adahop_status_t adahop_debug_e2m1(const float* v, int64_t n, uint8_t* codes_hw, uint8_t* codes_sw,
                                   adahop_stream_t stream) {
   if (!v || !codes_hw || !codes_sw || n < 0) return ADAHOP_E_INVALID_ARG;

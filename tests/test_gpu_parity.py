@@ -481,3 +481,21 @@ def test_linear_layer_matches_paths_and_oracle(strats, shape):
     for path, got, s in (("fwd", y, strats[0]), ("dgrad", gx, strats[1]), ("wgrad", gw, strats[2])):
         ref = O.linear(path, s, x=x, w=w, gy=gy, k=16)
         assert rel_fro(got.cpu().numpy(), ref) <= TOL_OUT, (path, s)
+
+
+def test_gemm_kernel_alone_matches_debug_gemm():
+    # adahop_debug_gemm_mxf4_tcsf (the kernel alone, scales already in the tcgen05 layout) equals the
+    # canonical-layout debug GEMM when every scale byte is the same (layout-independent scales)
+    M, N, K = 384, 640, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randint(0, 256, (M, K // 2), dtype=torch.uint8, device="cuda", generator=g)
+    b = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device="cuda", generator=g)
+    for e in (120, 127, 131):
+        sa = torch.full((M, K // 32), e, dtype=torch.uint8, device="cuda")
+        sb = torch.full((N, K // 32), e, dtype=torch.uint8, device="cuda")
+        ref = ah.debug_gemm_mxf4(a, sa, b, sb, out_dtype=torch.float32)
+        ea = torch.full((ah.debug_sf_bytes(M, K),), e, dtype=torch.uint8, device="cuda")
+        eb = torch.full((ah.debug_sf_bytes(N, K),), e, dtype=torch.uint8, device="cuda")
+        got = ah.debug_gemm_mxf4_tcsf(a, ea, b, eb, torch.empty((M, N), dtype=torch.float32, device="cuda"))
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)
