@@ -27,7 +27,7 @@ __all__ = [
     "debug_foid", "debug_gemm_mxf4", "debug_e2m1", "debug_e2m1_exhaustive", "last_launch_count",
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
     "calibrate_workspace_bytes", "classify_sums", "LinearContext", "linear_forward", "linear_backward",
-    "split_workspace_bytes", "linear_ctx_bytes", "layer_strategies",
+    "split_workspace_bytes", "linear_ctx_bytes", "layer_strategies", "debug_sf_bytes", "debug_gemm_mxf4_tcsf",
 ]
 
 

@@ -1211,14 +1211,25 @@ cudaError_t launch_foid_batch(const FoidJob* jobs, int n, bool in_f32, cudaStrea
     B.kb_off[i + 1] = B.kb_off[i] + int((J.R + 127) / 128);
     B.sb_off[i + 1] = B.sb_off[i] + int((J.R + B.rows_per_block - 1) / B.rows_per_block);
   }
-  if (in_f32) k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
-  else k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
+  // ADAHOP_FOID_PDL (experiment builds): 1 = the keys launch with programmatic dependent launch,
+  // 2 = both launches; default 0 (early-resident select CTAs measured slower in round 1)
+  static const int pdl = knob("ADAHOP_FOID_PDL", 0);
+  if (pdl >= 1) {
+    cudaError_t e = in_f32 ? launch_k(k_foid_keys_batch<float>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B)
+                           : launch_k(k_foid_keys_batch<__nv_bfloat16>, dim3(B.kb_off[n]), dim3(128), 0, st, 1, B);
+    if (e != cudaSuccess) return e;
+  } else if (in_f32) {
+    k_foid_keys_batch<float><<<B.kb_off[n], 128, 0, st>>>(B);
+  } else {
+    k_foid_keys_batch<__nv_bfloat16><<<B.kb_off[n], 128, 0, st>>>(B);
+  }
   static std::atomic<uint64_t> attr{0};
   cudaError_t ae = once_per_device(attr, [] {
     return cudaFuncSetAttribute(k_foid_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTopkMaxCand * 12));
   });
   if (ae != cudaSuccess) return ae;
-  // (the FOID kernels are launched without PDL: early-resident select CTAs measured slower)
+  if (pdl >= 2)
+    return launch_k(k_foid_select, dim3(B.sb_off[n]), dim3(kTopkThreads), size_t(kTopkMaxCand) * 12, st, 1, B);
   k_foid_select<<<B.sb_off[n], kTopkThreads, size_t(kTopkMaxCand) * 12, st>>>(B);
   return cudaGetLastError();
 }
