@@ -31,6 +31,13 @@
 #define QTC_ABLATE 0
 #endif
 
+// The tile's two TMA boxes are issued from two lanes of the producer warp: one issuing thread caps
+// a CTA's L2/HBM -> SM delivery near 27 B/clk, two lanes reach 34 (profiles/r02aa_tma_lanes.txt);
+// the layer step is ~1 % faster. QTC_PROD_LANES=1 restores the single issuing thread.
+#ifndef QTC_PROD_LANES
+#define QTC_PROD_LANES 2
+#endif
+
 // Experiment knob: QTC_TRACE=1 records per-tile timestamps of CTA 0 and prints them.
 #ifndef QTC_TRACE
 #define QTC_TRACE 0
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   const uint32_t tmem_base = *tmem_slot;
   const int npad = kOr ? J.orr.npad : 0;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane < uint32_t(QTC_PROD_LANES)) {
     // ------------------------------------------------------------ TMA producer
     int stage = 0;
     uint32_t phase = 0;
@@ -335,10 +342,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       QTC_T(0, i);
       uint8_t* dst = ring + stage * RG::kStage;
       const bool o = kOr && t.orr && !J.orr.dry;
-      ptx::mbar_arrive_expect_tx(&full[stage], kTile + (o ? 2 * npad * 128 : 0));
-      ptx::tma_load_2d(dst, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128), int32_t(t.rt * 128));
-      ptx::tma_load_2d(dst + kBox, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128 + 64), int32_t(t.rt * 128));
-      if (o) {
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&full[stage], kTile + (o ? 2 * npad * 128 : 0));
+      if (QTC_PROD_LANES == 1 || lane == 0)
+        ptx::tma_load_2d(dst, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128), int32_t(t.rt * 128));
+      if (QTC_PROD_LANES == 1 || lane == 1)
+        ptx::tma_load_2d(dst + kBox, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128 + 64), int32_t(t.rt * 128));
+      if (o && lane == 0) {
         // the slice rows S[0, npad) x tile rows [128 rt, +128) as two 64-row K boxes (rows >= kk: zeros)
         ptx::tma_load_2d(dst + kTile, &J.tor, &full[stage], int32_t(t.rt * 128), 0);
         ptx::tma_load_2d(dst + kTile + npad * 128, &J.tor, &full[stage], int32_t(t.rt * 128 + 64), 0);

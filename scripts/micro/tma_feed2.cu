@@ -17,7 +17,7 @@ __device__ __forceinline__ void wait_parity(uint32_t bar, uint32_t ph) {
 }
 
 struct P {
-  int stages, boxes, rows_per_box, nprod, iters, rows_total, pair;
+  int stages, boxes, rows_per_box, nprod, iters, rows_total, pair, lanes;   // lanes: issuing lanes of each producer warp
 };
 
 // nprod producer warps (lane 0 of warps 0..nprod-1), each owning `stages` stages of `boxes`
@@ -43,7 +43,7 @@ __global__ void k_feed(const __grid_constant__ CUtensorMap tm, P p, unsigned lon
   if (kPair) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   else __syncthreads();
   const unsigned long long t0 = clock64();
-  if (warp < p.nprod && lane == 0) {
+  if (warp < p.nprod && lane < p.lanes) {
     const uint32_t box_bytes = uint32_t(p.rows_per_box) * 128u;
     const uint32_t stage_bytes = uint32_t(p.boxes) * box_bytes;
     const int gid = kPair ? int(blockIdx.x / 2) : int(blockIdx.x);
@@ -72,10 +72,10 @@ __global__ void k_feed(const __grid_constant__ CUtensorMap tm, P p, unsigned lon
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(bar_local), "r"(0));
       }
       // the leader arms its own barrier for both CTAs' bytes (as the 2-SM GEMM does)
-      if (rank == 0)
+      if (rank == 0 && lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_local),
                      "r"(stage_bytes * (kPair ? 2u : 1u)) : "memory");
-      for (int b = 0; b < p.boxes; ++b) {
+      for (int b = lane; b < p.boxes; b += p.lanes) {
         const long long unit = ((long long)i * ng + gid) * p.nprod * p.boxes * 2 + (warp * p.boxes + b) * 2 + rank;
         const int row = int(unit * p.rows_per_box % p.rows_total);
         const uint32_t dst = su32(base + size_t(bi * p.boxes + b) * box_bytes);
@@ -123,7 +123,7 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-  struct C { const char* what; int ctas_per_sm, stages, boxes, rows_per_box, nprod, rows_total, pair; };
+  struct C { const char* what; int ctas_per_sm, stages, boxes, rows_per_box, nprod, rows_total, pair, lanes = 1; };
   const C cfgs[] = {
       {"baseline 1 CTA 1 prod 4x2 16KB", 1, 4, 2, 128, 1, rows, 0},
       {"1 CTA 1 prod 12x1 16KB", 1, 12, 1, 128, 1, rows, 0},
@@ -137,6 +137,8 @@ int main() {
       {"1 CTA 1 prod 4x2 16KB, 2 MB footprint", 1, 4, 2, 128, 1, 1 << 14, 0},
       {"1 CTA 2 prod 3x2 16KB, 2 MB footprint", 1, 3, 2, 128, 2, 1 << 14, 0},
       {"1 CTA 1 prod 6x2 16KB", 1, 6, 2, 128, 1, rows, 0},
+      {"1 CTA 1 prod warp, 2 issuing lanes, 4x2 16KB", 1, 4, 2, 128, 1, rows, 0, 2},
+      {"1 CTA 1 prod warp, 4 issuing lanes, 3x4 16KB", 1, 3, 4, 128, 1, rows, 0, 4},
       {"1 CTA 3 prod warps 2x2 16KB each", 1, 2, 2, 128, 3, rows, 0},
       {"1 CTA 6 prod warps 2x1 16KB each", 1, 2, 1, 128, 6, rows, 0},
       {"1 CTA 8 prod warps 1x1 16KB each", 1, 1, 1, 128, 8, rows, 0},
@@ -149,7 +151,7 @@ int main() {
   for (const C& c : cfgs) {
     P p;
     p.stages = c.stages; p.boxes = c.boxes; p.rows_per_box = c.rows_per_box; p.nprod = c.nprod;
-    p.iters = 3000; p.rows_total = c.rows_total; p.pair = c.pair;
+    p.iters = 3000; p.rows_total = c.rows_total; p.pair = c.pair; p.lanes = c.lanes;
     const int k = c.rows_per_box == 64 ? 0 : c.rows_per_box == 128 ? 1 : 2;
     const size_t smem = size_t(c.nprod) * c.stages * c.boxes * c.rows_per_box * 128 + 1024;
     auto kern = c.pair ? k_feed<true> : k_feed<false>;
