@@ -175,8 +175,16 @@ __device__ __forceinline__ void idx_range(const int32_t* __restrict__ idx, int k
   j1 = below + inside;
 }
 
+// Byte offset of (row, byte) in a warp's 32 x 128-byte stage: padded rows (LSU flush) or the
+// 128B-swizzled box a TMA store reads (16-byte chunk j of row r at chunk j ^ (r % 8)).
+template <bool kSw128>
+__device__ __forceinline__ int epi_stage_off(int row, int byte) {
+  return kSw128 ? row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15)) : row * kEpiPitch + byte;
+}
+
 // Patch the staged 32-row block (rows m0 .. m0+31, columns n0 .. n0+ncols-1) of C in the warp's
 // smem stage; call between staging and flushing (whole warp).
+template <bool kSw128 = false>
 __device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& op, int64_t m0, int64_t n0,
                                                    int ncols, int elt, int64_t M, int64_t N) {
   if (op.mode == 0) return;
@@ -192,7 +200,7 @@ __device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& 
       for (int j = j0; j < j1; ++j) {
         const int cl = int(__ldg(op.idx + j) - n0);
         const float v = oe_patch_value(op, j, m);
-        uint8_t* dst = stg + lane * kEpiPitch + cl * elt;
+        uint8_t* dst = stg + epi_stage_off<kSw128>(lane, cl * elt);
         if (elt == 4) *reinterpret_cast<float*>(dst) = v;
         else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
       }
@@ -203,13 +211,22 @@ __device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& 
         const int64_t n = n0 + c;
         if (n >= N) continue;
         const float v = __ldg(op.Dt + int64_t(j) * op.Mb + n);
-        uint8_t* dst = stg + rl * kEpiPitch + c * elt;
+        uint8_t* dst = stg + epi_stage_off<kSw128>(rl, c * elt);
         if (elt == 4) *reinterpret_cast<float*>(dst) = v;
         else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
       }
     }
   }
   __syncwarp();
+}
+
+// this lane's 128-byte row segment into a 128B-swizzled 32 x 128-byte stage (a TMA store box)
+__device__ __forceinline__ void epi_stage_sw128(uint8_t* stg, const uint32_t (&w)[32]) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* srow = stg + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<uint4*>(srow + ((j ^ (lane & 7)) << 4)) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
 __device__ __forceinline__ void epi_stage_only128(uint8_t* stg, const uint32_t (&w)[32]) {

@@ -94,6 +94,7 @@ template <int BN, int BUFS, int PM, int PN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
+                    const __grid_constant__ CUtensorMap tm_c, int tma_c,
                     void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe) {
   using G = Cfg<BN, BUFS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue (8 warps per CTA)
     const uint32_t q = warp & 3;            // TMEM lane quadrant
     const uint32_t half = (warp - 4) >> 2;  // column half of the tile
-    uint8_t* stg = epi_smem + (warp - 4) * G::kEpiBufs * kEpiStageBytes;
+    // TMA stores: a 4 KB 128B-swizzled box per warp (1024-aligned); else the padded LSU stage
+    uint8_t* stg = epi_smem + (warp - 4) * (tma_c ? 4096 : G::kEpiBufs * kEpiStageBytes);
     const int elt = out_f32 ? 4 : 2;
     const int cols_per_grp = 128 / elt;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
@@ -337,7 +339,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
 #pragma unroll 1
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < 2 && tma_c; ++g) {
+          // the previous TMA store has read the stage; stage, patch, then one bulk tensor store
+          if (lane == 0) ptx::bulk_wait_group_read<0>();
+          __syncwarp();
+          epi_stage_sw128(stg, g == 0 ? w0 : w1);
+          __syncwarp();
+          const int64_t n0 = nb * BN + half * (BN / 2) + g * 64;
+          epi_patch_outliers<true>(stg, oe, m0, n0, 64, 2, M, N);
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && rows_valid > 0 && n0 < N && !(GEMM_ABLATE & 8)) {
+            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::bulk_commit_group();
+          }
+        }
+#pragma unroll 1
+        for (int g = 0; g < 2 && !tma_c; ++g) {
           epi_stage_row128(stg, g == 0 ? w0 : w1);
           __syncwarp();
           const int64_t n0 = nb * BN + half * (BN / 2) + g * 64;
@@ -388,7 +406,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t nrem = N - n0;
         const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
-        if (rows_valid > 0 && bytes_valid > 0) {
+        if (rows_valid > 0 && bytes_valid > 0 && tma_c) {
+          if (lane == 0) ptx::bulk_wait_group_read<0>();
+          __syncwarp();
+          epi_stage_sw128(stg, w);
+          __syncwarp();
+          epi_patch_outliers<true>(stg, oe, m0, n0, cols_per_grp, elt, M, N);
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::bulk_commit_group();
+          }
+          __syncwarp();
+        } else if (rows_valid > 0 && bytes_valid > 0) {
           epi_stage_only128(stg, w);
           epi_patch_outliers(stg, oe, m0, n0, cols_per_grp, elt, M, N);
           epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid, bytes_valid, elt,
@@ -397,6 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (tma_c && lane == 0) ptx::bulk_wait_group<0>();   // this warp's stores are complete
+    __syncwarp();
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -415,6 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace mxf4x2
+
+// ADAHOP_GEMM_TMA_STORE=0 (experiment builds): the epilogue's LSU stores instead of TMA stores
+static bool tma_store_enabled() {
+  static const int v = knob("ADAHOP_GEMM_TMA_STORE", 1);
+  return v != 0;
+}
 
 template <int BN, int BUFS, int PM, int PN>
 static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st) {
@@ -436,6 +475,14 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   if (!make_tmap_2d(&tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
                     uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
+  // C by TMA stores (128B-swizzled 32-row boxes) when its rows are 16-byte aligned; else LSU stores
+  CUtensorMap tmc;
+  const int elt = a.out_f32 ? 4 : 2;
+  int tma_c = tma_store_enabled() && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ((a.ldc * elt) % 16) == 0 &&
+              make_tmap_2d(&tmc, a.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.C,
+                           uint64_t(a.N), uint64_t(a.M), uint64_t(a.ldc) * elt, uint32_t(128 / elt), 32,
+                           CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  if (!tma_c) memset(&tmc, 0, sizeof(tmc));
   // resident clusters of this shape (GPC packing decides it for clusters of 4 and 8), per device
   static std::atomic<uint64_t> attr{0};
   static PerDeviceInt cached;
@@ -468,7 +515,7 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   const int64_t tiles = ((a.M + 256 * PM - 1) / (256 * PM)) * ((a.N + BN * PN - 1) / (BN * PN));
   const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
   return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
-                  tsfb, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
+                  tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
 
 #if ADAHOP_EXPERIMENTS
