@@ -517,18 +517,24 @@ def main():
     # ---- calibration pass (a1, config 5): one stats + classify step over the layer's 21 tensors
     #      (X, W, G_Y of every linear), timed like the step; 2 B read per element is the work
     cal_t = [L[n] for L in lin.values() for n in ("x", "w", "gy")]
-    cal_ws = torch.empty(max(ah.calibrate_workspace_bytes(*t.shape) for t in cal_t), dtype=torch.uint8, device=dev)
+    cal_ws = torch.empty(ah.calibrate_batch_workspace_bytes([t.shape for t in cal_t]), dtype=torch.uint8, device=dev)
     cal_cv = torch.empty((len(cal_t), 4), dtype=torch.float64, device=dev)
     cal_pat = torch.empty(len(cal_t), dtype=torch.uint8, device=dev)
 
-    def step_calib():
+    def step_calib():   # adahop_calibrate_batch: the 21 tensors in three launches
+        ah.calibrate_batch_async(cal_t, cal_ws, cal_cv, cal_pat, params)
+
+    def step_calib_each():   # one adahop_calibrate per tensor (three launches each), for comparison
         for i, t in enumerate(cal_t):
             ah.calibrate_async(t, cal_ws, cal_cv[i], cal_pat[i:i + 1], params)
 
     step_calib()
     ms_cal, _ = timed(as_graph(step_calib), args.steps, args.warmup)
+    ms_cal_each, _ = timed(as_graph(step_calib_each), args.steps, args.warmup)
+    step_calib()
     cal_bytes = sum(t.numel() * 2 for t in cal_t)
-    calib = {"ms_per_calibration_step": ms_cal, "tensors": len(cal_t), "bytes_read": cal_bytes,
+    calib = {"ms_per_calibration_step": ms_cal, "api": "adahop_calibrate_batch (3 launches)",
+             "ms_per_calibration_step_per_tensor_calls": ms_cal_each, "tensors": len(cal_t), "bytes_read": cal_bytes,
              "GB_per_s": cal_bytes / (ms_cal * 1e-3) / 1e9,
              "frac_of_hbm": cal_bytes / (ms_cal * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
              "patterns": "".join("NRC"[int(v)] for v in cal_pat.cpu().tolist())}

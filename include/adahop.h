@@ -162,6 +162,17 @@ adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows,
                                  int64_t ld, const adahop_params_t* p, void* ws, size_t ws_bytes,
                                  double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
 
+/* n calibration steps at once — the operands of one training step (§5.1: every linear's X, W and
+ * G_Y) — in three kernel launches per 32 tensors instead of three per tensor. Tensor i
+ * is T[i] (device, dtype dt for all) with rows[i] x cols[i] elements, row pitch ld[i] (host arrays
+ * of n entries); results go to d_cv[4 i .. 4 i + 3] and d_pattern[i] exactly as n adahop_calibrate
+ * calls would write them (same partition and reduction order: bitwise equal). The workspace is
+ * the n single-tensor workspaces back to back (adahop_calibrate_batch_workspace_bytes). */
+size_t adahop_calibrate_batch_workspace_bytes(int32_t n, const int64_t* rows, const int64_t* cols);
+adahop_status_t adahop_calibrate_batch(int32_t n, const void* const* T, adahop_dtype_t dt, const int64_t* rows,
+                                       const int64_t* cols, const int64_t* ld, const adahop_params_t* p, void* ws,
+                                       size_t ws_bytes, double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
+
 /* ------------------------------------------------------------------- hot path */
 
 /* Generic AdaHOP GEMM in stored form: C[M x N] = A_store[M x K] · B_store[N x K]^T under

@@ -28,6 +28,7 @@ __all__ = [
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
     "calibrate_workspace_bytes", "classify_sums", "LinearContext", "linear_forward", "linear_backward",
     "split_workspace_bytes", "linear_ctx_bytes", "layer_strategies", "debug_sf_bytes", "debug_gemm_mxf4_tcsf",
+    "calibrate_batch_async", "calibrate_batch_workspace_bytes",
 ]
 
 
@@ -180,6 +181,34 @@ def calibrate_async(t: torch.Tensor, ws: torch.Tensor, cv: torch.Tensor, pat: to
     rows, cols = t.shape
     check("adahop_calibrate", lib.adahop_calibrate(_ptr(t), _dt(t), rows, cols, t.stride(0), C.byref(p),
                                                    _ptr(ws), ws.numel(), _ptr(cv), _ptr(pat), _stream()))
+
+
+def calibrate_batch_workspace_bytes(shapes) -> int:
+    """Workspace of calibrate_batch_async for tensors of the given (rows, cols) shapes."""
+    n = len(shapes)
+    rows = (C.c_int64 * n)(*[int(r) for r, _ in shapes])
+    cols = (C.c_int64 * n)(*[int(c) for _, c in shapes])
+    return int(lib.adahop_calibrate_batch_workspace_bytes(n, rows, cols))
+
+
+def calibrate_batch_async(tensors, ws: torch.Tensor, cv: torch.Tensor, pat: torch.Tensor,
+                          params: Params | None = None) -> None:
+    """adahop_calibrate_batch: one calibration step of every tensor in `tensors` (same dtype), three
+    launches per 32 tensors, graph-capturable; cv [n, 4] fp64 and pat [n] uint8 receive what n
+    calibrate_async calls would write."""
+    p = params or Params()
+    n = len(tensors)
+    for t in tensors:
+        _check_rowmajor(t)
+        assert t.dtype == tensors[0].dtype
+    assert cv.dtype == torch.float64 and cv.is_contiguous() and cv.numel() >= 4 * n
+    assert pat.dtype == torch.uint8 and pat.numel() >= n
+    ptrs = (C.c_void_p * n)(*[t.data_ptr() for t in tensors])
+    rows = (C.c_int64 * n)(*[t.shape[0] for t in tensors])
+    cols = (C.c_int64 * n)(*[t.shape[1] for t in tensors])
+    ld = (C.c_int64 * n)(*[t.stride(0) for t in tensors])
+    check("adahop_calibrate_batch", lib.adahop_calibrate_batch(n, ptrs, _dt(tensors[0]), rows, cols, ld, C.byref(p),
+                                                               _ptr(ws), ws.numel(), _ptr(cv), _ptr(pat), _stream()))
 
 
 def calibrate_workspace_bytes(rows: int, cols: int) -> int:

@@ -368,6 +368,53 @@ adahop_status_t adahop_calibrate(const void* T, adahop_dtype_t dt, int64_t rows,
   return ADAHOP_OK;
 }
 
+size_t adahop_calibrate_batch_workspace_bytes(int32_t n, const int64_t* rows, const int64_t* cols) {
+  if (n <= 0 || !rows || !cols) return 0;
+  size_t total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const size_t b = adahop_calibrate_workspace_bytes(rows[i], cols[i]);
+    if (b == 0) return 0;
+    total += (b + 255) & ~size_t(255);
+  }
+  return total;
+}
+
+adahop_status_t adahop_calibrate_batch(int32_t n, const void* const* T, adahop_dtype_t dt, const int64_t* rows,
+                                       const int64_t* cols, const int64_t* ld, const adahop_params_t* p, void* ws,
+                                       size_t ws_bytes, double* d_cv, uint8_t* d_pattern, adahop_stream_t stream) {
+  if (n <= 0 || !T || !rows || !cols || !ld || !p || !ws || !d_cv || !d_pattern) return ADAHOP_E_INVALID_ARG;
+  if (dt != ADAHOP_DT_BF16 && dt != ADAHOP_DT_F32) return ADAHOP_E_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i) {
+    if (!T[i]) return ADAHOP_E_INVALID_ARG;
+    if (rows[i] <= 0 || cols[i] <= 0 || ld[i] < cols[i]) return ADAHOP_E_SHAPE;
+  }
+  if (ws_bytes < adahop_calibrate_batch_workspace_bytes(n, rows, cols) || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ADAHOP_E_WORKSPACE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  int32_t launches = 0;
+  for (int32_t i0 = 0; i0 < n; i0 += kCalibMaxJobs) {
+    CalibJob jobs[kCalibMaxJobs];
+    const int m = int(std::min<int32_t>(kCalibMaxJobs, n - i0));
+    for (int k = 0; k < m; ++k) {
+      const int32_t i = i0 + k;
+      Carver c;   // the single-tensor layout of adahop_calibrate
+      double* rs = reinterpret_cast<double*>(base + c.take(size_t(rows[i]) * 32));
+      double* csum = reinterpret_cast<double*>(base + c.take(size_t(cols[i]) * 32));
+      double* sws = reinterpret_cast<double*>(base + c.take(adahop_stats_workspace_bytes(rows[i], cols[i])));
+      double* cvpart = reinterpret_cast<double*>(base + c.take(calib_cvpart_bytes(rows[i], cols[i])));
+      jobs[k] = CalibJob{T[i], rows[i], cols[i], ld[i], rs, csum, sws, cvpart, d_cv + 4 * int64_t(i), d_pattern + i};
+      base += (adahop_calibrate_workspace_bytes(rows[i], cols[i]) + 255) & ~size_t(255);
+    }
+    ADAHOP_LAUNCH(launch_calibrate_batch(jobs, m, dt == ADAHOP_DT_F32, double(p->eps), double(p->tau), cs));
+    launches += 3;
+  }
+  g_launches = launches;
+  return ADAHOP_OK;
+}
+
 // ------------------------------------------------------------------------ hot path
 size_t adahop_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
                                    const adahop_params_t* p) {

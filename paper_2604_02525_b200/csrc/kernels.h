@@ -146,6 +146,16 @@ size_t calib_cvpart_bytes(int64_t R, int64_t C);
 cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld, double* rs, double* cs,
                              double* part, double* cvpart, double eps, double tau, double* d_cv, uint8_t* pattern,
                              cudaStream_t st);
+// Several calibration steps (stats -> CV partials -> R/C/N) in three launches; every job uses
+// the single-tensor workspace layout (rs, cs, stats partials `part`, cvpart) and gets the same
+// bits as launch_calibrate.
+constexpr int kCalibMaxJobs = 32;
+struct CalibJob {
+  const void* in; int64_t R, C, ld;
+  double *rs, *cs, *part, *cvpart, *d_cv;
+  uint8_t* pattern;
+};
+cudaError_t launch_calibrate_batch(const CalibJob* jobs, int n, bool in_f32, double eps, double tau, cudaStream_t st);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);
 cudaError_t launch_classify_sums(double* d_cv, int64_t rows, int64_t cols, double tau, uint8_t* pattern,

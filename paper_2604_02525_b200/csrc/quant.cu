@@ -1295,12 +1295,10 @@ struct StatAcc {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kStatsThreads) k_stats_tile(const T* __restrict__ in, int64_t R, int64_t C,
-                                                              int64_t ld, int64_t rb_rows, double* __restrict__ rpart,
-                                                              double* __restrict__ cpart) {
-  __shared__ __align__(16) uint8_t tile[kStatsTileRows * kStatsPitch];   // bf16 inputs only
+__device__ __forceinline__ void stats_tile_block(const T* __restrict__ in, int64_t R, int64_t C, int64_t ld,
+                                                 int64_t rb_rows, double* __restrict__ rpart,
+                                                 double* __restrict__ cpart, int cb, int chunk, uint8_t* tile) {
   const int tid = threadIdx.x;
-  const int cb = blockIdx.x, chunk = blockIdx.y;
   const int64_t c0 = int64_t(cb) * 256;
   const int64_t r_end = min(R, int64_t(chunk) * rb_rows + rb_rows);
   const bool vec = sizeof(T) == 2 && c0 + 256 <= C && ((ld * 2) % 16) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
@@ -1390,6 +1388,13 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tile(const T* __restric
     p[0] = col.s; p[1] = col.s2; p[2] = col.sa; p[3] = double(col.mx);
   }
 }
+template <typename T>
+__global__ void __launch_bounds__(kStatsThreads) k_stats_tile(const T* __restrict__ in, int64_t R, int64_t C,
+                                                              int64_t ld, int64_t rb_rows, double* __restrict__ rpart,
+                                                              double* __restrict__ cpart) {
+  __shared__ __align__(16) uint8_t tile[kStatsTileRows * kStatsPitch];   // bf16 inputs only
+  stats_tile_block(in, R, C, ld, rb_rows, rpart, cpart, int(blockIdx.x), int(blockIdx.y), tile);
+}
 
 // cvpart (nullable): per-block partial sums of the CV terms std/(mean|x| + eps) of the rows
 // (cvpart[2 b]) and columns (cvpart[2 b + 1]) this block finalised (App. A), for
@@ -1408,13 +1413,12 @@ __host__ __device__ inline int stats_col_lanes(int64_t C) { return C <= 2048 ? 8
 __host__ __device__ inline int64_t stats_reduce_threads(int64_t R, int64_t C) {
   return (R + 31) / 32 * 32 + C * stats_col_lanes(C);
 }
-__global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* __restrict__ rpart, int64_t ncb,
-                                                                 int64_t R, const double* __restrict__ cpart,
-                                                                 int64_t nch, int64_t C, double* __restrict__ rs,
-                                                                 double* __restrict__ cs, double* __restrict__ cvpart,
-                                                                 double eps) {
-  __shared__ double red[2][kReduceThreads];
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void stats_reduce_block(const double* __restrict__ rpart, int64_t ncb, int64_t R,
+                                                   const double* __restrict__ cpart, int64_t nch, int64_t C,
+                                                   double* __restrict__ rs, double* __restrict__ cs,
+                                                   double* __restrict__ cvpart, double eps, int blk,
+                                                   double (*red)[kReduceThreads]) {
+  const int64_t i = int64_t(blk) * blockDim.x + threadIdx.x;
   const int64_t rpad = (R + 31) / 32 * 32;
   const int lanes = stats_col_lanes(C);
   const bool is_row = i < rpad;                                   // warp-uniform
@@ -1469,9 +1473,17 @@ __global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* _
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    cvpart[2 * blockIdx.x] = red[0][0];
-    cvpart[2 * blockIdx.x + 1] = red[1][0];
+    cvpart[2 * blk] = red[0][0];
+    cvpart[2 * blk + 1] = red[1][0];
   }
+}
+__global__ void __launch_bounds__(kReduceThreads) k_stats_reduce(const double* __restrict__ rpart, int64_t ncb,
+                                                                 int64_t R, const double* __restrict__ cpart,
+                                                                 int64_t nch, int64_t C, double* __restrict__ rs,
+                                                                 double* __restrict__ cs, double* __restrict__ cvpart,
+                                                                 double eps) {
+  __shared__ double red[2][kReduceThreads];
+  stats_reduce_block(rpart, ncb, R, cpart, nch, C, rs, cs, cvpart, eps, int(blockIdx.x), red);
 }
 
 // App. A decision (DESIGN R7) from the two CV sums: d_cv[0..1] = the sums,
@@ -1492,10 +1504,9 @@ __device__ __forceinline__ void classify_store(double sum_row, double sum_col, i
 }
 
 // Sum of the blocks' CV partials (fixed order) and the single-rank classification.
-__global__ void __launch_bounds__(256) k_classify_partials(const double* __restrict__ cvpart, int nb, int64_t rows,
-                                                          int64_t cols, double tau, double* __restrict__ d_cv,
-                                                          uint8_t* __restrict__ pattern) {
-  __shared__ double red[2][256];
+__device__ __forceinline__ void classify_partials_block(const double* __restrict__ cvpart, int nb, int64_t rows,
+                                                        int64_t cols, double tau, double* __restrict__ d_cv,
+                                                        uint8_t* __restrict__ pattern, double (*red)[256]) {
   double a = 0, b = 0;
   for (int k = threadIdx.x; k < nb; k += 256) { a += cvpart[2 * k]; b += cvpart[2 * k + 1]; }
   red[0][threadIdx.x] = a;
@@ -1509,6 +1520,53 @@ __global__ void __launch_bounds__(256) k_classify_partials(const double* __restr
     __syncthreads();
   }
   if (threadIdx.x == 0) classify_store(red[0][0], red[1][0], rows, cols, tau, d_cv, pattern);
+}
+__global__ void __launch_bounds__(256) k_classify_partials(const double* __restrict__ cvpart, int nb, int64_t rows,
+                                                          int64_t cols, double tau, double* __restrict__ d_cv,
+                                                          uint8_t* __restrict__ pattern) {
+  __shared__ double red[2][256];
+  classify_partials_block(cvpart, nb, rows, cols, tau, d_cv, pattern, red);
+}
+
+// Batched calibration: up to kCalibMaxJobs tensors per launch triple, every job's blocks exactly
+// as in the single-tensor launches (same partition, same reduction order: bitwise the same).
+struct CalibJobDev {
+  const void* in; int64_t R, C, ld, rb, ncb, nch;
+  double *rpart, *cpart, *rs, *cs, *cvpart, *d_cv;
+  uint8_t* pattern;
+  int nbr;   // reduce blocks
+};
+struct CalibBatchDev {
+  CalibJobDev j[kCalibMaxJobs];
+  int n, f32;
+  int tile_off[kCalibMaxJobs + 1], red_off[kCalibMaxJobs + 1];
+  double eps, tau;
+};
+__device__ __forceinline__ int calib_job_of(const int* off, int n, int b) {
+  int j = 0;
+  while (j + 1 < n && b >= off[j + 1]) ++j;
+  return j;
+}
+__global__ void __launch_bounds__(kStatsThreads) k_stats_tile_batch(const __grid_constant__ CalibBatchDev B) {
+  __shared__ __align__(16) uint8_t tile[kStatsTileRows * kStatsPitch];
+  const int jb = calib_job_of(B.tile_off, B.n, blockIdx.x);
+  const CalibJobDev& J = B.j[jb];
+  const int lid = int(blockIdx.x) - B.tile_off[jb];
+  const int cb = int(lid % J.ncb), chunk = int(lid / J.ncb);
+  if (B.f32) stats_tile_block(static_cast<const float*>(J.in), J.R, J.C, J.ld, J.rb, J.rpart, J.cpart, cb, chunk, tile);
+  else stats_tile_block(static_cast<const __nv_bfloat16*>(J.in), J.R, J.C, J.ld, J.rb, J.rpart, J.cpart, cb, chunk, tile);
+}
+__global__ void __launch_bounds__(kReduceThreads) k_stats_reduce_batch(const __grid_constant__ CalibBatchDev B) {
+  __shared__ double red[2][kReduceThreads];
+  const int jb = calib_job_of(B.red_off, B.n, blockIdx.x);
+  const CalibJobDev& J = B.j[jb];
+  stats_reduce_block(J.rpart, J.ncb, J.R, J.cpart, J.nch, J.C, J.rs, J.cs, J.cvpart, B.eps,
+                     int(blockIdx.x) - B.red_off[jb], red);
+}
+__global__ void __launch_bounds__(256) k_classify_partials_batch(const __grid_constant__ CalibBatchDev B) {
+  __shared__ double red[2][256];
+  const CalibJobDev& J = B.j[blockIdx.x];
+  classify_partials_block(J.cvpart, J.nbr, J.R, J.C, B.tau, J.d_cv, J.pattern, red);
 }
 
 size_t calib_cvpart_bytes(int64_t R, int64_t C) {
@@ -1547,6 +1605,35 @@ cudaError_t launch_calibrate(const void* in, bool in_f32, int64_t R, int64_t C, 
   const int nb = int((stats_reduce_threads(R, C) + kReduceThreads - 1) / kReduceThreads);
   k_stats_reduce<<<unsigned(nb), kReduceThreads, 0, st>>>(rpart, ncb, R, cpart, nch, C, rs, cs, cvpart, eps);
   k_classify_partials<<<1, 256, 0, st>>>(cvpart, nb, R, C, tau, d_cv, pattern);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_calibrate_batch(const CalibJob* jobs, int n, bool in_f32, double eps, double tau, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kCalibMaxJobs) return cudaErrorInvalidValue;
+  CalibBatchDev B{};
+  B.n = n;
+  B.f32 = in_f32 ? 1 : 0;
+  B.eps = eps;
+  B.tau = tau;
+  B.tile_off[0] = B.red_off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    const CalibJob& q = jobs[i];
+    CalibJobDev& J = B.j[i];
+    J.in = q.in; J.R = q.R; J.C = q.C; J.ld = q.ld;
+    J.ncb = (q.C + 255) / 256;
+    J.rb = stats_rb(q.R, q.C);
+    J.nch = (q.R + J.rb - 1) / J.rb;
+    J.rpart = q.part;
+    J.cpart = q.part + J.ncb * q.R * 4;
+    J.rs = q.rs; J.cs = q.cs; J.cvpart = q.cvpart; J.d_cv = q.d_cv; J.pattern = q.pattern;
+    J.nbr = int((stats_reduce_threads(q.R, q.C) + kReduceThreads - 1) / kReduceThreads);
+    B.tile_off[i + 1] = B.tile_off[i] + int(J.ncb * J.nch);
+    B.red_off[i + 1] = B.red_off[i] + J.nbr;
+  }
+  k_stats_tile_batch<<<unsigned(B.tile_off[n]), kStatsThreads, 0, st>>>(B);
+  k_stats_reduce_batch<<<unsigned(B.red_off[n]), kReduceThreads, 0, st>>>(B);
+  k_classify_partials_batch<<<unsigned(n), 256, 0, st>>>(B);
   return cudaGetLastError();
 }
 

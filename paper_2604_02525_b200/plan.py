@@ -112,16 +112,16 @@ class Calibrator:
         self.device = dev
 
     def workspace_bytes(self, T: int) -> int:
-        return max(max(ah.calibrate_workspace_bytes(T, d_in), ah.calibrate_workspace_bytes(d_out, d_in),
-                       ah.calibrate_workspace_bytes(T, d_out)) for _, d_in, d_out in self.linears)
+        return max(ah.calibrate_batch_workspace_bytes([(T, d_in), (d_out, d_in), (T, d_out)])
+                   for _, d_in, d_out in self.linears)
 
     def record(self, step: int, name: str, x: torch.Tensor, w: torch.Tensor, gy: torch.Tensor) -> None:
+        """One calibration step of the linear's X, W and G_Y (adahop_calibrate_batch: three launches)."""
         i = self.index[name]
-        need = max(ah.calibrate_workspace_bytes(*t.shape) for t in (x, w, gy))
+        need = ah.calibrate_batch_workspace_bytes([t.shape for t in (x, w, gy)])
         if self.ws is None or self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-        for j, t in enumerate((x, w, gy)):
-            ah.calibrate_async(t, self.ws, self.cv[step, i, j], self.pat[step, i, j:j + 1], self.params)
+        ah.calibrate_batch_async([x, w, gy], self.ws, self.cv[step, i], self.pat[step, i], self.params)
 
     def record_sharded(self, step: int, name: str, x_local: torch.Tensor, w: torch.Tensor, gy_local: torch.Tensor,
                        rows_global: int, group=None) -> None:

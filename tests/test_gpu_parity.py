@@ -499,3 +499,27 @@ def test_gemm_kernel_alone_matches_debug_gemm():
         got = ah.debug_gemm_mxf4_tcsf(a, ea, b, eb, torch.empty((M, N), dtype=torch.float32, device="cuda"))
         torch.cuda.synchronize()
         assert torch.equal(got, ref)
+
+
+def test_calibrate_batch_equals_per_tensor_calls():
+    # adahop_calibrate_batch: the same partition and reduction order as adahop_calibrate, so the CV
+    # sums, CVs and patterns are bitwise equal; 35 tensors exercise the 32-job chunking, ragged shapes
+    rng = np.random.default_rng(11)
+    shapes = [(int(rng.integers(1, 700)), int(rng.integers(1, 900))) for _ in range(33)] + [(2048, 512), (384, 4096)]
+    pats = "RCN"
+    ts = [dev_bf16(synth.operand(r, c, pats[i % 3], "X", case_id=700 + i)[0]) for i, (r, c) in enumerate(shapes)]
+    ws = torch.empty(ah.calibrate_batch_workspace_bytes([t.shape for t in ts]), dtype=torch.uint8, device="cuda")
+    cv = torch.full((len(ts), 4), -1.0, dtype=torch.float64, device="cuda")
+    pat = torch.full((len(ts),), 255, dtype=torch.uint8, device="cuda")
+    ah.calibrate_batch_async(ts, ws, cv, pat)
+    one_ws = torch.empty(max(ah.calibrate_workspace_bytes(*t.shape) for t in ts), dtype=torch.uint8, device="cuda")
+    cv1 = torch.empty_like(cv)
+    pat1 = torch.empty_like(pat)
+    for i, t in enumerate(ts):
+        ah.calibrate_async(t, one_ws, cv1[i], pat1[i:i + 1])
+    torch.cuda.synchronize()
+    assert torch.equal(cv.view(torch.int64), cv1.view(torch.int64))
+    assert torch.equal(pat, pat1)
+    for i, t in enumerate(ts):   # and the oracle's decision on the planted ones
+        if min(shapes[i]) >= 64:
+            assert "NRC"[int(pat[i])] == O.classify(t.float().cpu().numpy().astype(np.float64)), i
