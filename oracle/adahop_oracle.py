@@ -266,6 +266,27 @@ def classify(t: np.ndarray, tau: float = TAU, eps: float = EPS) -> str:
     return "N"
 
 
+KAPPA = 32.0            # [R16] the factor standing for App. D's ">>"
+
+
+def outlier_counts(t: np.ndarray, kappa: float = KAPPA):
+    """Outlier rows and columns of t (App. D): row i is an outlier row when
+    max_j |t_ij| >> median |t|, column j likewise. Reading [R16]: the median over all entries is
+    replaced by the mean |t| = sum |t| / (m n) (both computed in fp64; for the unimodal bulk the
+    two differ by a constant factor that kappa absorbs) and ">>" by kappa = 32.
+    Returns (rows, cols)."""
+    a = np.abs(np.asarray(t, dtype=np.float64))
+    thr = kappa * (a.sum() / a.size)
+    return int((a.max(axis=1) > thr).sum()), int((a.max(axis=0) > thr).sum())
+
+
+def adaptive_k(count: int, k_max: int = OE_K, granule: int = 16) -> int:
+    """Per-layer OE k (P:503 names "an adaptive per-layer selection strategy based on per-layer
+    outlier severity" as future work; reading [R16]): the OE operand's outlier rows (stored
+    orientation) rounded up to the tcgen05 N granule, clamped to [granule, k_max]."""
+    return int(min(k_max, max(granule, -(-int(count) // granule) * granule)))
+
+
 def transpose_pattern(p: str) -> str:
     """pattern(T^T) = swap(R <-> C) [R8] — CV_row(T^T) = CV_col(T)."""
     return {"R": "C", "C": "R", "N": "N"}[p]

@@ -445,3 +445,36 @@ def test_gamma_definition():
     assert O.gamma(a) == 1.0
     a[0, 0] = 4.0
     assert abs(O.gamma(a) - 16 * 16 / (15 + 16)) < 1e-12
+
+
+# ---------------------------------------------------------------------- outlier counts / adaptive k [R16]
+def test_outlier_counts_closed_forms():
+    # planted channels (x100, the synth recipe) are exactly the counted ones in the pattern's
+    # direction at Llama shapes; Gaussian bulk rows / columns (max ~ 4 sigma against 32 x mean|x|
+    # ~ 25 sigma) are never counted. (Across the pattern, App. D's definition flags most
+    # channels: every column of a Row-pattern tensor holds an outlier-row entry.)
+    for rows, cols in ((2048, 512), (4096, 2048), (512, 4096)):
+        for pat in "RCN":
+            t, planted = synth.operand(rows, cols, pat, "X", case_id=1300 + rows % 7)
+            r, c = O.outlier_counts(t)
+            if pat == "R":
+                assert r == len(planted.rows), (rows, cols, r)
+            elif pat == "C":
+                assert c == len(planted.cols), (rows, cols, c)
+            else:
+                assert (r, c) == (0, 0)
+    # transpose swaps the counts; a positive scale leaves them unchanged
+    t, _ = synth.operand(1024, 768, "R", "GY", case_id=1310)
+    assert O.outlier_counts(t.T) == tuple(reversed(O.outlier_counts(t)))
+    assert O.outlier_counts(t * 2.0 ** 37) == O.outlier_counts(t)
+    # a single entry: one row and one column; a constant matrix: none
+    z = np.zeros((64, 64))
+    z[5, 9] = 1.0
+    assert O.outlier_counts(z) == (1, 1)
+    assert O.outlier_counts(np.ones((64, 64))) == (0, 0)
+
+
+def test_adaptive_k_rounding_and_clamps():
+    assert [O.adaptive_k(c) for c in (0, 1, 15, 16, 17, 33, 48, 49, 64, 65, 1000)] == \
+        [16, 16, 16, 16, 32, 48, 48, 64, 64, 64, 64]
+    assert O.adaptive_k(5, k_max=256) == 16 and O.adaptive_k(200, k_max=256) == 208
