@@ -21,6 +21,7 @@ Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N 
 from __future__ import annotations
 
 import argparse
+from collections import Counter
 import json
 import os
 import sys
@@ -51,6 +52,8 @@ def parse():
     ap.add_argument("--calib-steps", type=int, default=30)
     ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
     ap.add_argument("--oe-k", type=int, default=64)
+    ap.add_argument("--adaptive-k", action="store_true",
+                    help="stack workload: per-linear OE k from the calibration plan (DESIGN R16, P:503)")
     ap.add_argument("--level", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -734,7 +737,12 @@ def run_stack(args, rank, world, local, dev, torch, dist, ah, ahd):
                       gx=torch.empty(T, d_in, dtype=torch.bfloat16, device=dev),
                       gw=torch.empty(d_out, d_in, dtype=torch.float32, device=dev))
     flops_step = sum(2.0 * T * dims[c[1]][0] * dims[c[1]][1] * 3 for c in cfg)
-    ws = ah.Workspace(max(ah.layer_workspace_bytes(T, d_in, d_out, plan.strategies(k), params)
+    # per-linear parameters: the global k, or (--adaptive-k) the plan's per-layer k (DESIGN R16)
+    lparams = {}
+    for lp in plan.linears:
+        k_lin = lp.oe_k if (args.adaptive_k and lp.oe_k > 0) else args.oe_k
+        lparams[lp.name] = params if k_lin == args.oe_k else ah.Params(oe_k=k_lin, level=args.level)
+    ws = ah.Workspace(max(ah.layer_workspace_bytes(T, d_in, d_out, plan.strategies(k), lparams[k])
                           for k, d_in, d_out in linears), dev)
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = [0]
@@ -744,7 +752,7 @@ def run_stack(args, rank, world, local, dev, torch, dist, ah, ahd):
         n = 0
         for k in keys:      # the plan fixes every GEMM's strategy: no runtime detection
             L = lin[k]
-            ah.linear_layer(L["x"], L["w"], L["gy"], plan.strategies(k), params, out=(L["y"], L["gx"], L["gw"]),
+            ah.linear_layer(L["x"], L["w"], L["gy"], plan.strategies(k), lparams[k], out=(L["y"], L["gx"], L["gw"]),
                             ws=ws)
             n += ah.last_launch_count()
             if world > 1:
@@ -844,7 +852,9 @@ def run_stack(args, rank, world, local, dev, torch, dist, ah, ahd):
                 "vs_baseline": None, "dtype": "mxfp4", "data": "synthetic",
                 "config": {"workload": "llama32_1b_stack_336gemm (BASELINE configs[4]: 16 layers x 7 linears x "
                                        "fwd/dgrad/wgrad) with calibration -> plan",
-                           "tokens_per_gpu": T, "global_tokens": T * world, "oe_k": args.oe_k, "level": args.level,
+                           "tokens_per_gpu": T, "global_tokens": T * world,
+                           "oe_k": ({"adaptive (DESIGN R16)": dict(Counter(lp.oe_k for lp in plan.linears))}
+                                    if args.adaptive_k else args.oe_k), "level": args.level,
                            "hadamard_block": 32, "out_dtype": "bf16 (Y, G_X), fp32 (G_W)",
                            "patterns": "Table-1 census of Llama3.2-1B (P:190-195), synth.llama32_1b_census_patterns",
                            "l2": "flushed between steps (256 MiB write, untimed)",

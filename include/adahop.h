@@ -173,6 +173,15 @@ adahop_status_t adahop_calibrate_batch(int32_t n, const void* const* T, adahop_d
                                        const int64_t* cols, const int64_t* ld, const adahop_params_t* p, void* ws,
                                        size_t ws_bytes, double* d_cv, uint8_t* d_pattern, adahop_stream_t stream);
 
+/* Outlier severity for a per-layer OE k (DESIGN R16, after App. D): called after
+ * adahop_calibrate_batch with the same n / rows / cols / ws (it reads the row and column statistics
+ * left there), writes d_counts[2 i] = the rows of tensor i whose max |x| exceeds kappa * mean |x|
+ * (mean over all entries) and d_counts[2 i + 1] = the columns likewise (int32, device). One launch
+ * per 32 tensors; kappa > 0 (the reading uses 32). */
+adahop_status_t adahop_calibrate_batch_outliers(int32_t n, const int64_t* rows, const int64_t* cols, const void* ws,
+                                                size_t ws_bytes, double kappa, int32_t* d_counts,
+                                                adahop_stream_t stream);
+
 /* ------------------------------------------------------------------- hot path */
 
 /* Generic AdaHOP GEMM in stored form: C[M x N] = A_store[M x K] · B_store[N x K]^T under

@@ -50,6 +50,7 @@ SIGNATURES = {
     "adahop_calibrate": (I32, [P, I32, I64, I64, I64, PP, P, SZ, P, P, P]),
     "adahop_calibrate_batch_workspace_bytes": (SZ, [I32, P, P]),
     "adahop_calibrate_batch": (I32, [I32, P, I32, P, P, P, PP, P, SZ, P, P, P]),
+    "adahop_calibrate_batch_outliers": (I32, [I32, P, P, P, SZ, C.c_double, P, P]),
     "adahop_gemm_workspace_bytes": (SZ, [I64, I64, I64, I32, PP]),
     "adahop_gemm": (I32, [P, I32, I64, P, I32, I64, P, I32, I64, I64, I64, I64, I32, PP, P, SZ, P]),
     "adahop_workspace_bytes": (SZ, [I32, I64, I64, I64, I32, PP]),

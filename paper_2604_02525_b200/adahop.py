@@ -28,7 +28,7 @@ __all__ = [
     "Workspace", "StageEvents", "linear_layer", "layer_workspace_bytes", "calibrate_async",
     "calibrate_workspace_bytes", "classify_sums", "LinearContext", "linear_forward", "linear_backward",
     "split_workspace_bytes", "linear_ctx_bytes", "layer_strategies", "debug_sf_bytes", "debug_gemm_mxf4_tcsf",
-    "calibrate_batch_async", "calibrate_batch_workspace_bytes",
+    "calibrate_batch_async", "calibrate_batch_workspace_bytes", "calibrate_batch_outliers_async", "KAPPA",
 ]
 
 
@@ -209,6 +209,21 @@ def calibrate_batch_async(tensors, ws: torch.Tensor, cv: torch.Tensor, pat: torc
     ld = (C.c_int64 * n)(*[t.stride(0) for t in tensors])
     check("adahop_calibrate_batch", lib.adahop_calibrate_batch(n, ptrs, _dt(tensors[0]), rows, cols, ld, C.byref(p),
                                                                _ptr(ws), ws.numel(), _ptr(cv), _ptr(pat), _stream()))
+
+
+KAPPA = 32.0   # DESIGN R16: the factor standing for App. D's ">>"
+
+
+def calibrate_batch_outliers_async(shapes, ws: torch.Tensor, counts: torch.Tensor, kappa: float = KAPPA) -> None:
+    """adahop_calibrate_batch_outliers after calibrate_batch_async with the same shapes and ws: counts
+    [n, 2] int32 receives each tensor's outlier rows and columns (DESIGN R16)."""
+    n = len(shapes)
+    assert counts.dtype == torch.int32 and counts.is_contiguous() and counts.numel() >= 2 * n
+    rows = (C.c_int64 * n)(*[int(r) for r, _ in shapes])
+    cols = (C.c_int64 * n)(*[int(c) for _, c in shapes])
+    check("adahop_calibrate_batch_outliers",
+          lib.adahop_calibrate_batch_outliers(n, rows, cols, _ptr(ws), ws.numel(), float(kappa), _ptr(counts),
+                                              _stream()))
 
 
 def calibrate_workspace_bytes(rows: int, cols: int) -> int:

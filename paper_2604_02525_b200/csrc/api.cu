@@ -415,6 +415,37 @@ adahop_status_t adahop_calibrate_batch(int32_t n, const void* const* T, adahop_d
   return ADAHOP_OK;
 }
 
+adahop_status_t adahop_calibrate_batch_outliers(int32_t n, const int64_t* rows, const int64_t* cols, const void* ws,
+                                                size_t ws_bytes, double kappa, int32_t* d_counts,
+                                                adahop_stream_t stream) {
+  if (n <= 0 || !rows || !cols || !ws || !d_counts || !(kappa > 0)) return ADAHOP_E_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i)
+    if (rows[i] <= 0 || cols[i] <= 0) return ADAHOP_E_SHAPE;
+  if (ws_bytes < adahop_calibrate_batch_workspace_bytes(n, rows, cols) || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ADAHOP_E_WORKSPACE;
+  adahop_status_t st = check_device(nullptr);
+  if (st != ADAHOP_OK) return st;
+  const uint8_t* base = static_cast<const uint8_t*>(ws);
+  int32_t launches = 0;
+  for (int32_t i0 = 0; i0 < n; i0 += kCalibMaxJobs) {
+    CalibJob jobs[kCalibMaxJobs];
+    const int m = int(std::min<int32_t>(kCalibMaxJobs, n - i0));
+    for (int k = 0; k < m; ++k) {
+      const int32_t i = i0 + k;
+      Carver c;   // rs and cs of adahop_calibrate's layout
+      double* rs = reinterpret_cast<double*>(const_cast<uint8_t*>(base) + c.take(size_t(rows[i]) * 32));
+      double* csum = reinterpret_cast<double*>(const_cast<uint8_t*>(base) + c.take(size_t(cols[i]) * 32));
+      jobs[k] = CalibJob{nullptr, rows[i], cols[i], cols[i], rs, csum, nullptr, nullptr, nullptr, nullptr};
+      base += (adahop_calibrate_workspace_bytes(rows[i], cols[i]) + 255) & ~size_t(255);
+    }
+    ADAHOP_LAUNCH(launch_outlier_counts_batch(jobs, m, kappa, d_counts + 2 * int64_t(i0),
+                                              reinterpret_cast<cudaStream_t>(stream)));
+    ++launches;
+  }
+  g_launches = launches;
+  return ADAHOP_OK;
+}
+
 // ------------------------------------------------------------------------ hot path
 size_t adahop_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, adahop_strategy_t s,
                                    const adahop_params_t* p) {

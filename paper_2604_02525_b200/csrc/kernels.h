@@ -156,6 +156,9 @@ struct CalibJob {
   uint8_t* pattern;
 };
 cudaError_t launch_calibrate_batch(const CalibJob* jobs, int n, bool in_f32, double eps, double tau, cudaStream_t st);
+// counts[2 i], counts[2 i + 1] = the outlier rows / columns of job i (DESIGN R16) from the
+// statistics launch_calibrate_batch left in jobs[i].rs / .cs
+cudaError_t launch_outlier_counts_batch(const CalibJob* jobs, int n, double kappa, int32_t* counts, cudaStream_t st);
 cudaError_t launch_stats(const void* in, bool in_f32, int64_t R, int64_t C, int64_t ld,
                          double* rs, double* cs, double* part, cudaStream_t st);
 cudaError_t launch_classify_sums(double* d_cv, int64_t rows, int64_t cols, double tau, uint8_t* pattern,

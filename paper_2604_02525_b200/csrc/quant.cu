@@ -1637,6 +1637,51 @@ cudaError_t launch_calibrate_batch(const CalibJob* jobs, int n, bool in_f32, dou
   return cudaGetLastError();
 }
 
+// Outlier rows / columns of each calibrated tensor (App. D, DESIGN R16): from the
+// statistics the batch left in its workspace — sum |x| of every row (fixed order over the rows)
+// gives mean |x|; rows / columns whose max |x| exceeds kappa * mean |x| are counted.
+__global__ void __launch_bounds__(256) k_outlier_counts_batch(const __grid_constant__ CalibBatchDev B, double kappa,
+                                                             int32_t* __restrict__ counts) {
+  __shared__ double red[256];
+  __shared__ int cnt[2];
+  const CalibJobDev& J = B.j[blockIdx.x];
+  double a = 0;
+  for (int64_t i = threadIdx.x; i < J.R; i += 256) a += J.rs[i * 4 + 2];
+  red[threadIdx.x] = a;
+  if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (int(threadIdx.x) < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  const double thr = kappa * (red[0] / (double(J.R) * double(J.C)));
+  int nr = 0, nc = 0;
+  for (int64_t i = threadIdx.x; i < J.R; i += 256) nr += J.rs[i * 4 + 3] > thr;
+  for (int64_t j = threadIdx.x; j < J.C; j += 256) nc += J.cs[j * 4 + 3] > thr;
+  atomicAdd(&cnt[0], nr);
+  atomicAdd(&cnt[1], nc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counts[2 * blockIdx.x] = cnt[0];
+    counts[2 * blockIdx.x + 1] = cnt[1];
+  }
+}
+
+cudaError_t launch_outlier_counts_batch(const CalibJob* jobs, int n, double kappa, int32_t* counts, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kCalibMaxJobs) return cudaErrorInvalidValue;
+  CalibBatchDev B{};
+  B.n = n;
+  for (int i = 0; i < n; ++i) {
+    B.j[i].R = jobs[i].R;
+    B.j[i].C = jobs[i].C;
+    B.j[i].rs = jobs[i].rs;
+    B.j[i].cs = jobs[i].cs;
+  }
+  k_outlier_counts_batch<<<unsigned(n), 256, 0, st>>>(B, kappa, counts);
+  return cudaGetLastError();
+}
+
 // CV sums (App. A) and the single-rank classification (DESIGN R7).
 __global__ void __launch_bounds__(1024) k_classify(const double* __restrict__ rs, int64_t rows,
                                                    int64_t row_len, const double* __restrict__ cs,

@@ -32,6 +32,29 @@ class LinearPlan:
     strategies: tuple                    # (fwd, dgrad, wgrad)
     fed_pairs: tuple                     # fed (left, right) patterns per path, e.g. ('CN', 'CN', 'RC')
     votes: dict = field(default_factory=dict)   # tensor -> {pattern: steps}
+    oe_k: int = 0                        # per-layer OE k (DESIGN R16; 0 = the global k)
+    outliers: dict = field(default_factory=dict)   # tensor -> [rows, cols], the largest over the steps
+
+
+# The OE operand of each path, as (tensor, axis of that tensor whose outlier count sizes k):
+# OE-Left extracts rows of A_store, OE-Right rows of B_store: fwd A = X, B_store = W;
+# dgrad A = G_Y, B_store = W^T (W's columns); wgrad A = G_Y^T (G_Y's columns), B_store = X^T (X's columns)
+OE_OPERAND = {("fwd", "OE_LEFT_IHT"): ("X", 0), ("fwd", "OE_RIGHT_IHT"): ("W", 0),
+              ("dgrad", "OE_LEFT_IHT"): ("G_Y", 0), ("dgrad", "OE_RIGHT_IHT"): ("W", 1),
+              ("wgrad", "OE_LEFT_IHT"): ("G_Y", 1), ("wgrad", "OE_RIGHT_IHT"): ("X", 1)}
+
+
+def adaptive_k(count: int, k_max: int = 64, granule: int = 16) -> int:
+    """DESIGN R16: the OE operand's outlier rows rounded up to the tcgen05 N granule,
+    clamped to [granule, k_max]."""
+    return int(min(k_max, max(granule, -(-int(count) // granule) * granule)))
+
+
+def layer_oe_k(strategies, outliers: dict, k_max: int = 64) -> int:
+    """One k per linear (adahop_linear_layer takes one): the largest over its OE paths."""
+    ks = [adaptive_k(outliers[OE_OPERAND[(p, s)][0]][OE_OPERAND[(p, s)][1]], k_max)
+          for p, s in zip(PATHS, strategies) if (p, s) in OE_OPERAND]
+    return max(ks) if ks else 0
 
 
 @dataclass
@@ -60,7 +83,8 @@ class Plan:
     def from_json(text: str) -> "Plan":
         d = json.loads(text)
         lins = [LinearPlan(e["name"], e["d_in"], e["d_out"], e["patterns"], tuple(e["strategies"]),
-                           tuple(e["fed_pairs"]), e.get("votes", {})) for e in d["linears"]]
+                           tuple(e["fed_pairs"]), e.get("votes", {}), e.get("oe_k", 0), e.get("outliers", {}))
+                for e in d["linears"]]
         return Plan(d["level"], d["steps"], lins)
 
     def save(self, path: str) -> None:
@@ -73,10 +97,12 @@ class Plan:
             return Plan.from_json(f.read())
 
 
-def plan_from_patterns(linears, per_step: dict, level: int = 1) -> Plan:
+def plan_from_patterns(linears, per_step: dict, level: int = 1, outliers: dict | None = None,
+                       k_max: int = 64) -> Plan:
     """linears: [(name, d_in, d_out)]; per_step[(name, tensor)] = the per-step pattern letters.
     Votes each record (adahop_majority_vote) and maps the voted patterns to the three strategies
-    (adahop_layer_strategies)."""
+    (adahop_layer_strategies). With outliers[(name, tensor)] = [rows, cols] (the largest over the
+    steps) each linear also gets its adaptive OE k (DESIGN R16)."""
     out = []
     steps = 0
     for name, d_in, d_out in linears:
@@ -87,7 +113,11 @@ def plan_from_patterns(linears, per_step: dict, level: int = 1) -> Plan:
             pats[t] = ah.majority_vote(rec)
             votes[t] = dict(Counter(rec))
         strategies, fed = ah.layer_strategies(pats["X"], pats["W"], pats["G_Y"], level)
-        out.append(LinearPlan(name, d_in, d_out, pats, strategies, fed, votes))
+        lp = LinearPlan(name, d_in, d_out, pats, strategies, fed, votes)
+        if outliers is not None:
+            lp.outliers = {t: list(outliers[(name, t)]) for t in TENSORS}
+            lp.oe_k = layer_oe_k(strategies, lp.outliers, k_max)
+        out.append(lp)
     return Plan(level, steps, out)
 
 
@@ -108,6 +138,7 @@ class Calibrator:
         n = len(self.linears)
         self.pat = torch.full((steps, n, 3), 255, dtype=torch.uint8, device=dev)
         self.cv = torch.zeros((steps, n, 3, 4), dtype=torch.float64, device=dev)
+        self.cnt = torch.full((steps, n, 3, 2), -1, dtype=torch.int32, device=dev)   # outlier rows / cols
         self.ws = None
         self.device = dev
 
@@ -121,7 +152,9 @@ class Calibrator:
         need = ah.calibrate_batch_workspace_bytes([t.shape for t in (x, w, gy)])
         if self.ws is None or self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        shapes = [x.shape, w.shape, gy.shape]
         ah.calibrate_batch_async([x, w, gy], self.ws, self.cv[step, i], self.pat[step, i], self.params)
+        ah.calibrate_batch_outliers_async(shapes, self.ws, self.cnt[step, i])
 
     def record_sharded(self, step: int, name: str, x_local: torch.Tensor, w: torch.Tensor, gy_local: torch.Tensor,
                        rows_global: int, group=None) -> None:
@@ -151,5 +184,14 @@ class Calibrator:
                 out[(name, t)] = [ah.PAT_NAME[c] for c in rec]
         return out
 
-    def plan(self, level: int = 1) -> Plan:
-        return plan_from_patterns(self.linears, self.per_step_patterns(), level)
+    def outlier_counts(self) -> dict | None:
+        """(name, tensor) -> [rows, cols], the largest over the steps; None if any step lacks them
+        (the token-sharded record keeps no counts)."""
+        c = self.cnt.cpu()
+        if bool((c < 0).any()):
+            return None
+        mx = c.amax(dim=0).tolist()
+        return {(name, t): mx[i][j] for name, i in self.index.items() for j, t in enumerate(TENSORS)}
+
+    def plan(self, level: int = 1, k_max: int = 64) -> Plan:
+        return plan_from_patterns(self.linears, self.per_step_patterns(), level, self.outlier_counts(), k_max)

@@ -53,3 +53,30 @@ def test_calibration_plan_recovers_table1_census():
         for t, p in zip(("X", "G_Y"), (px, pg)):
             if p != "N":
                 assert lp.votes[t] == {p: 26, "N": 4}
+    # adaptive k (DESIGN R16): T = 1024 tokens plant 2 channels per C tensor (0.1 % of 2048 / 8192
+    # columns: 3 / 9) and 2 rows per R tensor -> every OE operand's count rounds up to k = 16
+    for lp in plan.linears:
+        assert lp.oe_k == (16 if any(s.startswith("OE") for s in lp.strategies) else 0), (lp.name, lp.strategies)
+
+
+def test_outlier_counts_match_oracle():
+    # adahop_calibrate_batch_outliers against oracle.outlier_counts on planted tensors (the counts in
+    # the pattern's direction are the planted channels; across it App. D flags most channels)
+    import numpy as np
+    import oracle as O
+    shapes = [(2048, 512, "R"), (4096, 2048, "C"), (512, 4096, "R"), (1024, 768, "N"), (16384, 512, "C")]
+    host, ts = [], []
+    for i, (r, c, p) in enumerate(shapes):
+        a, _ = synth.operand(r, c, p, "GY", case_id=1400 + i)
+        host.append(a)
+        ts.append(torch.from_numpy(a).to(DEV, torch.bfloat16))
+    ws = torch.empty(ah.calibrate_batch_workspace_bytes([t.shape for t in ts]), dtype=torch.uint8, device=DEV)
+    cv = torch.empty((len(ts), 4), dtype=torch.float64, device=DEV)
+    pat = torch.empty(len(ts), dtype=torch.uint8, device=DEV)
+    cnt = torch.empty((len(ts), 2), dtype=torch.int32, device=DEV)
+    ah.calibrate_batch_async(ts, ws, cv, pat)
+    ah.calibrate_batch_outliers_async([t.shape for t in ts], ws, cnt)
+    got = cnt.cpu().tolist()
+    for (r, c, p), a, g in zip(shapes, host, got):
+        want = O.outlier_counts(np.asarray(a, np.float64))   # the bf16 values the GPU saw
+        assert tuple(g) == want, (r, c, p, g, want)

@@ -71,3 +71,17 @@ def test_plan_json_round_trip(tmp_path):
     assert [lp.strategies for lp in back.linears] == [lp.strategies for lp in plan.linears]
     # Lv2: the 8 CC wgrads run in BF16
     assert sum(1 for lp in back.linears if lp.strategies[2] == "BF16") == 8
+
+
+def test_adaptive_k_matches_oracle_and_picks_the_oe_operand():
+    # plan.adaptive_k is the host copy of oracle.adaptive_k (DESIGN R16)
+    for c in (0, 1, 15, 16, 17, 40, 63, 64, 65, 500):
+        assert plan_mod.adaptive_k(c) == O.adaptive_k(c)
+    out = {"X": [3, 40], "W": [0, 17], "G_Y": [5, 70]}
+    # wgrad OE-Right sizes k from X's columns; dgrad OE-Left from G_Y's rows; the largest wins
+    assert plan_mod.layer_oe_k(("IHT", "IHT", "OE_RIGHT_IHT"), out) == 48
+    assert plan_mod.layer_oe_k(("IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT"), out) == 48
+    assert plan_mod.layer_oe_k(("IHT", "OE_LEFT_IHT", "IHT"), out) == 16
+    assert plan_mod.layer_oe_k(("IHT", "IHT", "OE_LEFT_IHT"), out) == 64   # G_Y's columns (70) -> clamp
+    assert plan_mod.layer_oe_k(("IHT", "OE_RIGHT_IHT", "BF16"), out) == 32  # W's columns (17)
+    assert plan_mod.layer_oe_k(("IHT", "IHT", "IHT"), out) == 0
