@@ -95,6 +95,19 @@ def test_host_validation_without_device():
     assert f.adahop_classify_sums(ptr, 0, 64, C.byref(p), ptr, None) == 2
     # wgrad needs T % 32 == 0
     assert f.adahop_linear_wgrad(ptr, ptr, ptr, 1, 48, 64, 64, 0, C.byref(p), ptr, 4096, None) == 2
+    # batched calibration: empty / null / bad shapes are rejected before the device query
+    rows = (C.c_int64 * 2)(64, 64)
+    cols = (C.c_int64 * 2)(64, 0)
+    ts = (C.c_void_p * 2)(ptr.value, ptr.value)
+    assert f.adahop_calibrate_batch(0, ts, 0, rows, cols, rows, C.byref(p), ptr, 4096, ptr, ptr, None) == 1
+    assert f.adahop_calibrate_batch(2, None, 0, rows, cols, rows, C.byref(p), ptr, 4096, ptr, ptr, None) == 1
+    assert f.adahop_calibrate_batch(2, ts, 0, rows, cols, rows, C.byref(p), ptr, 4096, ptr, ptr, None) == 2
+    assert f.adahop_calibrate_batch_workspace_bytes(2, rows, cols) == 0        # a zero-column tensor
+    assert f.adahop_calibrate_batch_outliers(2, rows, cols, ptr, 4096, 32.0, ptr, None) == 2
+    assert f.adahop_calibrate_batch_outliers(1, rows, rows, ptr, 4096, 0.0, ptr, None) == 1   # kappa must be > 0
+    # the GEMM-alone debug entry point: K % 32 and alignment checks before the device
+    assert f.adahop_debug_gemm_mxf4_tcsf(ptr, ptr, ptr, ptr, ptr, 1, 64, 64, 64, 48, None) == 2
+    assert f.adahop_debug_sf_bytes(128, 48) == 0 and f.adahop_debug_sf_bytes(128, 256) > 0
 
 
 def test_workspace_sizes_are_host_computable():
