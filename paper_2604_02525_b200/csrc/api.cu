@@ -176,7 +176,13 @@ int current_device() {
 // ADAHOP_OR_FUSED=0 (experiment builds) runs the wgrad OE-Right product as a BF16 GEMM instead
 bool or_fusion_enabled() {
   static const int v = knob("ADAHOP_OR_FUSED", 1);
-  static const bool on = v == 1 || v == 3;
+  static const bool on = v == 1 || v == 3 || v == 4;
+  return on;
+}
+
+// ADAHOP_OR_FUSED=4 (experiment builds): only the OE-Right product is fused
+bool or_left_enabled() {
+  static const bool on = knob("ADAHOP_OR_FUSED", 1) != 4;
   return on;
 }
 
@@ -593,7 +599,8 @@ struct LayerPlan {
   Buf idx_row[3], idx_col[3], slice_row[3], slice_col[3];
   Buf keys_row[3], keys_col[3];   // per-FOID scratch
   Buf part[3], dt[3];             // per-path outlier split-K partials and folded Dt
-  int or_kk = 0;                  // wgrad OE-Right product fused into G_Y's quant pass (0: not planned)
+  int or_kk = 0;                  // the wgrad's outlier product fused into a quant pass (0: not planned)
+  int or_t = -1;                  // the streamed tensor: G_Y (OE-Right) or X (OE-Left, layer call only)
   Buf or_part, or_ticket;         // its per-(band, CTA) partials; the GEMM pre-fold's CTA count
   int splits[3];
   int64_t npad[3], mbig[3];
@@ -671,13 +678,19 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
     take(L->part[path], size_t(L->splits[path]) * size_t(L->mbig[path]) * size_t(L->npad[path]) * 4, false);
     take(L->dt[path], size_t(kk) * size_t(L->mbig[path]) * 4, false);
   }
-  // wgrad OE-Right (A = G_Y^T, B_out = X[:, S]): the product A B_out accumulates in G_Y's quant
-  // pass when G_Y is quantised in both orientations there ("fuses ... into a single kernel")
-  if (or_fusion_enabled() && s[2] == ADAHOP_OE_RIGHT_IHT && p->oe_k > 0 && L->kk_col[0] > 0 &&
-      L->need_row[2] && L->need_col[2]) {
-    const size_t b = quant_tc_or_part_bytes(T, d_out, L->kk_col[0], sms);
+  // The wgrad's outlier product accumulates in a quant pass that streams its big operand anyway
+  // ("fuses ... into a single kernel"), when that tensor is quantised in both orientations:
+  //   OE-Right (A = G_Y^T, B_out = X[:, S]): G_Y's pass, slice = X's columns S;
+  //   OE-Left (A_out = G_Y[:, S]^T, B = X): X's pass, slice = G_Y's columns S — only when X and G_Y
+  //   share the launch (the layer call; the split backward has no X pass and uses the BF16 GEMM).
+  const bool right = s[2] == ADAHOP_OE_RIGHT_IHT, left = s[2] == ADAHOP_OE_LEFT_IHT;
+  const int ot = right ? 2 : 0, st_ = right ? 0 : 2;   // streamed tensor, slice's tensor
+  if (or_fusion_enabled() && (right || (left && !split && or_left_enabled())) && p->oe_k > 0 && L->kk_col[st_] > 0 &&
+      L->need_row[ot] && L->need_col[ot]) {
+    const size_t b = quant_tc_or_part_bytes(L->R[ot], L->C[ot], L->kk_col[st_], sms);
     if (b > 0) {
-      L->or_kk = L->kk_col[0];
+      L->or_kk = L->kk_col[st_];
+      L->or_t = ot;
       take(L->or_part, b, false);
       take(L->or_ticket, 4, false);
     }
@@ -767,9 +780,11 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
         L.kk_col[t] ? sp.p<const int32_t>(L.idx_col[t]) : nullptr, L.kk_col[t],
         L.kk_col[t] ? sp.p<__nv_bfloat16>(L.slice_col[t]) : nullptr, sp.p<uint8_t>(L.q_col[t]), sp.p<uint8_t>(L.sf_col[t]),
         nullptr};
-    if (t == 2 && L.or_kk > 0) {
+    // OE-Right's slice (X's columns) is in this call or the saved context; OE-Left's (G_Y's columns)
+    // is gathered before this launch when G_Y is in it
+    if (t == L.or_t && L.or_kk > 0 && (t == 2 || (phases & tensor_phase(2)))) {
       QuantTcJob& q = tc_jobs[n_tc - 1];
-      q.or_slice = sp.p<const __nv_bfloat16>(L.slice_col[0]);
+      q.or_slice = sp.p<const __nv_bfloat16>(L.slice_col[2 - t]);
       q.or_kk = L.or_kk;
       q.or_part = sp.p<float>(L.or_part);
       q.or_part_bytes = quant_tc_or_part_bytes(R, C, L.or_kk, sms);
@@ -830,8 +845,8 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
     const int kk = col ? L.kk_col[t] : L.kk_row[t];
     const int32_t* idx = sp.p<const int32_t>(col ? L.idx_col[t] : L.idx_row[t]);
     if (path == 2 && or_fused) {   // the quant pass left the product's partials; the epilogue sums them
-      patch[path] = quant_tc_or_patch(T, d_out, kk, sms, sp.p<const float>(L.or_part), sp.p<unsigned>(L.or_ticket),
-                                      sp.p<float>(L.dt[path]), idx);
+      patch[path] = quant_tc_or_patch(L.R[L.or_t], L.C[L.or_t], kk, sms, sp.p<const float>(L.or_part),
+                                      sp.p<unsigned>(L.or_ticket), sp.p<float>(L.dt[path]), idx, left ? 2 : 1);
       continue;
     }
     const __nv_bfloat16* slice = sp.p<const __nv_bfloat16>(col ? L.slice_col[t] : L.slice_row[t]);

@@ -95,8 +95,8 @@ __device__ __forceinline__ void epi_store_rows128(uint8_t* stg, const uint32_t (
 // product is exactly 0 there and those entries of C are the BF16 outlier product alone:
 //   OE-Right (mode 1): C[m][idx[j]] = Dt[j][m]       OE-Left (mode 2): C[idx[j]][n] = Dt[j][n]
 // with Dt the split-K-folded, transposed outlier product (launch_outlier_fold). With `ticket`
-// (mode 1, the product fused into the quant pass, quant_tc.cu) Dt is first folded by the GEMM's
-// own epilogue threads from the quant pass's per-(band, CTA) partials, in CTA order:
+// (the wgrad product fused into the quant pass, quant_tc.cu) Dt is first folded by the GEMM's own
+// epilogue threads from the quant pass's per-(band, CTA) partials, in CTA order:
 //   Dt[j][m] = sum_s part[m / 128][s][j][m % 128],  s < the band's slot count,
 // each CTA a disjoint share while its first main loop runs; every CTA then counts itself in on
 // `ticket` (zeroed by the quant pass) and the first patch waits for all of them (the persistent
@@ -156,7 +156,8 @@ __device__ __forceinline__ void oe_prefold_wait(const OePatch& op) {
   }
   __syncwarp();
 }
-// Dt values written in this kernel (pre-fold) are read through L2, never the non-coherent path
+// Dt[j][m] (m: the row of C for OE-Right, its column for OE-Left); values written in this kernel
+// (pre-fold) are read through L2, never the non-coherent path
 __device__ __forceinline__ float oe_patch_value(const OePatch& op, int j, int64_t m) {
   return op.ticket ? __ldcg(op.Dt + int64_t(j) * op.Mb + m) : __ldg(op.Dt + int64_t(j) * op.Mb + m);
 }
@@ -210,7 +211,7 @@ __device__ __forceinline__ void epi_patch_outliers(uint8_t* stg, const OePatch& 
       for (int c = lane; c < ncols; c += 32) {
         const int64_t n = n0 + c;
         if (n >= N) continue;
-        const float v = __ldg(op.Dt + int64_t(j) * op.Mb + n);
+        const float v = oe_patch_value(op, j, n);
         uint8_t* dst = stg + epi_stage_off<kSw128>(rl, c * elt);
         if (elt == 4) *reinterpret_cast<float*>(dst) = v;
         else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);

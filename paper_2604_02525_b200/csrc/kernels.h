@@ -101,7 +101,7 @@ struct QuantTcJob {
   const __nv_bfloat16* in; int64_t R, C, ld;
   const int32_t* row_zero; int nrow_zero; __nv_bfloat16* slice_row; uint8_t* q_row; uint8_t* sf_row; float* had_row;
   const int32_t* col_zero; int ncol_zero; __nv_bfloat16* slice_col; uint8_t* q_col; uint8_t* sf_col; float* had_col;
-  // optional fused outlier product of this tensor (OE-Right wgrad, eq:oe_right P:280):
+  // optional fused outlier product of this tensor (the wgrad's, eq:oe_right P:280 / eq:oe_left P:273):
   // P[j][c] = sum_r T[r][c] or_slice[j][r] for j < or_kk (<= 64), c < C, left as per-(band, CTA)
   // partials in or_part (quant_tc_or_part_bytes bytes) that quant_tc_or_patch describes to the
   // MXFP4 GEMM epilogue; or_slice [or_kk][R] bf16 must be complete before the launch
@@ -116,7 +116,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cu
                                   bool* or_fused);
 size_t quant_tc_or_part_bytes(int64_t R, int64_t C, int kk, int num_sms);
 OePatch quant_tc_or_patch(int64_t R, int64_t C, int kk, int num_sms, const float* part, unsigned* ticket, float* Dt,
-                          const int32_t* idx);
+                          const int32_t* idx, int mode);
 cudaError_t launch_quant_tc(const __nv_bfloat16* in, int64_t R, int64_t C, int64_t ld, const int32_t* row_zero,
                             int nrow_zero, __nv_bfloat16* slice_row, uint8_t* q_row, uint8_t* sf_row, float* had_row,
                             const int32_t* col_zero, int ncol_zero, __nv_bfloat16* slice_col, uint8_t* q_col,

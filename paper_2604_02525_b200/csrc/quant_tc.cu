@@ -181,7 +181,8 @@ __device__ __forceinline__ void quant_block(const uint32_t (&d)[32], uint4& code
 // tiles, then job 1's, ...) that CTA b visits with stride gridDim.x, row bands first (ct fastest):
 // concurrent CTAs stream whole row bands, so the bf16 reads are long contiguous runs.
 //
-// Fused outlier product (OE-Right wgrad, eq:oe_right P:280 with A = G_Y^T, B_out = X[:, S]):
+// Fused outlier product of the wgrad (eq:oe_right P:280 with A = G_Y^T, B_out = X[:, S]: T = G_Y,
+// S = X's column slice; eq:oe_left P:273 with A_out = G_Y[:, S]^T, B = X: T = X, S = G_Y's):
 //   P[c][j] = sum_r T[r][c] * S[j][r]     (T = the streamed tensor [R x C], S = the slice [kk][R])
 // The last job of the launch may carry it (Jobs::orr). Its tiles are visited after the plain ones,
 // column band by column band (rt fastest), in contiguous chunks: OR-chunk b (of min(n, SMs)) goes
@@ -663,9 +664,9 @@ static qtc::OrSpec or_spec(int64_t R, int64_t C, int kk, int num_sms) {
   return o;
 }
 OePatch quant_tc_or_patch(int64_t R, int64_t C, int kk, int num_sms, const float* part, unsigned* ticket, float* Dt,
-                          const int32_t* idx) {
+                          const int32_t* idx, int mode) {
   const qtc::OrSpec o = or_spec(R, C, kk, num_sms);
-  OePatch p{Dt, idx, C, kk, 1};
+  OePatch p{Dt, idx, C, kk, mode};
   p.part = part;
   p.ticket = ticket;
   p.spb = o.spb;
