@@ -451,7 +451,7 @@ LAYER_STRATS = [("IHT", "IHT", "OE_RIGHT_IHT"), ("IHT", "OE_LEFT_IHT", "OE_LEFT_
                 ("BF16", "BF16", "IHT")]
 
 
-@pytest.mark.parametrize("shape", [(640, 384, 256), (544, 352, 224)])
+@pytest.mark.parametrize("shape", [(640, 384, 256), (544, 352, 224), (512, 160, 96)])
 @pytest.mark.parametrize("strats", LAYER_STRATS)
 def test_linear_layer_matches_paths_and_oracle(strats, shape):
     T, d_in, d_out = shape
