@@ -265,7 +265,7 @@ def config_dict(args, world):
             "api": "adahop_linear_* per path" if args.per_path else "adahop_linear_layer (dual-orientation quant)",
             "tokens_per_gpu": args.tokens, "global_tokens": args.tokens * world,
             "pairs": "CN NN RN RC NC CC (Table-1 census classes)", "oe_k": args.oe_k,
-            "level": args.level, "hadamard_block": 32, "out_dtype": "bf16",
+            "level": args.level, "hadamard_block": 32, "out_dtype": "bf16 (Y, G_X), fp32 (G_W)",
             "l2": "flushed between steps (256 MiB write, untimed)",
             "parallelism": f"dp{world} token-sharded, NCCL all-reduce of wgrad" if world > 1 else "single GPU"}
 
@@ -933,6 +933,7 @@ def library_fp4(gemms, args, l2, as_graph, timed, dev):
                 "ms_per_step": ms_lib, "TFLOP_s": flops / (ms_lib * 1e-3) / 1e12,
                 "ours_gemm_only_ms_per_step": ms_ours, "ours_gemm_only_TFLOP_s": flops / (ms_ours * 1e-3) / 1e12,
                 "ours_over_library": ms_lib / ms_ours,
+                "ours_gemm_only_frac": flops / (ms_ours * 1e-3) / 1e12 / (load_peaks()["bf16"] * 4.0),
                 "note": "the step's MXFP4 GEMM shapes and output dtypes; ours = k_gemm_mxf4_2sm alone (no outlier patch)"}
     except Exception as e:  # noqa: BLE001  (reported, not fatal: context only)
         return {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
