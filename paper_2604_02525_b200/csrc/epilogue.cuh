@@ -1,9 +1,10 @@
-// epilogue.cuh — coalesced GEMM epilogue store through a per-warp shared-memory stage.
+// epilogue.cuh — GEMM epilogue stores through a per-warp shared-memory stage, and the OE patch.
 //
 // After tcgen05.ld (32x32b) lane i of an epilogue warp holds one accumulator ROW. Storing
 // that directly makes every warp store touch 32 rows (32 L1 wavefronts per instruction);
-// instead each lane writes its 128-byte row segment into a padded smem stage and the warp
-// re-reads it so that 8 consecutive lanes write one full 128-byte line of C.
+// instead each lane writes its 128-byte row segment into a stage: a 128B-swizzled box that one
+// TMA tensor store writes out (the pair GEMM), or a padded stage that the warp re-reads so
+// that 8 consecutive lanes write one full 128-byte line of C (the LSU path).
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>

@@ -10,7 +10,10 @@
 //
 // Roles (384 threads per CTA): warp 0 TMA producer (both CTAs; completion is signalled on
 // the leader's barrier), warp 1 MMA issuer (leader only), warp 2 TMEM allocator, warps 4..11
-// epilogue (2 warps per TMEM lane quadrant, each owning half of the columns).
+// epilogue (2 warps per TMEM lane quadrant, each owning half of the columns). The epilogue
+// drains TMEM, hands the accumulator back, writes each warp's 32 rows x 128 bytes into a
+// 128B-swizzled box in shared memory, patches the outlier entries there and stores
+// the box with one TMA tensor store (LSU stores through a padded stage when C is unaligned).
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"

@@ -15,12 +15,15 @@
 //   the column quantisation (stored rows = the C columns, K = R)  — kCol,
 // each with its own OE mask (extracted rows / columns become zero blocks: codes 0, scale
 // 0x7F) and raw bf16 slice. Tiles of 128 x 128 arrive by TMA (two 128B-swizzled 64-column
-// boxes) in a 4-stage ring. Per tile the MMA warp issues, per 32-block, M=128 x N=32 x K=32:
+// boxes, issued by two producer lanes) in a 4-stage ring. Per tile the MMA warp issues, per
+// 32-block, M=128 x N=32 x K=32:
 //   row blocks: A = the tile's 32-column slice, K-major;
 //   column blocks: A = the transposed 32-row slice, MN-major (the same smem bytes);
 // B = H_32 (K-major, in smem). Accumulators (double-buffered, 2 x 256 TMEM columns) are
-// drained by 8 epilogue warps: 4 for row blocks (TMEM lane = tile row), 4 for column blocks
-// (TMEM lane = tile column).
+// drained by 16 epilogue warps: 8 for row blocks (TMEM lane = tile row), 8 for column blocks
+// (TMEM lane = tile column). With the fused wgrad outlier product (kOr, see "Fused outlier
+// product" below) the ring is 3 stages deep, the Hadamard accumulator single-buffered and a
+// product accumulator occupies TMEM columns [256, 256 + npad).
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
