@@ -92,6 +92,12 @@ int gemm_variant() {
   static const int v = knob("ADAHOP_GEMM_VARIANT", 256);
   return v;
 }
+// ADAHOP_GEMM_SPLITK (experiment builds): 0 = 256x128 tiles instead of split-K clusters,
+// 2 / 4 = that many pairs per cluster whenever the split applies
+int gemm_splitk() {
+  static const int v = knob("ADAHOP_GEMM_SPLITK", 1);
+  return v;
+}
 
 cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
   int v = gemm_variant();
@@ -100,7 +106,19 @@ cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
   // wgrad, 512 x 2048, K = 16384): the 256x128 double-buffered tiles keep twice as many pairs
   // busy (27 -> 22 us measured)
   const int64_t tiles256 = ((a.M + 255) / 256) * ((a.N + 255) / 256);
-  if (v == 256 && a.K >= 8192 && 2 * tiles256 < sms / 2) v = 128;
+  if (v == 256 && a.K >= 8192 && 2 * tiles256 < sms / 2) {
+    // split-K over clusters of 4 (or 2) pairs, one 256x256 tile per cluster, partials summed in
+    // distributed shared memory (e.g. 16 tiles x 4 pairs: 64 of the 74 pairs busy)
+    const int force = gemm_splitk();
+    if (force != 0)
+      for (int split = 4; split >= 2; split /= 2) {
+        if (force > 1 ? split != force : split * tiles256 > sms / 2) continue;
+        bool launched = false;
+        const cudaError_t e = launch_gemm_mxf4_2sm_split(a, sms, split, st, &launched);
+        if (e != cudaSuccess || launched) return e;
+      }
+    v = 128;
+  }
   return launch_gemm_mxf4_2sm(a, sms, v, st);
 }
 
@@ -557,10 +575,14 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
     ga.B = slice; ga.b_mn = 0; ga.ldb = K;
     ga.Mb = g.mbig; ga.Nb = g.kk; ga.K = K; ga.mode = 1;
     ga.part = reinterpret_cast<float*>(w + g.part); ga.splits = g.splits; ga.npad = g.npad;
-    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
     float* Dt = reinterpret_cast<float*>(w + g.dt);
-    ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, g.kk, Dt, cs));
-    launches += 2;
+    ga.Dt = Dt;   // one K range: the GEMM writes Dt itself
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    launches += 1;
+    if (ga.splits > 1) {
+      ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, g.kk, Dt, cs));
+      launches += 1;
+    }
     patch = OePatch{Dt, idx, ga.Mb, g.kk, oe_right ? 1 : 2};
   }
   stage_mark(3, cs);
@@ -856,10 +878,14 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
     ga.B = slice; ga.b_mn = 0; ga.ldb = MNK[path][2];
     ga.Mb = L.mbig[path]; ga.Nb = kk; ga.K = MNK[path][2]; ga.mode = 1;
     ga.part = sp.p<float>(L.part[path]); ga.splits = L.splits[path]; ga.npad = L.npad[path];
-    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
     float* Dt = sp.p<float>(L.dt[path]);
-    ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, kk, Dt, cs));
-    launches += 2;
+    ga.Dt = Dt;   // one K range: the GEMM writes Dt itself
+    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    launches += 1;
+    if (ga.splits > 1) {
+      ADAHOP_LAUNCH(launch_outlier_fold(ga.part, ga.splits, ga.Mb, ga.npad, kk, Dt, cs));
+      launches += 1;
+    }
     patch[path] = OePatch{Dt, idx, ga.Mb, kk, left ? 2 : 1};
   }
   stage_mark(3, cs);

@@ -33,7 +33,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n, int a_mn, int b_
          | (uint32_t(m >> 4) << 24);
 }
 
-template <int BN>
+template <int BN, bool kDeep = false>
 struct Cfg {
   static constexpr int kABytes = BM * BK * 2;  // 16 KB
   static constexpr int kBBytes = BN * BK * 2;
@@ -41,7 +41,8 @@ struct Cfg {
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
   // skinny outlier tiles (BN <= 64): 3 stages so that two CTAs share an SM (the split-K grid is
   // sized for two per SM); wider tiles: 4 stages, one CTA per SM
-  static constexpr int kStages = BN <= 64 ? 3 : kStagesMax;
+  // kDeep (one short K range per CTA, the direct-Dt outlier product): every k-step in flight at once
+  static constexpr int kStages = kDeep ? 8 : (BN <= 64 ? 3 : kStagesMax);
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 4 * kEpiStageBytes + 1024 + 256;
 };
 
@@ -65,12 +66,12 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn, int j) {
             : ptx::make_sdesc(base + j * 32, 16, 1024, 2);      // K-major: 32 bytes along K
 }
 
-template <int BN>
+template <int BN, bool kDeep = false>
 __global__ void __launch_bounds__(kThreads)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                 int a_mn, int b_mn, int64_t Mb, int64_t Nb, int64_t K, int mode, void* C,
-                int out_f32, int64_t ldc, float* part, int64_t npad) {
-  using G = Cfg<BN>;
+                int out_f32, int64_t ldc, float* part, int64_t npad, float* Dt) {
+  using G = Cfg<BN, kDeep>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   constexpr int kStages = G::kStages;
@@ -189,6 +190,14 @@ __global__ void __launch_bounds__(kThreads)
         w[16 + i] = pack_bf16x2(r1[2 * i], r1[2 * i + 1]);
       }
     }
+    if (mode == 1 && Dt != nullptr) {
+      // one K range (no split): lane = row m, register v = column j -> Dt[j][m], 128-byte runs
+      const int64_t m = mw + lane;
+#pragma unroll
+      for (int v = 0; v < 32; ++v)
+        if (m < Mb && nc + v < Nb) Dt[(nc + v) * Mb + m] = __uint_as_float(r0[v]);
+      continue;
+    }
     const int64_t nrem = ncols - nc;
     const int bytes_valid = int(nrem >= cols_per_grp ? 128 : (nrem > 0 ? nrem * elt : 0));
     if (rows_valid > 0 && bytes_valid > 0)
@@ -252,6 +261,9 @@ int64_t bf16_gemm_npad(int64_t Nb) {
 int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms) {
   const int64_t mt = (Mb + bf16g::BM - 1) / bf16g::BM;
   const int64_t nks = (K + bf16g::BK - 1) / bf16g::BK;
+  // short K (the dgrad OE-Left product over d_out, e.g. 64 x 512 x 2048): one K range per CTA,
+  // whose epilogue writes Dt itself — split-K would add the partial round trip and a fold launch
+  if (nks <= 16) return 1;
   int64_t s = (2 * num_sms) / mt;            // one full wave of ~2 CTAs per SM
   if (s > nks) s = nks;
   if (s > 32) s = 32;
@@ -259,9 +271,9 @@ int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms) {
   return int(s);
 }
 
-template <int BN>
+template <int BN, bool kDeep = false>
 static cudaError_t launch_bn(const Bf16GemmArgs& a, cudaStream_t st) {
-  using G = bf16g::Cfg<BN>;
+  using G = bf16g::Cfg<BN, kDeep>;
   CUtensorMap tma, tmb;
   // A: K-major [Mb][K] (box {64, 128}) or MN-major [K][Mb] (box {64, 64})
   if (!a.a_mn) {
@@ -285,18 +297,26 @@ static cudaError_t launch_bn(const Bf16GemmArgs& a, cudaStream_t st) {
   }
   static std::atomic<uint64_t> attr{0};
   cudaError_t ae = once_per_device(attr, [] {
-    return cudaFuncSetAttribute(bf16g::k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+    return cudaFuncSetAttribute(bf16g::k_gemm_bf16<BN, kDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
   });
   if (ae != cudaSuccess) return ae;
   const int splits = a.mode == 1 ? a.splits : 1;
   dim3 grid(unsigned((a.Mb + bf16g::BM - 1) / bf16g::BM),
             unsigned(a.mode == 1 ? 1 : (a.Nb + BN - 1) / BN), unsigned(splits));
-  return launch_k(bf16g::k_gemm_bf16<BN>, grid, dim3(bf16g::kThreads), G::kSmem, st, 1, tma, tmb, a.a_mn, a.b_mn,
-                  a.Mb, a.Nb, a.K, a.mode, a.C, a.out_f32 ? 1 : 0, a.ldc, a.part, a.npad);
+  return launch_k(bf16g::k_gemm_bf16<BN, kDeep>, grid, dim3(bf16g::kThreads), G::kSmem, st, 1, tma, tmb, a.a_mn, a.b_mn,
+                  a.Mb, a.Nb, a.K, a.mode, a.C, a.out_f32 ? 1 : 0, a.ldc, a.part, a.npad,
+                  a.mode == 1 && splits == 1 ? a.Dt : nullptr);
 }
 
 cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st) {
   if (a.mode == 0) return launch_bn<128>(a, st);
+  if (a.splits == 1 && a.Dt != nullptr && (a.K + bf16g::BK - 1) / bf16g::BK <= 8) {
+    switch (a.npad) {   // direct Dt, short K: the CTA's whole K range in flight
+      case 32: return launch_bn<32, true>(a, st);
+      case 64: return launch_bn<64, true>(a, st);   // 8 x 24 KB stages
+      default: break;
+    }
+  }
   switch (a.npad) {
     case 32: return launch_bn<32>(a, st);
     case 64: return launch_bn<64>(a, st);

@@ -93,7 +93,16 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t 
 // one cluster row (same pm) read the same A rows and the pairs in one cluster column the same
 // B rows, so each CTA loads 1/PN of its A box and 1/PM of its B box and multicasts them to the
 // CTAs that share them — the L2->SM operand traffic per flop drops by (1/PN + 1/PM)/2 ... 1.
-template <int BN, int BUFS, int PM, int PN>
+//
+// SPLIT > 1 (long-K GEMMs with fewer output tiles than CTA pairs, e.g. the Llama-3.2-1B k / v
+// wgrad: 16 tiles of 512 x 2048 over K = 16384): a cluster of SPLIT pairs computes ONE tile,
+// pair p over the K range [p nks / SPLIT, (p + 1) nks / SPLIT). Once every pair's MMAs are
+// complete (cluster barrier: the operand rings are idle), each CTA pushes column slice c of its
+// partial from TMEM into the ring of CTA (c, x) with remote shared-memory stores; after a second
+// cluster barrier CTA (p, x) sums its slice over the SPLIT partials in pair order 0, 1, ...
+// (deterministic, no workspace), patches and stores it. 512 x 2048 x 16384: 20.7 us with 2 pairs
+// per cluster vs 23.8 us for 256 x 128 tiles (profiles/r02as_gemm_splitk.txt).
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
@@ -112,9 +121,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tovl + 1);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  constexpr int NP = PM * PN, CS = 2 * NP;
+  static_assert(SPLIT == 1 || (PM == 1 && PN == 1 && BN == 256 && BUFS == 1), "split-K: single pairs, 256 x 256");
+  constexpr int NP = PM * PN, CS = 2 * NP * SPLIT;
   const uint32_t rank = ptx::cluster_ctarank();
-  const uint32_t x = rank & 1, pp = rank >> 1, pm = pp / PN, pn = pp % PN;
+  const uint32_t ksp = SPLIT > 1 ? rank >> 1 : 0u;   // this pair's K range (split-K)
+  const uint32_t x = rank & 1, pp = SPLIT > 1 ? 0u : rank >> 1, pm = pp / PN, pn = pp % PN;
   const bool leader = x == 0;
   const uint32_t leader_rank = rank & ~1u;
   const int64_t mblocks = (M + 255) / 256;
@@ -122,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t smblocks = (mblocks + PM - 1) / PM, snblocks = (nblocks + PN - 1) / PN;
   const int64_t ntiles = smblocks * snblocks;
   const int nks = int((K + BK - 1) / BK);
+  const int kb = int(int64_t(nks) * ksp / SPLIT), ke = int(int64_t(nks) * (ksp + 1) / SPLIT);
   const int64_t cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
   // multicast groups: the CTAs with this x and pm (A rows) / this x and pn (B rows)
   uint16_t mask_a = 0, mask_b = 0;
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // blocks past the edge of a ragged super tile are computed on clamped (valid) data
       // and never stored: every pair must still take part in the multicasts and commits
       const int64_t mb = min(smb * PM + pm, mblocks - 1), nb = min(snb * PN + pn, nblocks - 1);
-      for (int ks = 0; ks < nks; ++ks) {
+      for (int ks = kb; ks < ke; ++ks) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + size_t(stage) * G::kStage;
         uint8_t* sb = sa + G::kA;
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       GT(0, lt);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * G::kAccCols;
-      for (int ks = 0; ks < nks; ++ks) {
+      for (int ks = kb; ks < ke; ++ks) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const bool issuer = ptx::elect_one();
@@ -245,10 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((GEMM_ABLATE & 2) || !issuer) continue;
           ptx::mma_mxf4_2sm(d_tmem, ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2),
                             ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2), id, sfa_t, sfb_t,
-                            (ks > 0 || j > 0) ? 1u : 0u);
+                            (ks > kb || j > 0) ? 1u : 0u);
         }
         if (issuer) {
-          if (NP == 1) ptx::tc_commit_2sm(&empty[stage]);
+          if (SPLIT > 1) ptx::tc_commit_2sm_mask(&empty[stage], uint16_t(3u << leader_rank));
+          else if (NP == 1) ptx::tc_commit_2sm(&empty[stage]);
           else ptx::tc_commit_2sm_mask(&empty[stage], mask_all);   // every CTA fed by this pair's loads
         }
         __syncwarp();
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     oe_prefold(oe, int(threadIdx.x) - 128, kEpiWarps * 32, 1);
     oe_prefold_wait(oe);
     int64_t lt = 0;
-    for (int64_t tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
+    for (int64_t tile = cluster; tile < ntiles && SPLIT == 1; tile += nclusters, ++lt) {
       int64_t smb, snb;
       tile_coords(tile, smblocks, snblocks, smb, snb);
       const int64_t mb = smb * PM + pm, nb = snb * PN + pn;   // past the edge: rows/cols invalid, no stores
@@ -434,6 +447,110 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tma_c && lane == 0) ptx::bulk_wait_group<0>();   // this warp's stores are complete
     __syncwarp();
   }
+  if (SPLIT > 1) {
+    // Split-K reduction. Column group cg (32 columns) of the tile belongs to pair cg / kGrp; pair p's
+    // partial of it goes to slot p of the owner CTA's receive buffer (its idle ring):
+    //   recv[((p kGrp + cg % kGrp) 8 + j) 128 + row] = 16-byte chunk j of row `row`,
+    // remote stores from TMEM-loaded registers (fire-and-forget), a warp's store = 512 contiguous
+    // bytes. The owner then sums its slots in pair order 0, 1, ... (deterministic).
+    constexpr int kGrp = 8 / SPLIT;   // 32-column groups per owner
+    if (warp >= 4) {
+      ptx::mbar_wait(&tfull[0], 0);
+      if (warp == 4 && lane == 0) GT(2, 0);
+      ptx::tc_fence_after();
+    }
+    ptx::cluster_sync();   // every pair's MMAs are complete: the operand rings are free
+    if (warp >= 4 && cluster < ntiles) {
+      const uint32_t q = warp & 3, half = (warp - 4) >> 2;
+      const uint32_t row = q * 32 + lane;
+#pragma unroll 1
+      for (int g = 0; g < 4; ++g) {
+        const int cg = int(half) * 4 + g;
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + cg * 32, r);
+        ptx::tmem_ld_wait();
+        const uint32_t dst = ptx::mapa(smem, uint32_t(2 * (cg / kGrp)) + x) +
+                             ((uint32_t(ksp * kGrp + cg % kGrp) * 8) * 128 + row) * 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ptx::st_shared_cluster_v4(dst + j * 2048, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+      }
+      ptx::tc_fence_before();
+      if (warp == 4 && lane == 0) GT(3, 0);
+    }
+    ptx::cluster_sync();   // the partials are delivered (release / acquire)
+    if (warp >= 4 && cluster < ntiles) {
+      // CTA (ksp, x) owns tile columns [ksp 256 / SPLIT, (ksp + 1) 256 / SPLIT) of its 128 rows
+      const uint32_t q = warp & 3, half = (warp - 4) >> 2;
+      uint8_t* stg = epi_smem + (warp - 4) * (tma_c ? 4096 : G::kEpiBufs * kEpiStageBytes);
+      const int elt = out_f32 ? 4 : 2;
+      const int cpu = 128 / elt;                       // columns per unit (one 128-byte row segment)
+      const int units = (BN / SPLIT) / cpu;
+      const bool vec_ok = ((reinterpret_cast<uintptr_t>(C) | uintptr_t(ldc * elt)) & 15) == 0;
+      int64_t smb, snb;
+      tile_coords(cluster, smblocks, snblocks, smb, snb);
+      const int64_t m0 = smb * 256 + x * 128 + q * 32;
+      const int rows_valid = int(M - m0 < 32 ? (M - m0 > 0 ? M - m0 : 0) : 32);
+      const uint32_t row = q * 32 + lane;
+      const uint4* recv = reinterpret_cast<const uint4*>(smem);
+#pragma unroll 1
+      for (int u = int(half); u < units; u += 2) {
+        uint32_t w[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {   // 32-column groups of the unit (1 for fp32, 2 for bf16)
+          if (h == 1 && out_f32) break;
+          const int lg = u * (cpu / 32) + h;
+          float acc[32];
+#pragma unroll
+          for (int p = 0; p < SPLIT; ++p) {
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = recv[((p * kGrp + lg) * 8 + j) * 128 + row];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float f[4] = {__uint_as_float(v[j].x), __uint_as_float(v[j].y), __uint_as_float(v[j].z),
+                                  __uint_as_float(v[j].w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[4 * j + e] = p == 0 ? f[e] : acc[4 * j + e] + f[e];
+            }
+          }
+          if (out_f32) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(acc[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[16 * h + i] = pack_bf16x2(__float_as_uint(acc[2 * i]), __float_as_uint(acc[2 * i + 1]));
+          }
+        }
+        const int64_t n0 = snb * BN + int64_t(ksp) * (BN / SPLIT) + u * cpu;
+        const int64_t nrem = N - n0;
+        const int bytes_valid = int(nrem >= cpu ? 128 : (nrem > 0 ? nrem * elt : 0));
+        if (rows_valid <= 0 || bytes_valid <= 0) continue;
+        if (tma_c) {
+          if (lane == 0) ptx::bulk_wait_group_read<0>();
+          __syncwarp();
+          epi_stage_sw128(stg, w);
+          __syncwarp();
+          epi_patch_outliers<true>(stg, oe, m0, n0, cpu, elt, M, N);
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::bulk_commit_group();
+          }
+          __syncwarp();
+        } else {
+          epi_stage_only128(stg, w);
+          epi_patch_outliers(stg, oe, m0, n0, cpu, elt, M, N);
+          epi_flush128(stg, static_cast<char*>(C) + (m0 * ldc + n0) * elt, ldc * elt, rows_valid, bytes_valid, elt,
+                       vec_ok);
+          __syncwarp();
+        }
+      }
+      if (tma_c && lane == 0) ptx::bulk_wait_group<0>();
+      __syncwarp();
+      if (warp == 4 && lane == 0) GT(4, 0);
+    }
+  }
   ptx::tc_fence_before();
   ptx::cluster_sync();
   if (warp == 2) {
@@ -458,11 +575,11 @@ static bool tma_store_enabled() {
   return v != 0;
 }
 
-template <int BN, int BUFS, int PM, int PN>
-static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st) {
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
+static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st, bool* fits = nullptr) {
   using G = mxf4x2::Cfg<BN, BUFS>;
-  constexpr int CS = 2 * PM * PN;
-  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN>;
+  constexpr int CS = 2 * PM * PN * SPLIT;
+  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN, SPLIT>;
   CUtensorMap tma, tmb, tsfa, tsfb;
   const int64_t kch = sf_kchunks(a.K);
   if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
@@ -516,7 +633,13 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
     cached.v[dev].store(n, std::memory_order_relaxed);
   }
   const int64_t tiles = ((a.M + 256 * PM - 1) / (256 * PM)) * ((a.N + BN * PN - 1) / (BN * PN));
-  const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  if (SPLIT > 1) {
+    // one tile per cluster, all co-resident (the outlier pre-fold counts every CTA in)
+    if (fits) *fits = (tiles <= max_clusters || knob("ADAHOP_GEMM_SPLITK", 1) > 1) &&
+                      (a.K + mxf4x2::BK - 1) / mxf4x2::BK >= SPLIT;
+    if (fits && !*fits) return cudaSuccess;
+  }
+  const int64_t clusters = SPLIT > 1 || tiles < max_clusters ? tiles : max_clusters;
   return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
                   tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
 }
@@ -547,6 +670,18 @@ cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant
   // where the early MMA start competes with the output stores (profiles/r02c_gemm_overlap_ab.txt)
   if (a.K >= 4096) return launch_2sm<256, 2, 1, 1>(a, num_sms, st);
   return launch_2sm<256, 1, 1, 1>(a, num_sms, st);
+}
+
+// Split-K over clusters of `split` pairs (2 or 4). *launched = false (and nothing launched) when
+// the shape's clusters cannot all be co-resident or K has fewer than `split` k-steps.
+cudaError_t launch_gemm_mxf4_2sm_split(const Mxf4GemmArgs& a, int num_sms, int split, cudaStream_t st,
+                                       bool* launched) {
+  *launched = false;
+  cudaError_t e = split == 4   ? launch_2sm<256, 1, 1, 1, 4>(a, num_sms, st, launched)
+                  : split == 2 ? launch_2sm<256, 1, 1, 1, 2>(a, num_sms, st, launched)
+                               : cudaErrorInvalidValue;
+  if (e != cudaSuccess) *launched = false;
+  return e;
 }
 
 }  // namespace adahop

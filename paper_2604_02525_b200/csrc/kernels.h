@@ -186,6 +186,9 @@ cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st
 // gemm_mxf4_2sm.cu — CTA-pair (cta_group::2) version; variant = 128 (256x128 tiles, double-
 // buffered accumulators) or 256 (256x256 tiles, single accumulator).
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st);
+// split-K over clusters of `split` CTA pairs for long-K GEMMs with few output tiles
+cudaError_t launch_gemm_mxf4_2sm_split(const Mxf4GemmArgs& a, int num_sms, int split, cudaStream_t st,
+                                       bool* launched);
 
 // gemm_bf16.cu — D[Mb x Nb] = A[Mb x K] B[Nb x K]^T in BF16 (fp32 accumulate).
 // A/B are K-major (a_mn = 0: A[m*lda + k]) or MN-major (a_mn = 1: A[k*lda + m]).
@@ -206,6 +209,7 @@ struct Bf16GemmArgs {
   float* part;
   int splits;
   int64_t npad;
+  float* Dt = nullptr;   // mode 1 with splits == 1: the transposed product Dt[j][m] written directly (no fold)
 };
 int64_t bf16_gemm_npad(int64_t Nb);
 int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms);

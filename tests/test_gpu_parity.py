@@ -310,7 +310,10 @@ def test_gemm_mxf4_one_hot_layout():
         assert len(nz) <= 1
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 128, 256), (300, 200, 544), (128, 384, 2048), (1000, 520, 1024)])
+# the last three: long K with few 256 x 256 tiles -> split-K clusters (4 pairs: 8 and 6 ragged
+# tiles; 2 pairs: 24 tiles), partials summed across the cluster in distributed shared memory
+@pytest.mark.parametrize("M,N,K", [(256, 128, 256), (300, 200, 544), (128, 384, 2048), (1000, 520, 1024),
+                                   (512, 1024, 8192), (300, 700, 8192), (768, 2048, 8192)])
 @pytest.mark.parametrize("out", ["f32", "bf16"])
 def test_gemm_mxf4_random_vs_oracle(M, N, K, out):
     rng = np.random.default_rng(M + N + K)
@@ -350,6 +353,27 @@ def test_adahop_gemm_vs_oracle(strategy, a_ks, b_ks):
         idx = parts["idx"]
         sel = got[idx, :] if strategy == "OE_LEFT_IHT" else got[:, idx]
         # disjoint support: the extracted rows/cols carry exactly the BF16 outlier product
+        assert rel_fro(sel, parts["c_out"]) <= 1e-5
+
+
+@pytest.mark.parametrize("strategy", ["IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT"])
+def test_adahop_gemm_splitk_vs_oracle(strategy):
+    """Long-K GEMM with 4 output tiles: split-K over a cluster of 4 pairs; the outlier entries
+    are patched by the CTA that sums their column slice."""
+    M, N, K, k = 512, 384, 8192, 16
+    a, _ = synth.operand(M, K, "R", "X", case_id=33, count=4)
+    b, _ = synth.operand(N, K, "R", "W", case_id=34, count=3)
+    p = ah.Params(oe_k=k)
+    c = ah.gemm(dev_bf16(a), 0, dev_bf16(b), 0, M, N, K, strategy, p, out_dtype=torch.float32)
+    c2 = ah.gemm(dev_bf16(a), 0, dev_bf16(b), 0, M, N, K, strategy, p, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref, parts = O.adahop_matmul(a, b, strategy, k=k, return_parts=True)
+    got = c.cpu().numpy()
+    assert rel_fro(got, ref) <= TOL_OUT
+    np.testing.assert_array_equal(c2.cpu().numpy().view(np.uint32), got.view(np.uint32))   # fixed-order sum
+    if strategy != "IHT":
+        idx = parts["idx"]
+        sel = got[idx, :] if strategy == "OE_LEFT_IHT" else got[:, idx]
         assert rel_fro(sel, parts["c_out"]) <= 1e-5
 
 
