@@ -219,10 +219,15 @@ def test_quant_dual_bf16_extreme_magnitudes_production_path():
 @pytest.mark.parametrize("k_strided", [False, True])
 @pytest.mark.parametrize("R,K,k,probe", [(5000, 128, 64, 64), (300, 96, 8, 64), (2048, 64, 256, 64),
                                           (4100, 256, 16, 32), (50, 32, 64, 64), (16384, 512, 64, 64),
-                                          (16384, 64, 256, 64)])
+                                          (16384, 64, 256, 64), (32768, 64, 256, 64), (9000, 160, 64, 96),
+                                          (7, 64, 64, 64)])
 def test_foid_index_sets_bitexact(R, K, k, probe, k_strided):
+    # 32768 rows: 8 select blocks and their merge; probe 96 > 64 takes the generic key path;
+    # R = 7 < k clamps; a key tie across select blocks
     x, planted = synth.operand(R, K, "R", "X", case_id=R + k, count=min(5, R))
-    x[10] = x[11]                                  # an exact key tie
+    x[min(10, R - 1)] = x[min(11, R - 2)]          # an exact key tie
+    if R > 8192:
+        x[R - 3] = x[5]                            # a tie across the cluster's CTAs
     xin = x.T.copy() if k_strided else x
     idx, keys = ah.debug_foid(dev_bf16(xin), k=k, probe=probe, k_strided=k_strided)
     want_keys = O.foid_keys(x, probe)
