@@ -14,6 +14,10 @@
 // drains TMEM, hands the accumulator back, writes each warp's 32 rows x 128 bytes into a
 // 128B-swizzled box in shared memory, patches the outlier entries there and stores
 // the box with one TMA tensor store (LSU stores through a padded stage when C is unaligned).
+// The CTA's 16 box stores are paced across the next tile's main loop (one per 30 x min(nks, 16)
+// cycles; the last tile at once): issued as one 64-KB burst they stall the operand loads queued
+// behind them (CTA-0 trace: main loop of a K = 2048 tile 3.9k cycles without stores, 5.2k with a
+// burst, 4.3k paced; profiles/r02ax..r02bb).
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -77,6 +81,10 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
 }
 
 constexpr int64_t kGroupM = 8;  // grouped rasterisation (see gemm_mxf4.cu)
+#ifndef GEMM_PACE_MAX_STEPS
+#define GEMM_PACE_MAX_STEPS 16
+#endif
+constexpr int kPaceMaxSteps = GEMM_PACE_MAX_STEPS;   // store pacing scales with K up to this many k-steps
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t nblocks, int64_t& mb,
                                             int64_t& nb) {
   const int64_t per_group = kGroupM * nblocks;
@@ -107,7 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
                     const __grid_constant__ CUtensorMap tm_c, int tma_c,
-                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe) {
+                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe,
+                    int pace) {
   using G = Cfg<BN, BUFS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
@@ -354,8 +363,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (warp == 4 && lane == 0) GT(4, lt);
           continue;
         }
+        // Paced stores: the CTA's 16 box stores (8 warps x 2) go out one every pace x min(nks, 16)
+        // cycles after the drain, spread over the next tile's main loop instead of one 64-KB burst
+        // (a burst stalls the operand loads behind it: profiles/r02ay_gemm_store_pacing.txt)
+        // (the CTA's last tile stores at once: its stores are the kernel's tail)
+        const long long t_drained = clock64();
+        const long long slot = (long long)pace * (nks < kPaceMaxSteps ? nks : kPaceMaxSteps);
+        const bool paced = pace > 0 && tile + nclusters < ntiles;
 #pragma unroll 1
         for (int g = 0; g < 2 && tma_c; ++g) {
+          if (paced) {
+            const long long target = t_drained + (long long)(g * 8 + int(warp) - 4) * slot;
+            while (clock64() < target) __nanosleep(32);
+          }
           // the previous TMA store has read the stage; stage, patch, then one bulk tensor store
           if (lane == 0) ptx::bulk_wait_group_read<0>();
           __syncwarp();
@@ -569,6 +589,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace mxf4x2
 
+// Epilogue store pacing (cycles per k-step between a CTA's box stores; experiment builds:
+// ADAHOP_GEMM_PACE, 0 = one burst after the drain). 30 measured best on the 1B / 8B layer GEMMs:
+// GEMMs alone 752 -> 712 us (1B), 2284 -> 2141 us (8B) (profiles/r02bb_gemm_store_pacing.txt)
+constexpr int kStorePace = 30;
+
 // ADAHOP_GEMM_TMA_STORE=0 (experiment builds): the epilogue's LSU stores instead of TMA stores
 static bool tma_store_enabled() {
   static const int v = knob("ADAHOP_GEMM_TMA_STORE", 1);
@@ -641,7 +666,8 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   }
   const int64_t clusters = SPLIT > 1 || tiles < max_clusters ? tiles : max_clusters;
   return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
-                  tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe);
+                  tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe,
+                  knob("ADAHOP_GEMM_PACE", kStorePace));   // cycles per k-step between box stores (0: burst)
 }
 
 #if ADAHOP_EXPERIMENTS
