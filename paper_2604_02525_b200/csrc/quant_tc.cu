@@ -47,7 +47,7 @@
 #endif
 #if QTC_TRACE
 #include <cstdio>
-__device__ long long g_qtc_trace[5][64];
+__device__ long long g_qtc_trace[6][64];
 #define QTC_T(k, lt) do { if (blockIdx.x == 0 && (lt) < 64) g_qtc_trace[k][lt] = clock64(); } while (0)
 #else
 #define QTC_T(k, lt) do { } while (0)
@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         }
         ptx::bulk_commit_group();
         ptx::bulk_wait_group_read<0>();
+        QTC_T(5, lt);
         ptx::mbar_arrive(&stgfree[buf]);
       }
       __syncwarp();
@@ -616,9 +617,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     TileRef t;
     TileCursor cur(J);
     for (int i = 0; i < 64 && cur.next(J, t); ++i)
-      printf("qtc tile %2d: tma %7lld tempty %7lld full %7lld epi %7lld drained %7lld\n", i,
+      printf("qtc tile %2d: tma %7lld tempty %7lld full %7lld epi %7lld drained %7lld stored %7lld\n", i,
              g_qtc_trace[0][i] - t0, g_qtc_trace[1][i] - t0, g_qtc_trace[2][i] - t0, g_qtc_trace[3][i] - t0,
-             g_qtc_trace[4][i] - t0);
+             g_qtc_trace[4][i] - t0, g_qtc_trace[5][i] - t0);
   }
 #endif
 }
