@@ -97,13 +97,18 @@ def test_iht_quant_residual_mask(k_strided):
 
 
 @pytest.mark.parametrize("R,C,masks", [(256, 512, False), (384, 160, True), (2048, 1024, True),
-                                        (4096, 96, True), (256, 384, "dense")])
+                                        (4096, 96, True), (256, 384, "dense"), (544, 2048, "wide"),
+                                        (96, 1056, "wide")])
 def test_quant_dual_equals_single_orientation(R, C, masks):
     # one pass over T emitting both layouts == the row quantisation of T and of T^T, bitwise,
     # and both == the oracle quantiser on the Hadamard output (protocol (a)); "dense" puts more
-    # extracted rows + columns in one tile than the kernel's slice staging ring holds
+    # extracted rows + columns in one tile than the kernel's slice staging ring holds; "wide"
+    # (>= C / 128 extracted columns: a slice over most of every row's lines, ragged 256-column chunks)
     x, _ = synth.operand(R, C, "R", "X", case_id=R * 7 + C, bf16=True)
-    if masks == "dense":
+    if masks == "wide":
+        g = np.random.default_rng(R + C)
+        rz, cz = sorted({0, R // 3, R - 1}), sorted(g.choice(C, size=max(C // 32, 9), replace=False).tolist())
+    elif masks == "dense":
         rz, cz = list(range(0, R, 2)), list(range(0, C, 3))
     else:
         rz = sorted({0, 3, R // 2, R - 1}) if masks else None
