@@ -122,6 +122,14 @@ cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
   return launch_gemm_mxf4_2sm(a, sms, v, st);
 }
 
+// The full BF16 product (Lv2 CC): CTA pairs with 256 x 256 tiles, else the 1-CTA kernel.
+cudaError_t run_gemm_bf16_full(const Bf16GemmArgs& a, int sms, cudaStream_t st) {
+  bool launched = false;
+  const cudaError_t e = launch_gemm_bf16_2sm(a, sms, st, &launched);
+  if (e != cudaSuccess || launched) return e;
+  return launch_gemm_bf16(a, st);
+}
+
 // ---------------------------------------------------------------------- workspace carving
 struct Carver {
   size_t off = 0;
@@ -521,7 +529,7 @@ adahop_status_t adahop_gemm(const void* A, int32_t a_kstrided, int64_t lda, cons
     ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = C; ga.out_f32 = out_f32; ga.ldc = ldc;
     stage_mark(1, cs);
     stage_mark(2, cs);
-    ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+    ADAHOP_LAUNCH(run_gemm_bf16_full(ga, dev.sms, cs));
     stage_mark(3, cs);
     stage_mark(4, cs);
     g_launches = 1;
@@ -899,7 +907,7 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
       ga.A = static_cast<const __nv_bfloat16*>(rawA[path]); ga.a_mn = rawAks[path]; ga.lda = rawAld[path];
       ga.B = static_cast<const __nv_bfloat16*>(rawB[path]); ga.b_mn = rawBks[path]; ga.ldb = rawBld[path];
       ga.Mb = M; ga.Nb = N; ga.K = K; ga.mode = 0; ga.C = out[path]; ga.out_f32 = f32; ga.ldc = ldc[path];
-      ADAHOP_LAUNCH(launch_gemm_bf16(ga, cs));
+      ADAHOP_LAUNCH(run_gemm_bf16_full(ga, sms, cs));
       launches += 1;
       continue;
     }

@@ -55,12 +55,16 @@ constexpr int kEpiWarps = 8;
 // drains the shared 32 columns first and releases them on `tovl`: the next tile's MMAs start
 // after ~1/8 of the drain instead of after all of it. BN = 256, BUFS = 1: the single-accumulator
 // layout (experiment builds: ADAHOP_GEMM_OVL=0).
-template <int BN, int BUFS>
+// KIND 0: block-scaled MXFP4 (a stage = 256 fp4 of K); KIND 1: BF16 (kind::f16, a stage = 64 bf16
+// of K, A / B K-major or MN-major, no scale factors) — the Lv2 CC product and any plain
+// BF16 GEMM of the path; both stage 128 bytes of K per operand row.
+template <int BN, int BUFS, int KIND = 0>
 struct Cfg {
   static constexpr int kA = 128 * BK / 2;             // 16 KB: this CTA's 128 rows of A
   static constexpr int kB = (BN / 2) * BK / 2;        // this CTA's BN/2 rows of B
-  static constexpr int kSfa = 1024;                   // 128 rows x 8 K-blocks
-  static constexpr int kSfb = (BN / 128) * 1024;      // all BN rows (duplicated in both CTAs)
+  static constexpr int kSfa = KIND ? 0 : 1024;        // 128 rows x 8 K-blocks
+  static constexpr int kSfb = KIND ? 0 : (BN / 128) * 1024;   // all BN rows (duplicated in both CTAs)
+  static constexpr int kKStep = KIND ? 64 : BK;       // K elements per stage
   static constexpr int kStage = kA + kB + kSfa + kSfb;
   static constexpr int kStages = BN == 256 ? 5 : 7;
   static constexpr int kEpiBufs = 1;
@@ -76,6 +80,11 @@ struct Cfg {
   static_assert(kSfbCol + 2 * (BN / 32) * (kSfSets == 2 ? 2 : 1) <= 512 || kSfSets == 2, "TMEM overflow");
 };
 
+// kind::f16 instruction descriptor: D f32, A / B bf16, major-ness per operand (0 K, 1 MN)
+__host__ __device__ constexpr uint32_t bf16_idesc(int m, int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
   return (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(m >> 4) << 24);
 }
@@ -110,15 +119,17 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t 
 // cluster barrier CTA (p, x) sums its slice over the SPLIT partials in pair order 0, 1, ...
 // (deterministic, no workspace), patches and stores it. 512 x 2048 x 16384: 20.7 us with 2 pairs
 // per cluster vs 23.8 us for 256 x 128 tiles (profiles/r02as_gemm_splitk.txt).
-template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1, int KIND = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
                     const __grid_constant__ CUtensorMap tm_c, int tma_c,
                     void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe,
-                    int pace) {
-  using G = Cfg<BN, BUFS>;
+                    int pace, int a_mn, int b_mn) {
+  using G = Cfg<BN, BUFS, KIND>;
+  static_assert(KIND == 0 || (PM == 1 && PN == 1 && SPLIT == 1), "BF16: single pairs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint32_t pace_t0[kEpiWarps];   // epilogue store pacing: each warp's drain time
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* epi_smem = smem + size_t(G::kStages) * G::kStage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kEpiWarps * G::kEpiBufs * kEpiStageBytes);
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t nblocks = (N + BN - 1) / BN;
   const int64_t smblocks = (mblocks + PM - 1) / PM, snblocks = (nblocks + PN - 1) / PN;
   const int64_t ntiles = smblocks * snblocks;
-  const int nks = int((K + BK - 1) / BK);
+  const int nks = int((K + G::kKStep - 1) / G::kKStep);
   const int kb = int(int64_t(nks) * ksp / SPLIT), ke = int(int64_t(nks) * (ksp + 1) / SPLIT);
   const int64_t cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
   // multicast groups: the CTAs with this x and pm (A rows) / this x and pn (B rows)
@@ -195,7 +206,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t fb = ptx::mapa(&full[stage], leader_rank);
         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], ((GEMM_ABLATE & 4) ? 0 : 2 * (G::kSfa + G::kSfb)) +
                                                                ((GEMM_ABLATE & 16) ? 0 : 2 * (G::kA + G::kB)));
-        if (GEMM_ABLATE & 16) {
+        if (KIND == 1) {
+          // BF16: K-major boxes {64 k, rows}; MN-major boxes {64 mn, 64 k} stacked every 8 KB
+          const int32_t ma = int32_t(mb * 256 + x * 128), nbb = int32_t(nb * BN + x * (BN / 2));
+          if (!a_mn) ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * 64, ma);
+          else
+            for (int b = 0; b < 2; ++b) ptx::tma_load_2d_2sm(sa + b * 8192, &tm_a, fb, ma + b * 64, ks * 64);
+          if (!b_mn) ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * 64, nbb);
+          else
+            for (int b = 0; b < BN / 128; ++b) ptx::tma_load_2d_2sm(sb + b * 8192, &tm_b, fb, nbb + b * 64, ks * 64);
+        } else if (GEMM_ABLATE & 16) {
         } else if (PN == 1) {
           ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + x * 128));
         } else {
@@ -203,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_load_2d_2sm_mc(sa + pn * sub * 128, &tm_a, &full[stage], ks * (BK / 2),
                                   int32_t(mb * 256 + x * 128 + pn * sub), mask_a);
         }
-        if (GEMM_ABLATE & 16) {
+        if (KIND == 1 || (GEMM_ABLATE & 16)) {
         } else if (PM == 1) {
           ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + x * (BN / 2)));
         } else {
@@ -211,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_load_2d_2sm_mc(sb + pm * sub * 128, &tm_b, &full[stage], ks * (BK / 2),
                                   int32_t(nb * BN + x * (BN / 2) + pm * sub), mask_b);
         }
-        if (!(GEMM_ABLATE & 4)) {
+        if (KIND == 0 && !(GEMM_ABLATE & 4)) {
           ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + x));
           ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
         }
@@ -222,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // whole warp: waits and descriptor math stay warp-uniform (uniform registers); one elected
     // lane issues the tcgen05 operations
     // ------------------------------------------------------------ MMA issuer (leader)
-    constexpr uint32_t idesc = make_idesc(256, BN);
+    const uint32_t idesc = KIND ? bf16_idesc(256, BN, a_mn, b_mn) : make_idesc(256, BN);
     int stage = 0;
     uint32_t phase = 0;
     int64_t lt = 0;
@@ -246,9 +266,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // scale factors alternate between two TMEM column sets by k-step parity, so the copies
         // for step ks+1 do not overwrite columns the MMAs of step ks still read
         const uint32_t sfo = G::kSfSets == 2 ? uint32_t(ks & 1) * G::kSfSet : 0u;
+        if (KIND == 1) {
+          const uint32_t a_addr = ptx::smem_u32(sa), b_addr = ptx::smem_u32(sb);
+#pragma unroll
+          for (int j = 0; j < 4 && issuer; ++j)   // K = 16 per MMA
+            ptx::mma_bf16_2sm(d_tmem,
+                              a_mn ? ptx::make_sdesc(a_addr + j * 2048, 8192, 1024, 2) : ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2),
+                              b_mn ? ptx::make_sdesc(b_addr + j * 2048, 8192, 1024, 2) : ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2),
+                              idesc, (ks > kb || j > 0) ? 1u : 0u);
+        }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          if ((GEMM_ABLATE & 1) || !issuer) break;
+          if (KIND == 1 || (GEMM_ABLATE & 1) || !issuer) break;
           ptx::tmem_cp_32x128b_warpx4_2sm(tmem_base + G::kSfaCol + sfo + 4 * c,
                                           ptx::make_sdesc(ptx::smem_u32(ssfa + c * 512), 0, 128, 0));
 #pragma unroll
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sfa_t = (tmem_base + G::kSfaCol + sfo + 4 * (j >> 1)) | (sf_id << 30);
           const uint32_t sfb_t = (tmem_base + G::kSfbCol + sfo + (BN / 32) * (j >> 1)) | (sf_id << 30);
           const uint32_t id = idesc | (sf_id << 4) | (sf_id << 29);
-          if ((GEMM_ABLATE & 2) || !issuer) continue;
+          if (KIND == 1 || (GEMM_ABLATE & 2) || !issuer) continue;
           ptx::mma_mxf4_2sm(d_tmem, ptx::make_sdesc(a_addr + j * 32, 16, 1024, 2),
                             ptx::make_sdesc(b_addr + j * 32, 16, 1024, 2), id, sfa_t, sfb_t,
                             (ks > kb || j > 0) ? 1u : 0u);
@@ -367,14 +396,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // cycles after the drain, spread over the next tile's main loop instead of one 64-KB burst
         // (a burst stalls the operand loads behind it: profiles/r02ay_gemm_store_pacing.txt)
         // (the CTA's last tile stores at once: its stores are the kernel's tail)
-        const long long t_drained = clock64();
-        const long long slot = (long long)pace * (nks < kPaceMaxSteps ? nks : kPaceMaxSteps);
+        // (32-bit cycle arithmetic: the spread is far below 2^31 cycles; the drain time is parked in
+        // shared memory so that it does not hold a register across the packed accumulator values)
         const bool paced = pace > 0 && tile + nclusters < ntiles;
+        if (paced && lane == 0) pace_t0[warp - 4] = uint32_t(clock());
 #pragma unroll 1
         for (int g = 0; g < 2 && tma_c; ++g) {
           if (paced) {
-            const long long target = t_drained + (long long)(g * 8 + int(warp) - 4) * slot;
-            while (clock64() < target) __nanosleep(32);
+            const uint32_t wait =
+                uint32_t(g * 8 + int(warp) - 4) * uint32_t(pace) * uint32_t(nks < kPaceMaxSteps ? nks : kPaceMaxSteps);
+            __syncwarp();
+            const uint32_t t0 = *static_cast<volatile uint32_t*>(&pace_t0[warp - 4]);
+            while (uint32_t(clock()) - t0 < wait) __nanosleep(32);
           }
           // the previous TMA store has read the stage; stage, patch, then one bulk tensor store
           if (lane == 0) ptx::bulk_wait_group_read<0>();
@@ -604,7 +637,7 @@ template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
 static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st, bool* fits = nullptr) {
   using G = mxf4x2::Cfg<BN, BUFS>;
   constexpr int CS = 2 * PM * PN * SPLIT;
-  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN, SPLIT>;
+  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN, SPLIT, 0>;
   CUtensorMap tma, tmb, tsfa, tsfb;
   const int64_t kch = sf_kchunks(a.K);
   if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
@@ -667,7 +700,7 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
   const int64_t clusters = SPLIT > 1 || tiles < max_clusters ? tiles : max_clusters;
   return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
                   tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe,
-                  knob("ADAHOP_GEMM_PACE", kStorePace));   // cycles per k-step between box stores (0: burst)
+                  knob("ADAHOP_GEMM_PACE", kStorePace), 0, 0);   // pace: cycles per k-step between box stores (0: burst)
 }
 
 #if ADAHOP_EXPERIMENTS
@@ -696,6 +729,72 @@ cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant
   // where the early MMA start competes with the output stores (profiles/r02c_gemm_overlap_ab.txt)
   if (a.K >= 4096) return launch_2sm<256, 2, 1, 1>(a, num_sms, st);
   return launch_2sm<256, 1, 1, 1>(a, num_sms, st);
+}
+
+// BF16 C = A . B on CTA pairs (KIND 1): 256 x 256 tiles, kind::f16 with M = 256, operands K-major
+// or MN-major as the Lv2 CC product and the dgrad / wgrad views need them (the 1-CTA 128 x 128
+// k_gemm_bf16 reads 64 KB of shared memory per 2 MFLOP and is shared-memory bound at ~half
+// the BF16 rate). *launched = false when the shape is not worth a pair (M <= 128).
+template <int BUFS>
+static cudaError_t launch_bf16_2sm_t(const Bf16GemmArgs& a, int num_sms, cudaStream_t st) {
+  using G = mxf4x2::Cfg<256, BUFS, 1>;
+  auto kern = mxf4x2::k_gemm_mxf4_2sm<256, BUFS, 1, 1, 1, 1>;
+  CUtensorMap tma, tmb, tmc;
+  // A: K-major [M][K] (box {64, 128}) or MN-major [K][M] (box {64 mn, 64 k})
+  if (!(a.a_mn ? make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.A, uint64_t(a.Mb), uint64_t(a.K),
+                              uint64_t(a.lda) * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)
+               : make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.A, uint64_t(a.K), uint64_t(a.Mb),
+                              uint64_t(a.lda) * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return cudaErrorInvalidValue;
+  if (!(a.b_mn ? make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.B, uint64_t(a.Nb), uint64_t(a.K),
+                              uint64_t(a.ldb) * 2, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)
+               : make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.B, uint64_t(a.K), uint64_t(a.Nb),
+                              uint64_t(a.ldb) * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return cudaErrorInvalidValue;
+  const int elt = a.out_f32 ? 4 : 2;
+  int tma_c = tma_store_enabled() && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ((a.ldc * elt) % 16) == 0 &&
+              make_tmap_2d(&tmc, a.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.C,
+                           uint64_t(a.Nb), uint64_t(a.Mb), uint64_t(a.ldc) * elt, uint32_t(128 / elt), 32,
+                           CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  if (!tma_c) memset(&tmc, 0, sizeof(tmc));
+  static std::atomic<uint64_t> attr{0};
+  static PerDeviceInt cached;
+  cudaError_t ae = once_per_device(attr, [&kern] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+  });
+  if (ae != cudaSuccess) return ae;
+  const int dev = current_device();
+  int max_clusters = cached.v[dev].load(std::memory_order_relaxed);
+  if (max_clusters <= 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * (num_sms / 2)));
+    cfg.blockDim = dim3(mxf4x2::kThreads);
+    cfg.dynamicSmemBytes = G::kSmem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = num_sms / 2;
+    max_clusters = n;
+    cached.v[dev].store(n, std::memory_order_relaxed);
+  }
+  const int64_t tiles = ((a.Mb + 255) / 256) * ((a.Nb + 255) / 256);
+  const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  const OePatch none{};
+  return launch_k(kern, dim3(unsigned(2 * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, 2, tma, tmb, tma, tmb,
+                  tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.Mb, a.Nb, a.K, none,
+                  knob("ADAHOP_GEMM_PACE", kStorePace), a.a_mn, a.b_mn);
+}
+
+cudaError_t launch_gemm_bf16_2sm(const Bf16GemmArgs& a, int num_sms, cudaStream_t st, bool* launched) {
+  *launched = false;
+  if (a.mode != 0 || a.Mb <= 128 || knob("ADAHOP_BF16_2SM", 1) == 0) return cudaSuccess;
+  *launched = true;
+  return a.K >= 4096 ? launch_bf16_2sm_t<2>(a, num_sms, st) : launch_bf16_2sm_t<1>(a, num_sms, st);
 }
 
 // Split-K over clusters of `split` pairs (2 or 4). *launched = false (and nothing launched) when

@@ -211,6 +211,9 @@ struct Bf16GemmArgs {
   int64_t npad;
   float* Dt = nullptr;   // mode 1 with splits == 1: the transposed product Dt[j][m] written directly (no fold)
 };
+// the full BF16 product (mode 0) on CTA pairs; *launched = false: use launch_gemm_bf16
+cudaError_t launch_gemm_bf16_2sm(const Bf16GemmArgs& a, int num_sms, cudaStream_t st, bool* launched);
+
 int64_t bf16_gemm_npad(int64_t Nb);
 int bf16_gemm_splits(int64_t Mb, int64_t K, int num_sms);
 cudaError_t launch_gemm_bf16(const Bf16GemmArgs& a, cudaStream_t st);

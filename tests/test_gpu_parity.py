@@ -366,6 +366,24 @@ def test_adahop_gemm_vs_oracle(strategy, a_ks, b_ks):
         assert rel_fro(sel, parts["c_out"]) <= 1e-5
 
 
+@pytest.mark.parametrize("a_ks,b_ks", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(640, 520, 4128), (288, 1000, 544)])
+def test_adahop_gemm_bf16_pair_kernel_vs_oracle(M, N, K, a_ks, b_ks):
+    """The Lv2 CC product (P:300) on CTA pairs (kind::f16, M = 256 tiles; K >= 4096: overlapping
+    accumulators): K-major and MN-major operands, ragged M / N / K, bf16 = RN(fp32) output."""
+    a, _ = synth.operand(M, K, "C", "X", case_id=M + K + a_ks, count=3)
+    b, _ = synth.operand(N, K, "C", "W", case_id=N + K + b_ks, count=3)
+    ta = dev_bf16(a.T.copy() if a_ks else a)
+    tb = dev_bf16(b.T.copy() if b_ks else b)
+    c = ah.gemm(ta, a_ks, tb, b_ks, M, N, K, "BF16", out_dtype=torch.float32)
+    cb16 = ah.gemm(ta, a_ks, tb, b_ks, M, N, K, "BF16", out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    ref = O.adahop_matmul(a, b, "BF16")
+    got = c.cpu().numpy()
+    assert rel_fro(got, ref) <= 1e-5   # bf16 operands exact, fp32 accumulation
+    np.testing.assert_array_equal(cb16.float().cpu().numpy(), O.round_bf16(got).astype(np.float32))
+
+
 @pytest.mark.parametrize("strategy", ["IHT", "OE_LEFT_IHT", "OE_RIGHT_IHT"])
 def test_adahop_gemm_splitk_vs_oracle(strategy):
     """Long-K GEMM with 4 output tiles: split-K over a cluster of 4 pairs; the outlier entries
