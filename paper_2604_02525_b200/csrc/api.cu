@@ -122,6 +122,14 @@ cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
   return launch_gemm_mxf4_2sm(a, sms, v, st);
 }
 
+// Grouped launch of a linear's MXFP4 GEMMs when their total work is small (<= 0.8 TFLOP) and the
+// launcher's rule accepts it (one problem starving the machine; launch_gemm_mxf4_2sm_group).
+// Experiment builds: ADAHOP_GEMM_GROUP = 0 never, 2 = any size.
+bool group_gemms(double flops) {
+  static const int v = knob("ADAHOP_GEMM_GROUP", 1);
+  return v == 2 || (v == 1 && flops <= 0.8e12);
+}
+
 // The full BF16 product (Lv2 CC): CTA pairs with 256 x 256 tiles, else the 1-CTA kernel.
 cudaError_t run_gemm_bf16_full(const Bf16GemmArgs& a, int sms, cudaStream_t st) {
   bool launched = false;
@@ -898,6 +906,8 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
   }
   stage_mark(3, cs);
   // ---- 4. the MXFP4 GEMMs (or BF16 for Lv2 CC); the epilogue writes the outlier entries
+  Mxf4GemmArgs group[3];
+  int ng = 0;
   for (int path = 0; path < 3; ++path) {
     if (!(path_phase(path) & phases)) continue;
     const int64_t M = MNK[path][0], N = MNK[path][1], K = MNK[path][2];
@@ -917,8 +927,26 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
     const uint8_t* qb = sp.p<const uint8_t>(kPathBo[path] ? L.q_col[tb] : L.q_row[tb]);
     const uint8_t* qb_sf = sp.p<const uint8_t>(kPathBo[path] ? L.sf_col[tb] : L.sf_row[tb]);
     Mxf4GemmArgs ma{qa, qa_sf, qb, qb_sf, out[path], f32, ldc[path], M, N, K, patch[path]};
-    ADAHOP_LAUNCH(run_gemm_mxf4(ma, sms, cs));
-    launches += 1;
+    group[ng++] = ma;
+  }
+  // A small linear's GEMMs share one persistent launch (clusters split by work); large ones, and
+  // any with M <= 128 (the 1-CTA kernel), keep their own launches
+  double flops = 0;
+  bool pairs_ok = true;
+  for (int i = 0; i < ng; ++i) {
+    flops += 2.0 * double(group[i].M) * double(group[i].N) * double(group[i].K);
+    pairs_ok &= group[i].M > 128;
+  }
+  bool grouped = false;
+  if (ng >= 2 && pairs_ok && group_gemms(flops)) {
+    ADAHOP_LAUNCH(launch_gemm_mxf4_2sm_group(group, ng, sms, cs, &grouped));
+    if (grouped) launches += 1;
+  }
+  if (!grouped) {
+    for (int i = 0; i < ng; ++i) {
+      ADAHOP_LAUNCH(run_gemm_mxf4(group[i], sms, cs));
+      launches += 1;
+    }
   }
   stage_mark(4, cs);
   g_launches = launches;

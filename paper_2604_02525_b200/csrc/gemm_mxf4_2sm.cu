@@ -119,14 +119,53 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mblocks, int64_t 
 // cluster barrier CTA (p, x) sums its slice over the SPLIT partials in pair order 0, 1, ...
 // (deterministic, no workspace), patches and stores it. 512 x 2048 x 16384: 20.7 us with 2 pairs
 // per cluster vs 23.8 us for 256 x 128 tiles (profiles/r02as_gemm_splitk.txt).
-template <int BN, int BUFS, int PM, int PN, int SPLIT = 1, int KIND = 0>
+//
+// Grouped launch (GemmGroup, n > 1): the three GEMMs of one linear (fwd, dgrad, wgrad) in ONE
+// persistent launch. Problem 0 comes in the kernel's own parameters, problems 1..n-1 in `grp`;
+// problem p owns clusters [cl[p], cl[p+1]) (sized on the host in proportion to its work) and
+// every CTA of such a cluster walks only that problem's tiles, so each CTA keeps one problem for
+// its lifetime. The small linears' GEMMs each fill the machine for a wave or two at most (fill,
+// tail, the output writes); side by side they overlap.
+struct GemmExtra {
+  CUtensorMap tm_a, tm_b, tm_sfa, tm_sfb, tm_c;
+  void* C;
+  int64_t ldc, M, N, K;
+  OePatch oe;
+  int out_f32, tma_c;
+};
+constexpr int kGroupMax = 3;
+struct GemmGroup {
+  GemmExtra q[kGroupMax - 1];
+  int n;
+  int cl[kGroupMax + 1];
+};
+
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1, int KIND = 0, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                    const __grid_constant__ CUtensorMap tm_sfa, const __grid_constant__ CUtensorMap tm_sfb,
-                    const __grid_constant__ CUtensorMap tm_c, int tma_c,
-                    void* C, int out_f32, int64_t ldc, int64_t M, int64_t N, int64_t K, const OePatch oe,
-                    int pace, int a_mn, int b_mn) {
+    k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_b0,
+                    const __grid_constant__ CUtensorMap tm_sfa0, const __grid_constant__ CUtensorMap tm_sfb0,
+                    const __grid_constant__ CUtensorMap tm_c0, int tma_c0,
+                    void* C0, int out_f320, int64_t ldc0, int64_t M0, int64_t N0, int64_t K0, const OePatch oe0,
+                    int pace, int a_mn, int b_mn, const __grid_constant__ GemmGroup grp) {
   using G = Cfg<BN, BUFS, KIND>;
+  // this CTA's problem (one per cluster range) and its parameters
+  static_assert(!kGroup || (PM == 1 && PN == 1 && SPLIT == 1), "grouped launches: single pairs");
+  int pi = 0;
+  if (kGroup) {
+    const int64_t cluster_g = blockIdx.x / 2;
+    while (pi + 1 < grp.n && cluster_g >= grp.cl[pi + 1]) ++pi;
+  }
+  const GemmExtra* ex = kGroup && pi > 0 ? &grp.q[pi - 1] : nullptr;
+  const CUtensorMap* tm_a = ex ? &ex->tm_a : &tm_a0;
+  const CUtensorMap* tm_b = ex ? &ex->tm_b : &tm_b0;
+  const CUtensorMap* tm_sfa = ex ? &ex->tm_sfa : &tm_sfa0;
+  const CUtensorMap* tm_sfb = ex ? &ex->tm_sfb : &tm_sfb0;
+  const CUtensorMap* tm_c = ex ? &ex->tm_c : &tm_c0;
+  const int tma_c = ex ? ex->tma_c : tma_c0;
+  void* const C = ex ? ex->C : C0;
+  const int out_f32 = ex ? ex->out_f32 : out_f320;
+  const int64_t ldc = ex ? ex->ldc : ldc0, M = ex ? ex->M : M0, N = ex ? ex->N : N0, K = ex ? ex->K : K0;
+  const OePatch& oe = ex ? ex->oe : oe0;
   static_assert(KIND == 0 || (PM == 1 && PN == 1 && SPLIT == 1), "BF16: single pairs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint32_t pace_t0[kEpiWarps];   // epilogue store pacing: each warp's drain time
@@ -154,7 +193,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ntiles = smblocks * snblocks;
   const int nks = int((K + G::kKStep - 1) / G::kKStep);
   const int kb = int(int64_t(nks) * ksp / SPLIT), ke = int(int64_t(nks) * (ksp + 1) / SPLIT);
-  const int64_t cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
+  // cluster index / count within this CTA's problem
+  const int64_t cluster = blockIdx.x / CS - (kGroup ? grp.cl[pi] : 0);
+  const int64_t nclusters = kGroup ? grp.cl[pi + 1] - grp.cl[pi] : gridDim.x / CS;
   // multicast groups: the CTAs with this x and pm (A rows) / this x and pn (B rows)
   uint16_t mask_a = 0, mask_b = 0;
 #pragma unroll
@@ -164,10 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint16_t mask_all = uint16_t((1u << CS) - 1);
 
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tm_a);
-    ptx::prefetch_tmap(&tm_b);
-    ptx::prefetch_tmap(&tm_sfa);
-    ptx::prefetch_tmap(&tm_sfb);
+    ptx::prefetch_tmap(tm_a);
+    ptx::prefetch_tmap(tm_b);
+    ptx::prefetch_tmap(tm_sfa);
+    ptx::prefetch_tmap(tm_sfb);
     for (int s = 0; s < G::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], NP);   // one commit per pair of the cluster
@@ -209,31 +250,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (KIND == 1) {
           // BF16: K-major boxes {64 k, rows}; MN-major boxes {64 mn, 64 k} stacked every 8 KB
           const int32_t ma = int32_t(mb * 256 + x * 128), nbb = int32_t(nb * BN + x * (BN / 2));
-          if (!a_mn) ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * 64, ma);
+          if (!a_mn) ptx::tma_load_2d_2sm(sa, tm_a, fb, ks * 64, ma);
           else
-            for (int b = 0; b < 2; ++b) ptx::tma_load_2d_2sm(sa + b * 8192, &tm_a, fb, ma + b * 64, ks * 64);
-          if (!b_mn) ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * 64, nbb);
+            for (int b = 0; b < 2; ++b) ptx::tma_load_2d_2sm(sa + b * 8192, tm_a, fb, ma + b * 64, ks * 64);
+          if (!b_mn) ptx::tma_load_2d_2sm(sb, tm_b, fb, ks * 64, nbb);
           else
-            for (int b = 0; b < BN / 128; ++b) ptx::tma_load_2d_2sm(sb + b * 8192, &tm_b, fb, nbb + b * 64, ks * 64);
+            for (int b = 0; b < BN / 128; ++b) ptx::tma_load_2d_2sm(sb + b * 8192, tm_b, fb, nbb + b * 64, ks * 64);
         } else if (GEMM_ABLATE & 16) {
         } else if (PN == 1) {
-          ptx::tma_load_2d_2sm(sa, &tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + x * 128));
+          ptx::tma_load_2d_2sm(sa, tm_a, fb, ks * (BK / 2), int32_t(mb * 256 + x * 128));
         } else {
           constexpr int sub = 128 / PN;
-          ptx::tma_load_2d_2sm_mc(sa + pn * sub * 128, &tm_a, &full[stage], ks * (BK / 2),
+          ptx::tma_load_2d_2sm_mc(sa + pn * sub * 128, tm_a, &full[stage], ks * (BK / 2),
                                   int32_t(mb * 256 + x * 128 + pn * sub), mask_a);
         }
         if (KIND == 1 || (GEMM_ABLATE & 16)) {
         } else if (PM == 1) {
-          ptx::tma_load_2d_2sm(sb, &tm_b, fb, ks * (BK / 2), int32_t(nb * BN + x * (BN / 2)));
+          ptx::tma_load_2d_2sm(sb, tm_b, fb, ks * (BK / 2), int32_t(nb * BN + x * (BN / 2)));
         } else {
           constexpr int sub = (BN / 2) / PM;
-          ptx::tma_load_2d_2sm_mc(sb + pm * sub * 128, &tm_b, &full[stage], ks * (BK / 2),
+          ptx::tma_load_2d_2sm_mc(sb + pm * sub * 128, tm_b, &full[stage], ks * (BK / 2),
                                   int32_t(nb * BN + x * (BN / 2) + pm * sub), mask_b);
         }
         if (KIND == 0 && !(GEMM_ABLATE & 4)) {
-          ptx::tma_load_2d_2sm(ssfa, &tm_sfa, fb, ks * 256, int32_t(mb * 2 + x));
-          ptx::tma_load_2d_2sm(ssfb, &tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
+          ptx::tma_load_2d_2sm(ssfa, tm_sfa, fb, ks * 256, int32_t(mb * 2 + x));
+          ptx::tma_load_2d_2sm(ssfb, tm_sfb, fb, ks * 256, int32_t(nb * (BN / 128)));
         }
         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
       }
@@ -321,7 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t empty_leader = ptx::mapa(&tempty[0], leader_rank);
     const uint32_t ovl_leader = ptx::mapa(tovl, leader_rank);
     // fused outlier product: fold this CTA's share of Dt while the first main loop runs
-    oe_prefold(oe, int(threadIdx.x) - 128, kEpiWarps * 32, 1);
+    // (every CTA folds its share of every problem's product: the pre-fold counts the whole grid)
+    oe_prefold(oe0, int(threadIdx.x) - 128, kEpiWarps * 32, 1);
+    if (kGroup)
+      for (int q = 1; q < grp.n; ++q) oe_prefold(grp.q[q - 1].oe, int(threadIdx.x) - 128, kEpiWarps * 32, 1);
     oe_prefold_wait(oe);
     int64_t lt = 0;
     for (int64_t tile = cluster; tile < ntiles && SPLIT == 1; tile += nclusters, ++lt) {
@@ -419,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async();
           __syncwarp();
           if (lane == 0 && rows_valid > 0 && n0 < N && !(GEMM_ABLATE & 8)) {
-            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::tma_store_2d(tm_c, stg, int32_t(n0), int32_t(m0));
             ptx::bulk_commit_group();
           }
         }
@@ -484,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::tma_store_2d(tm_c, stg, int32_t(n0), int32_t(m0));
             ptx::bulk_commit_group();
           }
           __syncwarp();
@@ -587,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&tm_c, stg, int32_t(n0), int32_t(m0));
+            ptx::tma_store_2d(tm_c, stg, int32_t(n0), int32_t(m0));
             ptx::bulk_commit_group();
           }
           __syncwarp();
@@ -633,34 +677,55 @@ static bool tma_store_enabled() {
   return v != 0;
 }
 
-template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
-static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st, bool* fits = nullptr) {
+// Tensor maps of one MXFP4 problem (A / B codes, scale factors, C); tma_c = 0: LSU stores for C.
+template <int BN, int PM, int PN>
+static bool mxf4_maps(const Mxf4GemmArgs& a, CUtensorMap* tma, CUtensorMap* tmb, CUtensorMap* tsfa,
+                      CUtensorMap* tsfb, CUtensorMap* tmc, int* tma_c) {
+  const int64_t kch = sf_kchunks(a.K);
+  if (!make_tmap_2d(tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
+                    uint64_t(a.K / 2), 128, 128 / PN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  if (!make_tmap_2d(tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
+                    uint64_t(a.K / 2), 128, (BN / 2) / PM, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  // scale factors as uint32 rows of one 128-row group: [groups][kch * 128] u32
+  if (!make_tmap_2d(tsfa, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.a_sf, uint64_t(kch * 128), uint64_t((a.M + 127) / 128),
+                    uint64_t(kch * 512), 256, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return false;
+  if (!make_tmap_2d(tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
+                    uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return false;
+  // C by TMA stores (128B-swizzled 32-row boxes) when its rows are 16-byte aligned; else LSU stores
+  const int elt = a.out_f32 ? 4 : 2;
+  *tma_c = tma_store_enabled() && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ((a.ldc * elt) % 16) == 0 &&
+           make_tmap_2d(tmc, a.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.C,
+                        uint64_t(a.N), uint64_t(a.M), uint64_t(a.ldc) * elt, uint32_t(128 / elt), 32,
+                        CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  if (!*tma_c) memset(tmc, 0, sizeof(*tmc));
+  return true;
+}
+
+// n problems (1..kGroupMax; n > 1 only with PM = PN = SPLIT = 1) in one persistent launch.
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1, bool kGroup = false>
+static cudaError_t launch_2sm_n(const Mxf4GemmArgs* a, int n, int num_sms, cudaStream_t st, bool* fits = nullptr,
+                               bool* grouped = nullptr) {
   using G = mxf4x2::Cfg<BN, BUFS>;
   constexpr int CS = 2 * PM * PN * SPLIT;
-  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN, SPLIT, 0>;
-  CUtensorMap tma, tmb, tsfa, tsfb;
-  const int64_t kch = sf_kchunks(a.K);
-  if (!make_tmap_2d(&tma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.a_codes, uint64_t(a.K / 2), uint64_t(a.M),
-                    uint64_t(a.K / 2), 128, 128 / PN, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tmb, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.b_codes, uint64_t(a.K / 2), uint64_t(a.N),
-                    uint64_t(a.K / 2), 128, (BN / 2) / PM, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  // scale factors as uint32 rows of one 128-row group: [groups][kch * 128] u32
-  if (!make_tmap_2d(&tsfa, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.a_sf, uint64_t(kch * 128), uint64_t((a.M + 127) / 128),
-                    uint64_t(kch * 512), 256, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
-    return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tsfb, CU_TENSOR_MAP_DATA_TYPE_UINT32, a.b_sf, uint64_t(kch * 128), uint64_t((a.N + 127) / 128),
-                    uint64_t(kch * 512), 256, BN / 128, CU_TENSOR_MAP_SWIZZLE_NONE))
-    return cudaErrorInvalidValue;
-  // C by TMA stores (128B-swizzled 32-row boxes) when its rows are 16-byte aligned; else LSU stores
-  CUtensorMap tmc;
-  const int elt = a.out_f32 ? 4 : 2;
-  int tma_c = tma_store_enabled() && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ((a.ldc * elt) % 16) == 0 &&
-              make_tmap_2d(&tmc, a.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.C,
-                           uint64_t(a.N), uint64_t(a.M), uint64_t(a.ldc) * elt, uint32_t(128 / elt), 32,
-                           CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
-  if (!tma_c) memset(&tmc, 0, sizeof(tmc));
+  auto kern = mxf4x2::k_gemm_mxf4_2sm<BN, BUFS, PM, PN, SPLIT, 0, kGroup>;
+  if (n < 1 || n > mxf4x2::kGroupMax || (n > 1 && !kGroup)) return cudaErrorInvalidValue;
+  CUtensorMap tma, tmb, tsfa, tsfb, tmc;
+  int tma_c = 0;
+  if (!mxf4_maps<BN, PM, PN>(a[0], &tma, &tmb, &tsfa, &tsfb, &tmc, &tma_c)) return cudaErrorInvalidValue;
+  mxf4x2::GemmGroup grp;
+  memset(&grp, 0, sizeof(grp));
+  grp.n = n;
+  for (int i = 1; i < n; ++i) {
+    mxf4x2::GemmExtra& e = grp.q[i - 1];
+    if (!mxf4_maps<BN, PM, PN>(a[i], &e.tm_a, &e.tm_b, &e.tm_sfa, &e.tm_sfb, &e.tm_c, &e.tma_c))
+      return cudaErrorInvalidValue;
+    e.C = a[i].C; e.ldc = a[i].ldc; e.M = a[i].M; e.N = a[i].N; e.K = a[i].K; e.oe = a[i].oe;
+    e.out_f32 = a[i].out_f32 ? 1 : 0;
+  }
   // resident clusters of this shape (GPC packing decides it for clusters of 4 and 8), per device
   static std::atomic<uint64_t> attr{0};
   static PerDeviceInt cached;
@@ -684,23 +749,74 @@ static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t s
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    int n = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-    if (e != cudaSuccess || n <= 0) n = num_sms / CS;
-    max_clusters = n;
-    cached.v[dev].store(n, std::memory_order_relaxed);
+    int nc = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+    if (e != cudaSuccess || nc <= 0) nc = num_sms / CS;
+    max_clusters = nc;
+    cached.v[dev].store(nc, std::memory_order_relaxed);
   }
-  const int64_t tiles = ((a.M + 256 * PM - 1) / (256 * PM)) * ((a.N + BN * PN - 1) / (BN * PN));
+  int64_t tiles[mxf4x2::kGroupMax];
+  for (int i = 0; i < n; ++i)
+    tiles[i] = ((a[i].M + 256 * PM - 1) / (256 * PM)) * ((a[i].N + BN * PN - 1) / (BN * PN));
   if (SPLIT > 1) {
     // one tile per cluster, all co-resident (the outlier pre-fold counts every CTA in)
-    if (fits) *fits = (tiles <= max_clusters || knob("ADAHOP_GEMM_SPLITK", 1) > 1) &&
-                      (a.K + mxf4x2::BK - 1) / mxf4x2::BK >= SPLIT;
+    if (fits) *fits = (tiles[0] <= max_clusters || knob("ADAHOP_GEMM_SPLITK", 1) > 1) &&
+                      (a[0].K + mxf4x2::BK - 1) / mxf4x2::BK >= SPLIT;
     if (fits && !*fits) return cudaSuccess;
   }
-  const int64_t clusters = SPLIT > 1 || tiles < max_clusters ? tiles : max_clusters;
+  int64_t clusters = 0;
+  if (n == 1) {
+    clusters = SPLIT > 1 || tiles[0] < max_clusters ? tiles[0] : max_clusters;
+    grp.cl[0] = 0;
+    grp.cl[1] = int(clusters);
+  } else {
+    // clusters per problem: greedy on the makespan ceil(tiles / clusters) x (k-steps + ~4 for the
+    // epilogue) — each cluster walks its problem's tiles round-robin, so the slowest cluster of
+    // the slowest problem sets the kernel's time
+    int64_t cost[mxf4x2::kGroupMax], c[mxf4x2::kGroupMax], used = 0;
+    for (int i = 0; i < n; ++i) {
+      cost[i] = (a[i].K + mxf4x2::BK - 1) / mxf4x2::BK + 4;
+      c[i] = 1;
+      ++used;
+    }
+    if (used > max_clusters) return cudaErrorInvalidValue;
+    while (used < max_clusters) {
+      int worst = -1;
+      int64_t wm = 0;
+      for (int i = 0; i < n; ++i) {
+        const int64_t m = (tiles[i] + c[i] - 1) / c[i] * cost[i];
+        if (c[i] < tiles[i] && m > wm) { wm = m; worst = i; }
+      }
+      if (worst < 0) break;
+      ++c[worst];
+      ++used;
+    }
+    // worth it only when one problem leaves most of the machine idle on its own (<= 1/4 of the
+    // clusters' worth of tiles: the Llama-3.2-1B k / v wgrad, 16 tiles) and the grouped makespan
+    // beats the problems one after another (each on every cluster) plus ~10 k-step units per
+    // extra launch boundary; measured: 1B v linear -10 %, k neutral, while grouping the 1B q / o
+    // or the 8B k / v was slower (profiles/r02bl_gemm_group_ab.txt)
+    int64_t grouped_ms = 0, seq_ms = 10 * (n - 1);
+    bool starved = false;
+    for (int i = 0; i < n; ++i) {
+      grouped_ms = std::max<int64_t>(grouped_ms, (tiles[i] + c[i] - 1) / c[i] * cost[i]);
+      seq_ms += (tiles[i] + max_clusters - 1) / max_clusters * cost[i];
+      starved |= 4 * tiles[i] <= max_clusters;
+    }
+    if (grouped) *grouped = starved && grouped_ms < seq_ms;
+    if (grouped && !*grouped) return cudaSuccess;
+    grp.cl[0] = 0;
+    for (int i = 0; i < n; ++i) grp.cl[i + 1] = grp.cl[i] + int(c[i]);
+    clusters = used;
+  }
   return launch_k(kern, dim3(unsigned(CS * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, CS, tma, tmb, tsfa,
-                  tsfb, tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.M, a.N, a.K, a.oe,
-                  knob("ADAHOP_GEMM_PACE", kStorePace), 0, 0);   // pace: cycles per k-step between box stores (0: burst)
+                  tsfb, tmc, tma_c, a[0].C, a[0].out_f32 ? 1 : 0, a[0].ldc, a[0].M, a[0].N, a[0].K, a[0].oe,
+                  knob("ADAHOP_GEMM_PACE", kStorePace), 0, 0, grp);   // pace: cycles per k-step between box stores (0: burst)
+}
+
+template <int BN, int BUFS, int PM, int PN, int SPLIT = 1>
+static cudaError_t launch_2sm(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st, bool* fits = nullptr) {
+  return launch_2sm_n<BN, BUFS, PM, PN, SPLIT>(&a, 1, num_sms, st, fits);
 }
 
 #if ADAHOP_EXPERIMENTS
@@ -785,9 +901,13 @@ static cudaError_t launch_bf16_2sm_t(const Bf16GemmArgs& a, int num_sms, cudaStr
   const int64_t tiles = ((a.Mb + 255) / 256) * ((a.Nb + 255) / 256);
   const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
   const OePatch none{};
+  mxf4x2::GemmGroup grp;
+  memset(&grp, 0, sizeof(grp));
+  grp.n = 1;
+  grp.cl[1] = int(clusters);
   return launch_k(kern, dim3(unsigned(2 * clusters)), dim3(mxf4x2::kThreads), G::kSmem, st, 2, tma, tmb, tma, tmb,
                   tmc, tma_c, a.C, a.out_f32 ? 1 : 0, a.ldc, a.Mb, a.Nb, a.K, none,
-                  knob("ADAHOP_GEMM_PACE", kStorePace), a.a_mn, a.b_mn);
+                  knob("ADAHOP_GEMM_PACE", kStorePace), a.a_mn, a.b_mn, grp);
 }
 
 cudaError_t launch_gemm_bf16_2sm(const Bf16GemmArgs& a, int num_sms, cudaStream_t st, bool* launched) {
@@ -795,6 +915,15 @@ cudaError_t launch_gemm_bf16_2sm(const Bf16GemmArgs& a, int num_sms, cudaStream_
   if (a.mode != 0 || a.Mb <= 128 || knob("ADAHOP_BF16_2SM", 1) == 0) return cudaSuccess;
   *launched = true;
   return a.K >= 4096 ? launch_bf16_2sm_t<2>(a, num_sms, st) : launch_bf16_2sm_t<1>(a, num_sms, st);
+}
+
+// The n (2..3) MXFP4 GEMMs of one linear in one persistent launch (single accumulator), when the
+// estimated makespan beats separate launches; *launched = false: nothing launched.
+cudaError_t launch_gemm_mxf4_2sm_group(const Mxf4GemmArgs* a, int n, int num_sms, cudaStream_t st, bool* launched) {
+  *launched = false;
+  const cudaError_t e = launch_2sm_n<256, 1, 1, 1, 1, true>(a, n, num_sms, st, nullptr, launched);
+  if (e != cudaSuccess) *launched = false;
+  return e;
 }
 
 // Split-K over clusters of `split` pairs (2 or 4). *launched = false (and nothing launched) when

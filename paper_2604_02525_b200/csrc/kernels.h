@@ -186,6 +186,8 @@ cudaError_t launch_gemm_mxf4(const Mxf4GemmArgs& a, int num_sms, cudaStream_t st
 // gemm_mxf4_2sm.cu — CTA-pair (cta_group::2) version; variant = 128 (256x128 tiles, double-
 // buffered accumulators) or 256 (256x256 tiles, single accumulator).
 cudaError_t launch_gemm_mxf4_2sm(const Mxf4GemmArgs& a, int num_sms, int variant, cudaStream_t st);
+// 2..3 MXFP4 GEMMs (the paths of one linear) in one persistent launch, clusters split by work
+cudaError_t launch_gemm_mxf4_2sm_group(const Mxf4GemmArgs* a, int n, int num_sms, cudaStream_t st, bool* launched);
 // split-K over clusters of `split` CTA pairs for long-K GEMMs with few output tiles
 cudaError_t launch_gemm_mxf4_2sm_split(const Mxf4GemmArgs& a, int num_sms, int split, cudaStream_t st,
                                        bool* launched);
