@@ -99,7 +99,10 @@ int gemm_splitk() {
   return v;
 }
 
-cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
+// allow_splitk = false (the layer and split-step calls): one accumulation order per output for
+// every schedule, so that the split forward / backward stays bitwise equal to the layer call
+// whether or not either call groups its GEMMs (§6.4); those calls group a starving wgrad instead.
+cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st, bool allow_splitk = true) {
   int v = gemm_variant();
   if (v == 1 || a.M <= 128) return launch_gemm_mxf4(a, sms, st);
   // long-K GEMMs with fewer 256x256 tiles than half the CTA pairs (e.g. the Llama-3.2-1B k/v
@@ -110,7 +113,7 @@ cudaError_t run_gemm_mxf4(const Mxf4GemmArgs& a, int sms, cudaStream_t st) {
     // split-K over clusters of 4 (or 2) pairs, one 256x256 tile per cluster, partials summed in
     // distributed shared memory (e.g. 16 tiles x 4 pairs: 64 of the 74 pairs busy)
     const int force = gemm_splitk();
-    if (force != 0)
+    if (force != 0 && allow_splitk)
       for (int split = 4; split >= 2; split /= 2) {
         if (force > 1 ? split != force : split * tiles256 > sms / 2) continue;
         bool launched = false;
@@ -944,7 +947,7 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
   }
   if (!grouped) {
     for (int i = 0; i < ng; ++i) {
-      ADAHOP_LAUNCH(run_gemm_mxf4(group[i], sms, cs));
+      ADAHOP_LAUNCH(run_gemm_mxf4(group[i], sms, cs, false));
       launches += 1;
     }
   }
