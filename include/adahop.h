@@ -254,7 +254,10 @@ adahop_status_t adahop_linear_layer(const void* X, const void* W, const void* GY
  *                           Lv2 BF16 wgrad; adahop_linear_backward_needs_x tells the
  *                           caller whether it must keep X alive (pass NULL otherwise).
  * Results are bitwise those of adahop_linear_layer with the same arguments (same kernels, same
- * inputs). The context must not be modified between the two calls; W must be unchanged. Both
+ * inputs), except the k extracted rows of G_W (wgrad OE-Left) and of G_X (dgrad OE-Left): the layer
+ * call accumulates those outlier products in a quant pass (X's / W's), the split backward, which has
+ * neither pass, in a BF16 GEMM — two fp32 summation orders of the same products that agree to
+ * rounding (DESIGN R15). The context must not be modified between the two calls; W must be unchanged. Both
  * calls use the workspace size adahop_linear_split_workspace_bytes (scratch, may be shared). */
 size_t adahop_linear_ctx_bytes(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t* s,
                                const adahop_params_t* p);

@@ -223,6 +223,12 @@ bool or_left_enabled() {
   return on;
 }
 
+// ADAHOP_OR_DGRAD=0 (experiment builds): the dgrad's OE-Left product as a BF16 GEMM
+bool or_dgrad_enabled() {
+  static const bool on = knob("ADAHOP_OR_DGRAD", 1) != 0;
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = knob("ADAHOP_PDL", 1) != 0;
   return on;
@@ -643,6 +649,8 @@ struct LayerPlan {
   int or_kk = 0;                  // the wgrad's outlier product fused into a quant pass (0: not planned)
   int or_t = -1;                  // the streamed tensor: G_Y (OE-Right) or X (OE-Left, layer call only)
   Buf or_part, or_ticket;         // its per-(band, CTA) partials; the GEMM pre-fold's CTA count
+  int od_kk = 0;                  // the dgrad's OE-Left product fused into W's quant pass (layer call)
+  Buf od_part, od_ticket;
   int splits[3];
   int64_t npad[3], mbig[3];
   size_t ws_total = 0, ctx_total = 0;
@@ -736,6 +744,18 @@ void plan_layer(int64_t T, int64_t d_in, int64_t d_out, const adahop_strategy_t*
       take(L->or_ticket, 4, false);
     }
   }
+  // The dgrad's OE-Left product (A_out = G_Y[S, :], B = W^T stored: C_out = G_Y[S, :] W, eq:oe_left
+  // P:273) streams W, which the layer call quantises in both orientations: W's pass accumulates it
+  // with G_Y's row slice (gathered before the launch) as the product's second operand
+  if (or_fusion_enabled() && or_dgrad_enabled() && !split && s[1] == ADAHOP_OE_LEFT_IHT && p->oe_k > 0 &&
+      L->kk_row[2] > 0 && L->need_row[1] && L->need_col[1]) {
+    const size_t b = quant_tc_or_part_bytes(L->R[1], L->C[1], L->kk_row[2], sms);
+    if (b > 0) {
+      L->od_kk = L->kk_row[2];
+      take(L->od_part, b, false);
+      take(L->od_ticket, 4, false);
+    }
+  }
   L->ws_total = c[0].take(0) + 256;
   L->ctx_total = split ? c[1].take(0) + 256 : 0;
 }
@@ -804,15 +824,20 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
   // ---- 2. one quantisation pass per tensor (both orientations when both are consumed); the
   //         tensors that need both orientations share ONE persistent tensor-core launch
   QuantTcJob tc_jobs[3];
+  int tc_t[3];   // tensor of each tc job
   int n_tc = 0;
   bool in_tc[3] = {false, false, false};
+  // tensors quantised by the tensor-core pass: their OE slices are gathered before it (a fused
+  // product may only take its slice from such a tensor, or from the saved context)
+  bool will_tc[3];
+  for (int t = 0; t < 3; ++t)
+    will_tc[t] = (tensor_phase(t) & phases) && L.need_row[t] && L.need_col[t] && quant_use_tc() &&
+                 quant_tc_supported(L.R[t], L.C[t], L.C[t], src[t], L.kk_row[t] > 0, L.kk_col[t] > 0);
   for (int t = 0; t < 3; ++t) {
-    if (!(tensor_phase(t) & phases)) continue;
+    if (!will_tc[t]) continue;
     const int64_t R = L.R[t], C = L.C[t];
-    if (!(L.need_row[t] && L.need_col[t]) || !quant_use_tc() ||
-        !quant_tc_supported(R, C, C, src[t], L.kk_row[t] > 0, L.kk_col[t] > 0))
-      continue;
     in_tc[t] = true;
+    tc_t[n_tc] = t;
     tc_jobs[n_tc++] = QuantTcJob{
         src[t], R, C, C,
         L.kk_row[t] ? sp.p<const int32_t>(L.idx_row[t]) : nullptr, L.kk_row[t],
@@ -823,7 +848,7 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
         nullptr};
     // OE-Right's slice (X's columns) is in this call or the saved context; OE-Left's (G_Y's columns)
     // is gathered before this launch when G_Y is in it
-    if (t == L.or_t && L.or_kk > 0 && (t == 2 || (phases & tensor_phase(2)))) {
+    if (t == L.or_t && L.or_kk > 0 && (t == 2 ? !(phases & tensor_phase(0)) || will_tc[0] : will_tc[2])) {
       QuantTcJob& q = tc_jobs[n_tc - 1];
       q.or_slice = sp.p<const __nv_bfloat16>(L.slice_col[2 - t]);
       q.or_kk = L.or_kk;
@@ -831,15 +856,28 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
       q.or_part_bytes = quant_tc_or_part_bytes(R, C, L.or_kk, sms);
       q.or_ticket = sp.p<unsigned>(L.or_ticket);
     }
+    // the dgrad's OE-Left product in W's pass (G_Y's row slice is gathered before this launch)
+    if (t == 1 && L.od_kk > 0 && will_tc[2]) {
+      QuantTcJob& q = tc_jobs[n_tc - 1];
+      q.or_slice = sp.p<const __nv_bfloat16>(L.slice_row[2]);
+      q.or_kk = L.od_kk;
+      q.or_part = sp.p<float>(L.od_part);
+      q.or_part_bytes = quant_tc_or_part_bytes(R, C, L.od_kk, sms);
+      q.or_ticket = sp.p<unsigned>(L.od_ticket);
+    }
     if ((R % 128) || (C % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_row[t]), 0, size_t(sf_bytes(R, C)), cs));
     if ((C % 128) || (R % 256)) ADAHOP_LAUNCH(cudaMemsetAsync(sp.p<uint8_t>(L.sf_col[t]), 0, size_t(sf_bytes(C, R)), cs));
   }
-  bool or_fused = false;
+  bool fused_t[3] = {false, false, false};   // the tensor's pass carried its fused product
   if (n_tc) {
     int nl = 0;
-    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, sms, cs, &nl, &or_fused));
+    bool fj[3] = {false, false, false};
+    ADAHOP_LAUNCH(launch_quant_tc_multi(tc_jobs, n_tc, sms, cs, &nl, fj));
+    for (int i = 0; i < n_tc; ++i) fused_t[tc_t[i]] = fj[i];
     launches += nl;
   }
+  const bool or_fused = L.or_kk > 0 && L.or_t >= 0 && fused_t[L.or_t];
+  const bool od_fused = L.od_kk > 0 && fused_t[1];
   for (int t = 0; t < 3; ++t) {
     if (!(tensor_phase(t) & phases) || in_tc[t]) continue;
     const int64_t R = L.R[t], C = L.C[t];
@@ -888,6 +926,11 @@ adahop_status_t run_layer(int phases, const void* X, const void* W, const void* 
     if (path == 2 && or_fused) {   // the quant pass left the product's partials; the epilogue sums them
       patch[path] = quant_tc_or_patch(L.R[L.or_t], L.C[L.or_t], kk, sms, sp.p<const float>(L.or_part),
                                       sp.p<unsigned>(L.or_ticket), sp.p<float>(L.dt[path]), idx, left ? 2 : 1);
+      continue;
+    }
+    if (path == 1 && od_fused) {   // the dgrad's OE-Left product from W's pass (rows idx of G_X)
+      patch[path] = quant_tc_or_patch(L.R[1], L.C[1], kk, sms, sp.p<const float>(L.od_part),
+                                      sp.p<unsigned>(L.od_ticket), sp.p<float>(L.dt[path]), idx, 2);
       continue;
     }
     const __nv_bfloat16* slice = sp.p<const __nv_bfloat16>(col ? L.slice_col[t] : L.slice_row[t]);

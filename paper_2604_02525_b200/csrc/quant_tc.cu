@@ -22,8 +22,9 @@
 // B = H_32 (K-major, in smem). Accumulators (double-buffered, 2 x 256 TMEM columns) are
 // drained by 16 epilogue warps: 8 for row blocks (TMEM lane = tile row), 8 for column blocks
 // (TMEM lane = tile column). With the fused wgrad outlier product (kOr, see "Fused outlier
-// product" below) the ring is 3 stages deep, the Hadamard accumulator single-buffered and a
-// product accumulator occupies TMEM columns [256, 256 + npad).
+// product" below) the ring is 3 stages deep, the Hadamard accumulator single-buffered and the
+// product accumulators occupy TMEM columns [256 + 64 i, 256 + 64 i + npad) (up to two products
+// per launch: the wgrad's on G_Y's or X's tiles, the dgrad OE-Left's on W's).
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -210,42 +211,54 @@ struct OrSpec {
   unsigned* ticket;   // zeroed here; the MXFP4 GEMM's pre-fold counts its CTAs on it
   int dry;            // experiment builds (ADAHOP_OR_FUSED=3): the OR tile order without the product
 };
+constexpr int kMaxOr = 2;   // fused products per launch (the wgrad's and the dgrad OE-Left's)
 struct Jobs {
-  CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs], tor;
+  CUtensorMap tm[kMaxJobs], tqr[kMaxJobs], tqc[kMaxJobs], tor[kMaxOr];
   Job j[kMaxJobs];
-  int n, ntiles;   // jobs; plain tiles (every job but the OR job)
-  OrSpec orr;
+  int n, ntiles;   // jobs; plain tiles (every job but the OR jobs)
+  int nor;         // OR jobs: the last nor jobs of the launch, job n - nor + i carries orr[i]
+  OrSpec orr[kMaxOr];
 };
 struct TileRef {
   int jb, rt, ct;
   bool orr, first, last;   // an OR tile; first / last tile of its (band, CTA) segment
+  int oi;                  // its product (Jobs::orr index)
 };
 __device__ __forceinline__ int or_chunk_lo(const OrSpec& o, int b) { return int((int64_t(b) * o.n) / o.chunks); }
 // This CTA's tile sequence (the same in every role): plain tiles b, b + G, ... then its OR chunk.
 struct TileCursor {
-  int g, u, uend;   // next plain tile; next / end OR tile
+  int g, u, uend;   // next plain tile; next / end OR tile of product oi
   int lo;           // first OR tile of the chunk
+  int oi;           // product whose chunk is being walked
+  __device__ __forceinline__ void start(const Jobs& J) {
+    u = uend = lo = 0;
+    if (oi < J.nor && J.orr[oi].on && int(blockIdx.x) < J.orr[oi].chunks) {
+      lo = u = or_chunk_lo(J.orr[oi], int(blockIdx.x));
+      uend = or_chunk_lo(J.orr[oi], int(blockIdx.x) + 1);
+    }
+  }
   __device__ __forceinline__ explicit TileCursor(const Jobs& J) {
     g = int(blockIdx.x);
-    u = uend = lo = 0;
-    if (J.orr.on && int(blockIdx.x) < J.orr.chunks) {
-      lo = u = or_chunk_lo(J.orr, int(blockIdx.x));
-      uend = or_chunk_lo(J.orr, int(blockIdx.x) + 1);
-    }
+    oi = 0;
+    start(J);
   }
   __device__ __forceinline__ bool next(const Jobs& J, TileRef& t) {
     if (g < J.ntiles) {
-      const int nplain = J.n - (J.orr.on ? 1 : 0);
+      const int nplain = J.n - J.nor;
       int jb = 0;
       while (jb + 1 < nplain && g >= J.j[jb + 1].tile0) ++jb;
       const int lt0 = g - J.j[jb].tile0, ctiles = J.j[jb].ctiles;
-      t = TileRef{jb, lt0 / ctiles, lt0 % ctiles, false, false, false};
+      t = TileRef{jb, lt0 / ctiles, lt0 % ctiles, false, false, false, 0};
       g += int(gridDim.x);
       return true;
     }
-    if (u >= uend) return false;
-    const int rt = u % J.orr.rtiles;
-    t = TileRef{J.n - 1, rt, u / J.orr.rtiles, true, u == lo || rt == 0, u + 1 == uend || rt == J.orr.rtiles - 1};
+    while (u >= uend) {   // this product's chunk is done: the next product's
+      if (++oi >= J.nor) return false;
+      start(J);
+    }
+    const OrSpec& o = J.orr[oi];
+    const int rt = u % o.rtiles;
+    t = TileRef{J.n - J.nor + oi, rt, u / o.rtiles, true, u == lo || rt == 0, u + 1 == uend || rt == o.rtiles - 1, oi};
     ++u;
     return true;
   }
@@ -280,9 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   uint64_t* tempty = tfull + 2;        // [2]
   uint64_t* staged = tempty + 2;       // [2] epilogue warps -> store warp
   uint64_t* stgfree = staged + 2;      // [2] store warp -> epilogue warps
-  uint64_t* orfull = stgfree + 2;      // MMA -> flush warps: a segment's product is complete
-  uint64_t* orempty = orfull + 1;      // flush warps -> MMA: the product accumulator is drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(orempty + 1);
+  uint64_t* orfull = stgfree + 2;      // [kMaxOr] MMA -> flush warps: a segment's product is complete
+  uint64_t* orempty = orfull + kMaxOr; // [kMaxOr] flush warps -> MMA: the product accumulator is drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(orempty + kMaxOr);
   Mask* masks = reinterpret_cast<Mask*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [job][row, col]
   uint32_t* mbits = reinterpret_cast<uint32_t*>(masks + 2 * kMaxJobs);               // bitmaps (Out::bits_off)
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
@@ -295,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       if (kRow) ptx::prefetch_tmap(&J.tqr[jb]);
       if (kCol) ptx::prefetch_tmap(&J.tqc[jb]);
     }
-    if (kOr) ptx::prefetch_tmap(&J.tor);
+    if (kOr)
+      for (int o = 0; o < J.nor; ++o) ptx::prefetch_tmap(&J.tor[o]);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 2);   // MMA commit + OE-slice gather warp
@@ -306,8 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       ptx::mbar_init(&staged[b], kEpiWarps);
       ptx::mbar_init(&stgfree[b], 1);
     }
-    ptx::mbar_init(orfull, 1);
-    ptx::mbar_init(orempty, 4);       // the four warps of epilogue group 0
+    for (int o = 0; o < kMaxOr; ++o) {
+      ptx::mbar_init(&orfull[o], 1);
+      ptx::mbar_init(&orempty[o], 4);   // the four warps of epilogue group 0
+    }
     ptx::fence_barrier_init();
   }
   // H (n = j rows, k = i): core matrices of 8 rows x 16 bytes, (n/8, k/8) -> ((n/8)*4 + k/8)*128
@@ -327,13 +343,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       mask_build(&masks[2 * jb + 1], mbits + J.j[jb].ocol.bits_off, J.j[jb].ocol.zero, J.j[jb].ocol.nzero, J.j[jb].C);
   }
   // the previous user of the ticket (an earlier GEMM) has completed: griddep_wait above
-  if (kOr && J.orr.on && blockIdx.x == 0 && threadIdx.x == 0) *J.orr.ticket = 0u;
+  if (kOr && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int o = 0; o < J.nor; ++o)
+      if (J.orr[o].on) *J.orr[o].ticket = 0u;
   ptx::fence_proxy_async();  // H written by threads, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int npad = kOr ? J.orr.npad : 0;
 
   if (warp == 0 && lane < uint32_t(QTC_PROD_LANES)) {
     // ------------------------------------------------------------ TMA producer
@@ -345,7 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       QTC_T(0, i);
       uint8_t* dst = ring + stage * RG::kStage;
-      const bool o = kOr && t.orr && !J.orr.dry;
+      const bool o = kOr && t.orr && !J.orr[t.oi].dry;
+      const int npad = o ? J.orr[t.oi].npad : 0;
       if (lane == 0) ptx::mbar_arrive_expect_tx(&full[stage], kTile + (o ? 2 * npad * 128 : 0));
       if (QTC_PROD_LANES == 1 || lane == 0)
         ptx::tma_load_2d(dst, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128), int32_t(t.rt * 128));
@@ -353,8 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         ptx::tma_load_2d(dst + kBox, &J.tm[t.jb], &full[stage], int32_t(t.ct * 128 + 64), int32_t(t.rt * 128));
       if (o && lane == 0) {
         // the slice rows S[0, npad) x tile rows [128 rt, +128) as two 64-row K boxes (rows >= kk: zeros)
-        ptx::tma_load_2d(dst + kTile, &J.tor, &full[stage], int32_t(t.rt * 128), 0);
-        ptx::tma_load_2d(dst + kTile + npad * 128, &J.tor, &full[stage], int32_t(t.rt * 128 + 64), 0);
+        ptx::tma_load_2d(dst + kTile, &J.tor[t.oi], &full[stage], int32_t(t.rt * 128), 0);
+        ptx::tma_load_2d(dst + kTile + npad * 128, &J.tor[t.oi], &full[stage], int32_t(t.rt * 128 + 64), 0);
       }
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
@@ -364,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     const uint64_t bdesc = ptx::make_sdesc(ptx::smem_u32(hmat), 128, 512, 0);
     int stage = 0;
     uint32_t phase = 0;
-    int segs = 0;   // completed outlier-product segments
+    int segs[kMaxOr] = {0, 0};   // completed outlier-product segments per product
     TileRef t;
     TileCursor cur(J);
     for (int lt = 0; cur.next(J, t); ++lt) {
@@ -374,9 +392,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       QTC_T(1, lt);
       ptx::mbar_wait(&full[stage], phase);
       QTC_T(2, lt);
-      const bool o = kOr && t.orr && !J.orr.dry;
-      // a new segment reuses the product accumulator once the previous segment is flushed
-      if (o && t.first && segs > 0) ptx::mbar_wait(orempty, uint32_t((segs - 1) & 1));
+      const bool o = kOr && t.orr && !J.orr[t.oi].dry;
+      const int npad = o ? J.orr[t.oi].npad : 0;
+      const int sg = o ? segs[t.oi] : 0;
+      // a new segment reuses its product's accumulator once the previous segment is flushed
+      if (o && t.first && sg > 0) ptx::mbar_wait(&orempty[t.oi], uint32_t((sg - 1) & 1));
       ptx::tc_fence_after();
       const uint32_t base = ptx::smem_u32(ring + stage * RG::kStage);
       const uint32_t d0 = tmem_base + buf * 256;
@@ -408,15 +428,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           const uint64_t bor = ptx::make_sdesc(base + kTile, 16, 1024, 2);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            ptx::mma_bf16(tmem_base + kOrCol, acol + uint64_t((k * 16 * 128) >> 4),
+            ptx::mma_bf16(tmem_base + kOrCol + kOrMaxN * t.oi, acol + uint64_t((k * 16 * 128) >> 4),
                           bor + uint64_t(((k >> 2) * npad * 128 + (k & 3) * 32) >> 4), idesc_or(npad),
                           (t.first && k == 0) ? 0u : 1u);
         }
         ptx::tc_commit(&empty[stage]);
-        if (o && t.last) ptx::tc_commit(orfull);
+        if (o && t.last) ptx::tc_commit(&orfull[t.oi]);
       }
       __syncwarp();
-      if (o && t.last) ++segs;
+      if (o && t.last) ++segs[t.oi];
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 3) {
@@ -522,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     const uint32_t blk0 = sub * kBlocksPerGroup;
     const uint32_t oi = kRow ? orient : 0;     // staging slot of this orientation
     const uint32_t sw = (row >> 1) & 3;        // 64B swizzle of the staging row
-    int segs = 0;
+    int segs[kMaxOr] = {0, 0};
     TileRef t;
     TileCursor cur(J);
     for (int lt = 0; cur.next(J, t); ++lt) {
@@ -578,21 +598,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       ptx::fence_proxy_async();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&staged[sbuf]);
-      if (kOr && t.orr && t.last && !J.orr.dry) {
+      if (kOr && t.orr && t.last && !J.orr[t.oi].dry) {
         if (group == 0) {
           // flush the finished segment: P[c = 128 ct + row][j] -> its (band, CTA) partial slot
-          ptx::mbar_wait(orfull, uint32_t(segs & 1));
+          const OrSpec& os = J.orr[t.oi];
+          const int npad = os.npad;
+          const uint32_t pcol = kOrCol + kOrMaxN * t.oi;
+          ptx::mbar_wait(&orfull[t.oi], uint32_t(segs[t.oi] & 1));
           ptx::tc_fence_after();
           uint32_t p0[32], p1[32];
-          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + kOrCol, p0);
-          if (npad > 32) ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + kOrCol + 32, p1);
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + pcol, p0);
+          if (npad > 32) ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + pcol + 32, p1);
           ptx::tmem_ld_wait();
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(orempty);
-          const int u0 = ct * J.orr.rtiles;
-          const int slot = int(blockIdx.x) - or_chunk_of(J.orr, u0);
-          float* dst = J.orr.part + (int64_t(ct) * J.orr.spb + slot) * npad * 128 + row;
+          if (lane == 0) ptx::mbar_arrive(&orempty[t.oi]);
+          const int u0 = ct * os.rtiles;
+          const int slot = int(blockIdx.x) - or_chunk_of(os, u0);
+          float* dst = os.part + (int64_t(ct) * os.spb + slot) * npad * 128 + row;
           // lanes = consecutive columns: one 128-byte store per (warp, j)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -601,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           for (int j = 0; j < 32; ++j)
             if (32 + j < npad) dst[int64_t(32 + j) * 128] = __uint_as_float(p1[j]);
         }
-        ++segs;
+        ++segs[t.oi];
       }
     }
   }
@@ -630,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 static size_t quant_tc_smem(bool masks, int64_t bitmap_words, bool orr) {
   const size_t ring = orr ? size_t(qtc::Ring<true>::kStages) * qtc::Ring<true>::kStage
                           : size_t(qtc::Ring<false>::kStages) * qtc::Ring<false>::kStage;
-  return ring + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 160 +
+  return ring + 4 * qtc::kStg + 4 * 512 + qtc::kHBytes + 1024 + 176 +
          (masks ? 2 * qtc::kMaxJobs * sizeof(qtc::Mask) + size_t(bitmap_words) * 4 : 0);
 }
 constexpr size_t kSmemLimit = 232448;   // 227 KB per CTA on sm_100
@@ -696,7 +719,9 @@ static cudaError_t launch_tc(const qtc::Jobs& J, bool masks, int64_t bitmap_word
                                 int(quant_tc_smem_max(kOr)));
   });
   if (ae != cudaSuccess) return ae;
-  const int tiles = J.ntiles + (kOr ? J.orr.n : 0);
+  int tiles = J.ntiles;
+  if (kOr)
+    for (int o = 0; o < J.nor; ++o) tiles += J.orr[o].n;
   const unsigned grid = unsigned(tiles < num_sms ? tiles : num_sms);
   return launch_k(qtc::k_quant_tc<kRow, kCol, kHad, kOr>, dim3(grid), dim3(qtc::kThreads), smem, st, 1, J);
 }
@@ -778,34 +803,43 @@ static bool gather_after_quant() {
 
 cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms, cudaStream_t st, int* launches,
                                   bool* or_fused) {
-  if (or_fused) *or_fused = false;
+  if (or_fused)
+    for (int i = 0; i < n; ++i) or_fused[i] = false;
   if (n <= 0) return cudaSuccess;
   if (n > qtc::kMaxJobs) return cudaErrorInvalidValue;
   // The OE slices come from a separate gather (copying them inside the quant pipeline stalls
   // it), launched before the quant pass (see gather_after_quant for the measured alternative).
   const bool after = gather_after_quant();
   const bool fused = gather_fused() && !after;
-  // The fused outlier product (at most one job; its slice must exist before the launch, so not
-  // with the in-kernel gathers) runs on the dual-orientation kernel; its job goes last.
-  int or_in = -1;
-  for (int i = 0; i < n; ++i)
-    if (jobs_in[i].or_slice) {
-      if (or_in >= 0) return cudaErrorInvalidValue;
-      or_in = i;
-    }
-  bool orr = or_in >= 0 && !after && !fused && jobs_in[or_in].q_row && jobs_in[or_in].q_col &&
-             !jobs_in[or_in].had_row && !jobs_in[or_in].had_col && jobs_in[or_in].or_kk > 0 &&
-             jobs_in[or_in].or_kk <= qtc::kOrMaxN && jobs_in[or_in].or_ticket &&
-             jobs_in[or_in].or_part_bytes >= quant_tc_or_part_bytes(jobs_in[or_in].R, jobs_in[or_in].C,
-                                                                    jobs_in[or_in].or_kk, num_sms);
+  // The fused outlier products (up to kMaxOr jobs; their slices must exist before the launch, so
+  // not with the in-kernel gathers) run on the dual-orientation kernel; their jobs go last.
+  int or_in[qtc::kMaxOr], nor = 0;
+  bool orr = !after && !fused;
+  for (int i = 0; i < n; ++i) {
+    if (!jobs_in[i].or_slice) continue;
+    if (nor == qtc::kMaxOr) return cudaErrorInvalidValue;
+    or_in[nor++] = i;
+    const QuantTcJob& q = jobs_in[i];
+    orr &= q.q_row && q.q_col && !q.had_row && !q.had_col && q.or_kk > 0 && q.or_kk <= qtc::kOrMaxN && q.or_ticket &&
+           q.or_part_bytes >= quant_tc_or_part_bytes(q.R, q.C, q.or_kk, num_sms);
+  }
+  orr &= nor > 0;
+  auto is_or = [&](int i) {
+    for (int o = 0; o < nor; ++o)
+      if (or_in[o] == i) return true;
+    return false;
+  };
   QuantTcJob jobs[qtc::kMaxJobs];
+  int src[qtc::kMaxJobs];   // jobs_in index of jobs[m]
   int m = 0;
   for (int pass = 0; pass < (after ? 2 : 1); ++pass)
     for (int i = 0; i < n; ++i) {
       const bool colg = jobs_in[i].q_col && jobs_in[i].ncol_zero > 0 && jobs_in[i].slice_col;
-      if (orr ? i != or_in : (!after || colg == (pass == 1))) jobs[m++] = jobs_in[i];
+      if (orr ? !is_or(i) : (!after || colg == (pass == 1))) { src[m] = i; jobs[m++] = jobs_in[i]; }
     }
-  if (orr) jobs[m++] = jobs_in[or_in];
+  if (orr)
+    for (int o = 0; o < nor; ++o) { src[m] = or_in[o]; jobs[m++] = jobs_in[or_in[o]]; }
+  const int nor_l = orr ? nor : 0;   // OR jobs of this launch (the last nor_l)
   auto gathers = [&]() -> cudaError_t {
     for (int i = 0; i < n; ++i) {
       const QuantTcJob& q = jobs[i];
@@ -850,7 +884,7 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     jj.R = q.R; jj.C = q.C;
     jj.ctiles = int((q.C + 127) / 128);
     jj.tile0 = tiles;
-    if (!(orr && i == n - 1)) tiles += jj.ctiles * int((q.R + 127) / 128);
+    if (i < n - nor_l) tiles += jj.ctiles * int((q.R + 127) / 128);
     jj.kch_row = sf_kchunks(q.C);
     jj.kch_col = sf_kchunks(q.R);
     jj.orow = qtc::Out{q.q_row, q.sf_row, q.row_zero, row ? q.nrow_zero : 0, fused ? q.slice_row : nullptr, q.had_row, 0};
@@ -868,20 +902,26 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
     masks |= jj.orow.nzero > 0 || jj.ocol.nzero > 0;
   }
   J.ntiles = tiles;
-  if (orr) {
-    const QuantTcJob& q = jobs[n - 1];
-    J.orr = or_spec(q.R, q.C, q.or_kk, num_sms);
-    J.orr.part = q.or_part;
-    J.orr.ticket = q.or_ticket;
-    J.orr.dry = knob("ADAHOP_OR_FUSED", 1) == 3 ? 1 : 0;
+  J.nor = nor_l;
+  bool fits = quant_tc_smem(masks, words, true) <= kSmemLimit;
+  for (int o = 0; o < nor_l && fits; ++o) {
+    const QuantTcJob& q = jobs[n - nor_l + o];
+    J.orr[o] = or_spec(q.R, q.C, q.or_kk, num_sms);
+    J.orr[o].part = q.or_part;
+    J.orr[o].ticket = q.or_ticket;
+    J.orr[o].dry = knob("ADAHOP_OR_FUSED", 1) == 3 ? 1 : 0;
     // the slice S [kk][R] (R contiguous): boxes of 64 rows of T (128 B) x npad slice rows, OOB -> 0
-    if (quant_tc_smem(masks, words, true) > kSmemLimit ||
-        !make_tmap_2d(&J.tor, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q.or_slice, uint64_t(q.R), uint64_t(q.or_kk),
-                      uint64_t(q.R) * 2, 64, uint32_t(J.orr.npad), CU_TENSOR_MAP_SWIZZLE_128B)) {
-      // does not fit: the caller runs the BF16 outlier GEMM; the job becomes a plain one again
-      orr = false;
-      J.orr = qtc::OrSpec{};
-      J.ntiles = tiles + J.j[n - 1].ctiles * int((q.R + 127) / 128);
+    fits = make_tmap_2d(&J.tor[o], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q.or_slice, uint64_t(q.R), uint64_t(q.or_kk),
+                        uint64_t(q.R) * 2, 64, uint32_t(J.orr[o].npad), CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (orr && !fits) {
+    // does not fit: the caller runs the BF16 outlier GEMMs; the jobs become plain ones again
+    orr = false;
+    J.nor = 0;
+    for (int o = 0; o < qtc::kMaxOr; ++o) J.orr[o] = qtc::OrSpec{};
+    for (int o = 0; o < nor_l; ++o) {
+      const qtc::Job& jj = J.j[n - nor_l + o];
+      J.ntiles += jj.ctiles * int((jj.R + 127) / 128);
     }
   }
   if (!after && !fused) {
@@ -899,7 +939,8 @@ cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs_in, int n, int num_sms,
   else if (col) e = had ? launch_tc<false, true, true, false>(J, masks, words, num_sms, st)
                         : launch_tc<false, true, false, false>(J, masks, words, num_sms, st);
   if (e != cudaSuccess) return e;
-  if (orr && or_fused) *or_fused = true;
+  if (orr && or_fused)
+    for (int o = 0; o < nor_l; ++o) or_fused[src[n - nor_l + o]] = true;
   return after ? gathers() : cudaSuccess;
 }
 

@@ -518,8 +518,17 @@ def test_linear_layer_matches_paths_and_oracle(strats, shape):
     gx1 = ah.linear_dgrad(gd, wd, strats[1], p, out_dtype=torch.float32)
     gw1 = ah.linear_wgrad(gd, xd, strats[2], p, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    for a, b in ((y, y1), (gx, gx1)):
-        np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+    np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), y1.cpu().numpy().view(np.uint32))
+    # dgrad: bitwise, except that with OE-Left the layer call accumulates the outlier product
+    # G_Y[S, :] W in W's quant pass and the per-path call in a BF16 GEMM (DESIGN R15): the k
+    # extracted rows of G_X agree to rounding
+    a, b = gx.cpu().numpy(), gx1.cpu().numpy()
+    diff = a.view(np.uint32) != b.view(np.uint32)
+    if strats[1] == "OE_LEFT_IHT":
+        assert len(np.unique(np.nonzero(diff)[0])) <= 16
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    else:
+        assert not diff.any()
     # wgrad: the MXFP4 part is bitwise equal; with OE the layer call accumulates the outlier product
     # in a quant pass (G_Y's for OE-Right, X's for OE-Left) and the per-path call in a split-K BF16
     # GEMM, two fp32 summation orders of the same product (DESIGN R15), so the extracted

@@ -59,8 +59,16 @@ def test_split_equals_layer_and_oracle(strats, pats, level, shape):
     gx, gw = ah.linear_backward(gd, wd, ctx, gx_dtype=torch.float32, gw_dtype=torch.float32)
     torch.cuda.synchronize()
     assert ctx.needs_x == (strats[2] == "BF16" or strats[2] == "OE_LEFT_IHT")
-    for a, b in ((y, y_l), (gx, gx_l)):
-        np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+    np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), y_l.cpu().numpy().view(np.uint32))
+    a, b = gx.cpu().numpy(), gx_l.cpu().numpy()
+    if strats[1] == "OE_LEFT_IHT":
+        # the layer call accumulates the dgrad OE-Left product in W's quant pass, the split backward
+        # (no W pass) in a BF16 GEMM: the k extracted rows agree to rounding (DESIGN R15)
+        diff = a.view(np.uint32) != b.view(np.uint32)
+        assert len(np.unique(np.nonzero(diff)[0])) <= 16
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    else:
+        np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
     a, b = gw.cpu().numpy(), gw_l.cpu().numpy()
     if strats[2] == "OE_LEFT_IHT":
         # the layer call accumulates the wgrad OE-Left product in X's quant pass, the split backward
