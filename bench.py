@@ -260,6 +260,15 @@ def make_host_inputs(model, pats, tokens):
     return host
 
 
+def nccl_version():
+    try:
+        import torch
+        v = torch.cuda.nccl.version()
+        return ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:   # noqa: BLE001 - informational only
+        return None
+
+
 def config_dict(args, world):
     return {"workload": f"{args.workload}_layer_21gemm (7 linears x fwd/dgrad/wgrad)",
             "api": "adahop_linear_* per path" if args.per_path else "adahop_linear_layer (dual-orientation quant)",
@@ -267,7 +276,8 @@ def config_dict(args, world):
             "pairs": "CN NN RN RC NC CC (Table-1 census classes)", "oe_k": args.oe_k,
             "level": args.level, "hadamard_block": 32, "out_dtype": "bf16 (Y, G_X), fp32 (G_W)",
             "l2": "flushed between steps (256 MiB write, untimed)",
-            "parallelism": f"dp{world} token-sharded, NCCL all-reduce of wgrad" if world > 1 else "single GPU"}
+            "parallelism": f"dp{world} token-sharded, NCCL all-reduce of wgrad" if world > 1 else "single GPU",
+            **({"nccl": nccl_version()} if world > 1 else {})}
 
 
 # ------------------------------------------------------------------------------- GPU arm
@@ -294,6 +304,10 @@ def main():
         # of the sharding / reduction plumbing; NCCL needs one GPU per rank)
         backend = os.environ.get("ADAHOP_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init log (stderr) records the transport and whether NVLS / NVLink SHARP is
+            # used for the wgrad all-reduce; the JSON line is on stdout
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
