@@ -108,10 +108,12 @@ struct QuantTcJob {
   const __nv_bfloat16* or_slice = nullptr; int or_kk = 0; float* or_part = nullptr; size_t or_part_bytes = 0;
   unsigned* or_ticket = nullptr;   // 4 bytes, zeroed by the launch, counted by the GEMM pre-fold
 };
-// Up to 3 tensors in one persistent launch (same orientation set for all).
+// Up to 3 tensors in one persistent launch (same orientation set for all), up to two of them with
+// a fused outlier product (their or_slice complete before the launch).
 // OE slices are produced by a separate gather launch; *launches (nullable) counts every launch.
-// *or_fused (nullable) tells whether a job's outlier product was computed (else the caller runs
-// the BF16 outlier GEMM: the product is fused only on the dual-orientation kernel when it fits).
+// or_fused (nullable, n entries, indexed like jobs) tells whether a job's outlier product was
+// computed (else the caller runs the BF16 outlier GEMM: the products are fused only on the
+// dual-orientation kernel when they fit).
 cudaError_t launch_quant_tc_multi(const QuantTcJob* jobs, int n, int num_sms, cudaStream_t st, int* launches,
                                   bool* or_fused);
 size_t quant_tc_or_part_bytes(int64_t R, int64_t C, int kk, int num_sms);
